@@ -1,0 +1,108 @@
+"""Generate golden fixtures by running the REFERENCE package in this container.
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \
+        python tests/golden/make_golden.py
+
+The reference (/root/reference/pkg/src/bsattn, numpy + OpenBLAS) does not
+exist on the GPU box, so its outputs are committed here as small .npz files.
+Inputs are never stored: every case is regenerated from a numpy PCG64 seed
+exactly as the reference's own tests and bench do (bench.py:46-70,
+test_sparse.py:15-21): ``default_rng(seed).standard_normal((H, T, d))`` for
+q, k, v in that order, cast to float32.  ``tests/golden_inputs.py`` holds the
+shared regeneration code.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))  # tests/
+
+from golden_inputs import CASES_ATTN, CASES_SCORE, SCORE_POLICIES, make_qkv, sample_rows  # noqa: E402
+
+import bsattn  # noqa: E402  (the reference, via PYTHONPATH)
+from bsattn import (  # noqa: E402
+    AttentionInputs,
+    BlockGeometry,
+    MaskPolicy,
+    SparseAttentionJob,
+    TokenLayout,
+    patch_token_indices,
+    predict_mask,
+    sparse_attention,
+)
+from bsattn.maskpred import block_pool, pooled_scores, select_blocks  # noqa: E402
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def score_case(name, frames, patches, specials, heads, d, seed, block_q, block_k):
+    t0 = time.time()
+    lay = TokenLayout(frames, patches, specials)
+    q, k, _ = make_qkv(heads, lay.total_tokens, d, seed)
+    pidx = patch_token_indices(lay)
+    qp_in, kp_in = np.ascontiguousarray(q[:, pidx]), np.ascontiguousarray(k[:, pidx])
+    g = BlockGeometry(lay.patch_tokens, block_q, block_k)
+    qp = block_pool(qp_in, block_q)
+    kp = block_pool(kp_in, block_k)
+    probs = pooled_scores(qp, kp, d)
+    out = dict(
+        frames=frames, patches=patches, specials=specials, heads=heads, d=d, seed=seed,
+        block_q=block_q, block_k=block_k,
+        qp_sha=sha(qp), kp_sha=sha(kp), probs_sha=sha(probs),
+        probs_head0=probs[0, :16],
+        qp_head0=qp[0, :16], kp_head0=kp[0, :32],
+    )
+    for i, (tau, rho) in enumerate(SCORE_POLICIES):
+        m = select_blocks(probs, MaskPolicy(tau, rho, g)).blocks
+        out[f"mask{i}_bits"] = np.packbits(m.reshape(-1, m.shape[2]), axis=1, bitorder="little")
+        out[f"mask{i}_tau_rho"] = np.array([tau, rho])
+    np.savez_compressed(os.path.join(HERE, f"score_{name}.npz"), **out)
+    print(f"score_{name}: nq={g.nq_blocks} nk={g.nk_blocks} ({time.time() - t0:.1f}s)")
+
+
+def attn_case(name, frames, patches, specials, heads, d, seed, block_q, block_k, tau, rho,
+              full=True):
+    t0 = time.time()
+    lay = TokenLayout(frames, patches, specials)
+    q, k, v = make_qkv(heads, lay.total_tokens, d, seed)
+    pidx = patch_token_indices(lay)
+    g = BlockGeometry(lay.patch_tokens, block_q, block_k)
+    mask = predict_mask(q[:, pidx], k[:, pidx], MaskPolicy(tau, rho, g))
+    job = SparseAttentionJob(AttentionInputs(q, k, v), lay, mask)
+    o = sparse_attention(job, threads=os.cpu_count() or 1)
+    out = dict(
+        frames=frames, patches=patches, specials=specials, heads=heads, d=d, seed=seed,
+        block_q=block_q, block_k=block_k, tau=tau, rho=rho,
+        mask_bits=np.packbits(mask.blocks.reshape(-1, g.nk_blocks), axis=1, bitorder="little"),
+        out_sum=np.float64(o.astype(np.float64).sum()),
+        out_abs_sum=np.float64(np.abs(o.astype(np.float64)).sum()),
+    )
+    if full:
+        out["out"] = o
+    else:
+        rows = sample_rows(lay, block_q)
+        out["rows"] = rows
+        out["out_rows"] = o[:, rows]
+    np.savez_compressed(os.path.join(HERE, f"attn_{name}.npz"), **out)
+    print(f"attn_{name}: T={lay.total_tokens} ({time.time() - t0:.1f}s)")
+
+
+def main():
+    print("reference bsattn", bsattn.__version__, "numpy", np.__version__)
+    for c in CASES_SCORE:
+        score_case(**c)
+    for c in CASES_ATTN:
+        attn_case(**c)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,69 @@
+"""Seeded input regeneration shared by the golden generator and the tests.
+
+Inputs follow the reference's own generators (bench.py:46-70 bench_inputs,
+test_sparse.py:15-21 make_inputs): numpy PCG64 ``default_rng(seed)`` and
+``standard_normal((H, T, d)).astype(float32)`` for q, k, v in that order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+# (tau, rho) pairs checked bit-exactly on every scoring case.
+SCORE_POLICIES = [
+    (0.4, 0.8),    # README/SPEC example point, paper's 74.74% row
+    (0.0, 0.75),   # exact 25% density "S75"
+    (0.9, 0.5),
+    (0.97, 0.1),
+    (0.5, 1.0),    # pure CDF
+    (1.0, 1.0),    # tau = 1 edge
+]
+
+CASES_SCORE = [
+    # config 1 (N=8 VGGT frames, 16 heads, d64)
+    dict(name="cfg1", frames=8, patches=1369, specials=5, heads=16, d=64, seed=0,
+         block_q=128, block_k=64),
+    # N=100 frames, 2 heads (config 2 shapes)
+    dict(name="n100h2", frames=100, patches=1369, specials=5, heads=2, d=64, seed=0,
+         block_q=128, block_k=64),
+    # smaller geometries (probe where the numpy/OpenBLAS order model holds)
+    dict(name="f2p700", frames=2, patches=700, specials=5, heads=3, d=64, seed=7,
+         block_q=128, block_k=64),
+    dict(name="f3p500d32", frames=3, patches=500, specials=4, heads=2, d=32, seed=11,
+         block_q=64, block_k=32),
+]
+
+CASES_ATTN = [
+    dict(name="small_spec", frames=2, patches=300, specials=5, heads=2, d=64, seed=21,
+         block_q=128, block_k=64, tau=0.4, rho=0.8),
+    dict(name="small_nospec", frames=1, patches=777, specials=0, heads=2, d=64, seed=22,
+         block_q=128, block_k=64, tau=0.0, rho=0.75),
+    dict(name="small_d32", frames=3, patches=150, specials=3, heads=2, d=32, seed=23,
+         block_q=64, block_k=32, tau=0.9, rho=0.5),
+    dict(name="cfg1", frames=8, patches=1369, specials=5, heads=16, d=64, seed=0,
+         block_q=128, block_k=64, tau=0.4, rho=0.8, full=False),
+]
+
+
+def make_qkv(heads: int, tokens: int, d: int, seed: int):
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((heads, tokens, d)).astype(np.float32)
+    k = rng.standard_normal((heads, tokens, d)).astype(np.float32)
+    v = rng.standard_normal((heads, tokens, d)).astype(np.float32)
+    return q, k, v
+
+
+def sample_rows(layout, block_q: int) -> np.ndarray:
+    """Source-order rows covering specials, first/last q-blocks, ragged tail."""
+    f, p, s = layout.frames, layout.patches_per_frame, layout.specials_per_frame
+    per = p + s
+    rows = set()
+    for fr in (0, f // 2, f - 1):
+        for j in range(s):
+            rows.add(fr * per + j)
+    tp = f * p
+    for pi in list(range(0, 3)) + [block_q - 1, block_q, tp // 2, tp // 2 + 1] + \
+            list(range(max(0, tp - 70), tp, 7)) + [tp - 1]:
+        fr, loc = divmod(pi, p)
+        rows.add(fr * per + s + loc)
+    return np.array(sorted(rows), dtype=np.int64)
