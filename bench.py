@@ -1,0 +1,407 @@
+"""Benchmark: one block-sparse global-attention layer at VGGT shapes.
+
+Workload (BASELINE.json metric "global-attn ms/layer & frames/s at N=200"):
+N=200 frames x 1374 tokens (5 specials + 1369 patches, 518^2), 16 heads x
+d64, bf16 Q/K/V resident in HBM, synthetic Gaussian data (seeded).  One step =
+the whole hot path of one layer through the public API:
+    predict_mask (pool -> pooled QK^T -> softmax -> CDF/top-k select)
+  + sparse_attention (pack, LPT schedule, tcgen05 block-sparse FA forward).
+Policy: tau=0, rho=0.75 (exact 25% block density, the paper's S75 point).
+
+Arms:
+  default            our B200 path; prints one JSON line (rank 0).
+  --impl reference   the reference's CPU algorithm (oracle/ restatement:
+                     C scoring + numpy BLAS attention) on the host cores, on a
+                     bounded sample of the same workload, extrapolated to a
+                     full layer.
+
+Multi-GPU (torchrun, NCCL): every rank runs its own independent layer
+(replicas of the per-GPU workload: "scaling": "weak"); no collective on the
+data path; timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+P_PER_FRAME, S_PER_FRAME = 1369, 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=200)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--dim", type=int, default=64)
+    ap.add_argument("--tau", type=float, default=0.0)
+    ap.add_argument("--rho", type=float, default=0.75)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense SDPA baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def workload_config(a, extra=None):
+    T = a.frames * (P_PER_FRAME + S_PER_FRAME)
+    cfg = {
+        "workload": f"VGGT global attention, N={a.frames} frames x 1374 tok (518^2), "
+                    f"{a.heads} heads x d{a.dim}, tau={a.tau} rho={a.rho}",
+        "frames": a.frames, "tokens": T, "heads": a.heads, "head_dim": a.dim,
+        "block_q": 128, "block_k": 64, "tau": a.tau, "rho": a.rho,
+        "l2": "inputs larger than L2 (3 x %.2f GB bf16 Q/K/V vs 126 MB L2)" %
+              (a.heads * T * a.dim * 2 / 1e9),
+        "parallelism": f"replicas x{a.gpus} (one independent layer per GPU, no collective)",
+    }
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_07120_b200 as bsa
+    from paper_2509_07120_b200 import sparse as sp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    lay = bsa.TokenLayout(a.frames, P_PER_FRAME, S_PER_FRAME)
+    T, H, d = lay.total_tokens, a.heads, a.dim
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    pol = bsa.MaskPolicy(a.tau, a.rho, g)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(a.seed + 1000 * rank)
+    q, k, v = (torch.randn((H, T, d), generator=gen, device=dev, dtype=torch.float32)
+               .to(torch.bfloat16) for _ in range(3))
+
+    def step(qq, kk, vv, timing=False):
+        mask = bsa.predict_mask(qq, kk, pol, layout=lay)
+        job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
+        return bsa.sparse_attention(job, timing=timing), mask
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        out, mask = step(q, k, v)
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(a.steps):
+            out, mask = step(q, k, v)
+        e1.record(stream)
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / a.steps
+
+    # stage split + live kernel time of the dominant (tensor-core) kernel,
+    # CUDA events on the launching stream, averaged over `steps` launches
+    score_ms, kern_ms = [], []
+    for _ in range(a.steps):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        mask = bsa.predict_mask(q, k, pol, layout=lay)
+        s1.record(stream)
+        job = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask)
+        bsa.sparse_attention(job, timing=True)
+        kern_ms.append(sp.last_kernel_ms())
+        score_ms.append(s0.elapsed_time(s1))
+    kernel_ms = float(np.mean(kern_ms))
+    area = mask.selected_area().astype(np.int64)
+    Ts, Tp = lay.special_tokens, lay.patch_tokens
+    # algorithmic work: 2 GEMMs (QK^T, PV) x 2 flop/MAC over allowed entries
+    flops = int(sum(4 * d * (Ts * T + Tp * Ts + int(ar)) for ar in area))
+    dense_flops = 4 * d * T * T * H
+    density = float(area.sum()) / float(H * Tp * Tp)
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
+    peak_src = "measured burst cuBLAS bf16 (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks else \
+        "fallback 1.59 PF/s (B200_PROFILING.md)"
+    achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
+
+    # dense baseline on the same GPU: library SDPA (cuDNN / flash) in bf16
+    dense_ms = None
+    dense_backend = None
+    if not a.no_dense and rank == 0:
+        import torch.nn.functional as F
+        qb, kb, vb = (t.unsqueeze(0) for t in (q, k, v))
+        try:
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+            backends = [(SDPBackend.CUDNN_ATTENTION, "cudnn"), (SDPBackend.FLASH_ATTENTION, "flash"),
+                        (SDPBackend.EFFICIENT_ATTENTION, "mem_efficient")]
+        except ImportError:
+            backends = []
+        best = None
+        for be, name in backends:
+            try:
+                with sdpa_kernel([be]):
+                    F.scaled_dot_product_attention(qb, kb, vb)
+                    torch.cuda.synchronize()
+                    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    d0.record(stream)
+                    for _ in range(2):
+                        F.scaled_dot_product_attention(qb, kb, vb)
+                    d1.record(stream)
+                    torch.cuda.synchronize()
+                    t = d0.elapsed_time(d1) / 2
+                if best is None or t < best[0]:
+                    best = (t, name)
+            except Exception:  # backend unavailable for these shapes
+                continue
+        if best:
+            dense_ms, dense_backend = best
+
+    # end to end through the public API with host buffers (pinned): H2D of
+    # Q/K/V, scoring + attention, D2H of the full output, every step
+    e2e = None
+    if not a.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        hout = torch.empty((H, T, d), dtype=torch.bfloat16).pin_memory()
+
+        def e2e_step():
+            dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
+            o, _ = step(dq, dk, dv)
+            hout.copy_(o, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(a.steps):
+            e2e_step()
+        x1.record(stream)
+        barrier()
+        e2e_ms = x0.elapsed_time(x1) / a.steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": a.frames * world / (e2e_ms * 1e-3), "unit": "frames/s",
+               "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 3 * H * T * d * 2, "d2h_bytes_per_step": H * T * d * 2}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_reference(a, budget_s=a.cpu_budget_s)
+
+    if rank == 0:
+        line = {
+            "metric": "global-attn frames/s at N=200 (one layer, 518^2, 16x d64), bf16",
+            "value": a.frames * world / (ms_step * 1e-3),
+            "unit": "frames/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_step,
+            "ms_per_layer": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded Gaussian Q/K/V, VGGT token layout)",
+            "config": workload_config(a, {"block_density": density}),
+            "stages_ms": {"predict_mask": float(np.mean(score_ms)),
+                          "attention_kernel": kernel_ms},
+            "dense_baseline": {"ms_per_layer": dense_ms, "backend": dense_backend,
+                               "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None},
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": None,
+                         "kernel": "bsa_tc_kernel", "algorithmic_flops_per_launch": flops,
+                         "dense_flops": dense_flops, "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": 10 * a.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+def cpu_reference(a, budget_s=20.0):
+    """Reference CPU path on a bounded sample, extrapolated to one layer:
+    scoring of one head over the full sequence, attention of a sample of
+    q-block rows (plus the special rows) of one head; x heads."""
+    import oracle
+
+    threads = oracle.host_threads()
+    lay_T = a.frames * (P_PER_FRAME + S_PER_FRAME)
+    Tp, Ts = a.frames * P_PER_FRAME, a.frames * S_PER_FRAME
+    rng = np.random.default_rng(a.seed)
+    q, k, v = (rng.standard_normal((1, lay_T, a.dim), dtype=np.float32) for _ in range(3))
+    pidx = oracle.patch_indices(a.frames, P_PER_FRAME, S_PER_FRAME)
+    t0 = time.perf_counter()
+    mask, _ = oracle.predict_mask(q[:, pidx], k[:, pidx], 128, 64, a.tau, a.rho)
+    t_score = time.perf_counter() - t0
+    nq = mask.shape[1]
+    perm, _ = oracle.partition_perm(a.frames, P_PER_FRAME, S_PER_FRAME)
+    qp, kp, vp = q[:, perm], k[:, perm], v[:, perm]
+    # attention sample: q-blocks spread over the sequence, run until the budget
+    sample = list(range(0, nq, max(1, nq // 64)))
+    done, t_attn = 0, 0.0
+    t_start = time.perf_counter()
+    chunk = max(1, threads)
+    while done < len(sample) and (time.perf_counter() - t_start) < budget_s * 0.6:
+        items = [(0, qb) for qb in sample[done:done + chunk]]
+        t1 = time.perf_counter()
+        oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, S_PER_FRAME, mask, 128, 64,
+                                     threads=threads, inputs_permuted=True, work=items)
+        t_attn += time.perf_counter() - t1
+        done += len(items)
+    per_qblock = t_attn / max(done, 1)
+    # special rows: 256-row chunk sample over all keys
+    t2 = time.perf_counter()
+    rows = min(Ts, 256)
+    s = (qp[0, :rows] @ kp[0].T) * np.float32(1 / np.sqrt(a.dim))
+    s -= s.max(axis=1, keepdims=True)
+    np.exp(s, out=s)
+    s /= s.sum(axis=1, keepdims=True)
+    _ = s @ vp[0]
+    t_spec = (time.perf_counter() - t2) * (Ts / max(rows, 1))
+    per_head_s = t_score + per_qblock * nq + t_spec
+    layer_s = per_head_s * a.heads
+    return {
+        "value": a.frames / layer_s, "unit": "frames/s", "cores": threads,
+        "kind": "port", "ms_per_layer": layer_s * 1e3,
+        "sample": f"1 of {a.heads} heads: full scoring ({t_score:.2f}s), {done} of {nq} patch "
+                  f"q-blocks ({t_attn:.2f}s, numpy BLAS, {threads} threads), {rows} of {Ts} "
+                  f"special rows; extrapolated x{nq}/{done} q-blocks and x{a.heads} heads",
+    }
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per = []
+    cpu = None
+    for i in range(a.warmup + a.steps):
+        res = cpu_reference(a, budget_s=max(4.0, 60.0 / max(1, a.warmup + a.steps)))
+        if i >= a.warmup:
+            per.append(res["ms_per_layer"])
+            cpu = res
+    ms = float(np.median(per))
+    value = a.frames / (ms * 1e-3)
+    line = {
+        "impl": "reference",
+        "metric": "global-attn frames/s at N=200 (one layer, 518^2, 16x d64), bf16",
+        "value": value, "unit": "frames/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "ms_per_layer": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded Gaussian Q/K/V, VGGT token layout)",
+        "config": workload_config(a),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cpu["cores"],
+                         "kind": "port", "sample": cpu["sample"]},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * bsa.h -- C ABI of the B200-native block-sparse global-attention library
+ * (libbsa.so, sm_100a).  Plain pointers and sizes only: no torch, no CUDA
+ * types.  Streams are passed as `void*` (a cudaStream_t); all device memory,
+ * including workspace, is owned and allocated by the caller.
+ *
+ * Every entry point replaces one operator of the reference package `bsattn`
+ * (/root/reference/pkg/src/bsattn, the Python API re-exported by
+ * __init__.py:8-59).  The reference has no FFI; its operator boundary is the
+ * Python call, so the binding a maintainer adds is a ctypes stub (see
+ * INTEGRATION.md) and the Python mirror paper_2509_07120_b200/ keeps the
+ * reference's names, argument meaning and ValueError behaviour.
+ *
+ * Conventions
+ *   - Asynchronous on `stream`; no host synchronisation; re-entrant.
+ *   - Return codes: BSA_OK, BSA_EINVAL (bad argument -> ValueError in Python),
+ *     BSA_EUNSUPPORTED (valid but not implemented on this device path),
+ *     BSA_ECUDA (CUDA error -> RuntimeError).  bsa_last_error() gives a
+ *     thread-local message for the last failure.
+ *   - Tensors are (heads, tokens, dim) with unit stride on dim.
+ *   - Block masks use the reference .bsm row layout (maskpred.py:17-19): one
+ *     bitset per (head, query block) row, ceil(nk/8) bytes, LSB-first.
+ */
+#ifndef BSA_H_
+#define BSA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSA_OK 0
+#define BSA_EINVAL 1
+#define BSA_EUNSUPPORTED 2
+#define BSA_ECUDA 3
+
+#define BSA_F32 0
+#define BSA_BF16 1
+
+/* attention path selection (bsa_sparse_attention `flags`) */
+#define BSA_PATH_AUTO 0     /* tcgen05 kernel when bf16/d64/128x64, else SIMT */
+#define BSA_PATH_SIMT 1     /* force the CUDA-core kernel (fp32 math)        */
+#define BSA_PATH_TC 2       /* require the tcgen05 kernel (EUNSUPPORTED if not) */
+#define BSA_FLAG_TIMING 16  /* bracket the attention kernel with CUDA events */
+
+/* TokenLayout (layout.py:27-66): F frames of S specials + P patches. */
+typedef struct {
+  int64_t frames;
+  int64_t patches_per_frame;
+  int64_t specials_per_frame;
+  int32_t specials_first; /* 1: [s0..sS-1, p0..pP-1] per frame (layout.py:35) */
+} bsa_layout;
+
+/* (heads, tokens, dim) device tensor, dim contiguous; strides in elements. */
+typedef struct {
+  const void* data;
+  int32_t dtype; /* BSA_F32 | BSA_BF16 */
+  int64_t heads, tokens, dim;
+  int64_t stride_head, stride_token;
+} bsa_tensor;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int bsa_version(void);
+/* Message for the last failing call on this thread ("" if none). */
+const char* bsa_last_error(void);
+/* Number of SMs of the current device (for persistent grids / sharding). */
+int bsa_device_sm_count(void);
+
+/* ------------------------------------------------------------------ */
+/* Scoring stage                                                      */
+/* ------------------------------------------------------------------ */
+
+/* block_pool (maskpred.py:104-120).  Mean over token blocks of `block` rows,
+ * ragged tail over its true length, reference fp32 summation order.
+ * If `patch_gather` is non-NULL, `x` holds the full interleaved sequence
+ * (tokens == layout total) and only its patch rows are pooled, in patch order
+ * (the caller's patch_token_indices gather, README:127-128, folded into the
+ * addressing).  out: (heads, ceil(n/block), dim) fp32 contiguous. */
+int bsa_block_pool(const bsa_tensor* x, const bsa_layout* patch_gather, int32_t block,
+                   float* out, void* stream);
+
+/* pooled_scores (maskpred.py:123-139 + tensorio.py:73-87): per head
+ * row_softmax(qp @ kp^T, scale).  qp (H,nq,d), kp (H,nk,d), probs (H,nq,nk),
+ * all fp32 contiguous.  Bit-exact with the reference's numpy/OpenBLAS order.
+ * ws: bsa_pooled_scores_workspace() bytes. */
+size_t bsa_pooled_scores_workspace(int64_t heads, int64_t nq, int64_t nk);
+int bsa_pooled_scores(const float* qp, const float* kp, int64_t heads, int64_t nq, int64_t nk,
+                      int64_t dim, float scale, float* probs, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* row_softmax (tensorio.py:73-87): out = softmax(a * scale) per row of a
+ * (rows, cols) fp32 matrix, reference arithmetic (numpy exp, pairwise sum). */
+int bsa_row_softmax(const float* a, int64_t rows, int64_t cols, float scale, float* out,
+                    void* stream);
+
+/* select_blocks (maskpred.py:142-174).  probs (H,nq,nk) fp32 contiguous ->
+ * mask_bits (H*nq rows of ceil(nk/8) bytes) and counts[H*nq] (selected
+ * blocks per row).  k_floor = MaskPolicy.min_blocks (maskpred.py:52-57),
+ * computed by the caller.  ws: bsa_select_workspace() bytes. */
+size_t bsa_select_workspace(int64_t heads, int64_t nq, int64_t nk);
+int bsa_select_blocks(const float* probs, int64_t heads, int64_t nq, int64_t nk, double tau,
+                      int64_t k_floor, uint8_t* mask_bits, int32_t* counts, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* predict_mask (maskpred.py:177-194): pool -> score -> select in one call.
+ * q,k: patch-only (H,Tp,d) when patch_gather == NULL, else full interleaved
+ * sequences described by patch_gather.  probs_out (H,nq,nk) fp32 is
+ * optional (NULL to skip).  ws: bsa_predict_mask_workspace() bytes. */
+size_t bsa_predict_mask_workspace(int64_t heads, int64_t patch_tokens, int64_t dim,
+                                  int32_t block_q, int32_t block_k);
+int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* patch_gather,
+                     int32_t block_q, int32_t block_k, float scale, double tau,
+                     int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Attention stage                                                    */
+/* ------------------------------------------------------------------ */
+
+/* sparse_attention (sparse.py:157-205).  q,k,v: (H,T,d) in interleaved
+ * source order (or [specials|patches] order when inputs_permuted != 0).
+ * out: (H,T,d) contiguous, out_dtype BSA_F32|BSA_BF16, same order as the
+ * inputs.  Special query rows attend every key; patch query rows attend all
+ * special keys plus the key blocks set in their mask row, ascending.
+ * `counts` may be NULL (recomputed on device).  `shard`/`num_shards` split
+ * the LPT-ordered work list for multi-GPU runs (0/1 = everything); rows of
+ * other shards are not written.  ws: bsa_sparse_attention_workspace(). */
+size_t bsa_sparse_attention_workspace(const bsa_layout* layout, int64_t heads, int64_t dim,
+                                      int32_t block_q, int32_t block_k, int32_t in_dtype,
+                                      int32_t inputs_permuted, int32_t flags);
+int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                         void* out, int32_t out_dtype, const bsa_layout* layout,
+                         int32_t block_q, int32_t block_k, const uint8_t* mask_bits,
+                         const int32_t* counts, float scale, int32_t inputs_permuted,
+                         int32_t shard, int32_t num_shards, int32_t flags, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* Device time (ms) of the last tensor-core attention kernel launched on this
+ * host thread with BSA_FLAG_TIMING set (waits for it); -1 on error. */
+float bsa_last_kernel_ms(void);
+
+/* Which path bsa_sparse_attention would take for these arguments:
+ * BSA_PATH_SIMT or BSA_PATH_TC (or <0 on invalid arguments). */
+int bsa_sparse_attention_path(const bsa_layout* layout, int64_t dim, int32_t block_q,
+                              int32_t block_k, int32_t in_dtype, int32_t flags);
+
+/* Selected patch-patch area per head (BlockMask.selected_area,
+ * maskpred.py:97-101), int64[heads]: sum of |q block| * |k block| over set
+ * bits with ragged tails weighted by their true length. */
+int bsa_mask_selected_area(const uint8_t* mask_bits, int64_t heads, int64_t patch_tokens,
+                           int32_t block_q, int32_t block_k, int64_t* area_out,
+                           void* stream);
+
+/* CSR view of a mask: row_ptr[H*nq+1] (int32, exclusive scan of per-row
+ * counts) and col_idx (int32, ascending key blocks per row). */
+int bsa_mask_to_csr(const uint8_t* mask_bits, int64_t heads, int64_t nq, int64_t nk,
+                    int32_t* row_ptr, int32_t* col_idx, void* ws, size_t ws_bytes,
+                    void* stream);
+size_t bsa_mask_to_csr_workspace(int64_t heads, int64_t nq);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSA_H_ */

@@ -53,6 +53,8 @@ def lib():
         vp = ctypes.c_void_p
         L.oracle_np_expf.argtypes = [f32]
         L.oracle_np_expf.restype = f32
+        L.oracle_pairwise_sum.argtypes = [vp, i64]
+        L.oracle_pairwise_sum.restype = f32
         L.oracle_block_pool.argtypes = [vp, i64, i64, i64, i64, vp]
         L.oracle_pooled_scores.argtypes = [vp, vp, i64, i64, i64, i64, f32, vp]
         L.oracle_select_blocks.argtypes = [vp, i64, i64, i64, f64, i64, vp, vp]

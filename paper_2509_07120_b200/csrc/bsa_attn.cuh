@@ -1,0 +1,114 @@
+// bsa_attn.cuh -- geometry and key-stream helpers shared by the attention kernels.
+#pragma once
+
+#include "bsa_common.cuh"
+
+namespace bsa {
+
+// Attention geometry in partitioned order: [specials (Ts) | patches (Tp)].
+struct AttnGeom {
+  Layout L;
+  int64_t H, T, Ts, Tp;
+  int d;
+  int64_t bq, bk, nq, nk, mask_row_bytes;
+  __host__ __device__ int64_t simt_tiles_per_head() const {
+    return ceil_div(Ts, 32) + nq * ceil_div(bq, 32);
+  }
+};
+
+inline AttnGeom make_geom(const Layout& L, int64_t H, int d, int64_t bq, int64_t bk) {
+  AttnGeom G;
+  G.L = L;
+  G.H = H;
+  G.T = L.tokens();
+  G.Ts = L.n_spec();
+  G.Tp = L.n_patch();
+  G.d = d;
+  G.bq = bq;
+  G.bk = bk;
+  G.nq = ceil_div(G.Tp, bq);
+  G.nk = ceil_div(G.Tp, bk);
+  G.mask_row_bytes = ceil_div(G.nk, 8);
+  return G;
+}
+
+// Key stream of one query row group, as chunks of <= CH consecutive
+// partitioned-order keys: special query rows (qb < 0) see [0, T); patch
+// q-block rows see the special strip [0, Ts) and then each selected key
+// block ascending (sparse.py:101-119, :122-131).
+struct KeyChunker {
+  int64_t Ts, Tp, T, bk, nk;
+  const uint8_t* row;   // mask row bits (nullptr for special rows)
+  int CH;
+  int phase;            // 0: contiguous range, 1: mask blocks, 2: done
+  int64_t pos, end;     // current contiguous range [pos, end)
+  int64_t byte_idx;     // mask iteration
+  unsigned int cur;     // remaining bits of the current byte
+  __device__ KeyChunker(const AttnGeom& G, int64_t qb, const uint8_t* mask_row, int ch)
+      : Ts(G.Ts), Tp(G.Tp), T(G.T), bk(G.bk), nk(G.nk), row(qb < 0 ? nullptr : mask_row),
+        CH(ch), phase(0), pos(0), end(qb < 0 ? G.T : G.Ts), byte_idx(-1), cur(0) {}
+
+  // next selected key block (>= 0) or -1
+  __device__ __forceinline__ int64_t next_block() {
+    while (cur == 0) {
+      ++byte_idx;
+      if (byte_idx * 8 >= nk) return -1;
+      cur = row[byte_idx];
+    }
+    const int b = __ffs(cur) - 1;
+    cur &= cur - 1;
+    return byte_idx * 8 + b;
+  }
+
+  __device__ __forceinline__ bool next(int64_t& start, int& len) {
+    while (true) {
+      if (pos < end) {
+        start = pos;
+        const int64_t n = end - pos;
+        len = (int)(n < CH ? n : CH);
+        pos += len;
+        return true;
+      }
+      if (phase == 0 && row) {
+        phase = 1;
+      }
+      if (phase == 1) {
+        const int64_t kb = next_block();
+        if (kb < 0) { phase = 2; return false; }
+        pos = Ts + kb * bk;
+        const int64_t e = (kb + 1) * bk;
+        end = Ts + (e < Tp ? e : Tp);
+        continue;
+      }
+      phase = 2;
+      return false;
+    }
+  }
+};
+
+int launch_simt_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                          void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
+                          int permuted, float scale, int shard, int num_shards, cudaStream_t st);
+
+struct TcArgs {
+  const __nv_bfloat16* qp;   // packed partitioned (H, T, 64)
+  const __nv_bfloat16* kp;
+  const __nv_bfloat16* vp;
+  void* out;
+  int out_bf16;
+  int permuted_out;          // write rows in partitioned order
+  const uint8_t* bits;
+  const int32_t* counts;     // per (h, qb) selected blocks
+  const int32_t* items;      // LPT-ordered work items
+  int32_t n_items;
+  int32_t* work_counter;
+  float scale_log2;          // scale * log2(e)
+  int shard, num_shards;
+  int timing;                // record events around the launch (bsa_last_kernel_ms)
+};
+
+int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);
+cudaEvent_t timing_events(int which);
+size_t tc_smem_bytes();
+
+}  // namespace bsa

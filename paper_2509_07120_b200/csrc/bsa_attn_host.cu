@@ -1,0 +1,358 @@
+// bsa_attn_host.cu -- attention-stage entry points of the C ABI, plus the
+// small device passes around the attention kernels:
+//   pack_kernel      source order (f32|bf16, any strides) -> contiguous bf16
+//                    [specials | patches] order (layout.py:113-132), the TMA
+//                    operand layout of the tcgen05 kernel.
+//   counts_kernel    per-row popcount of the .bsm bitsets.
+//   schedule_kernel  per head, an LPT (longest-first) counting sort of the
+//                    work items (special-row tiles, patch q-blocks) by their
+//                    key-tile count; heads stay contiguous so the K/V of one
+//                    head stay L2-resident while the SMs drain it.
+//   area_kernel      BlockMask.selected_area (maskpred.py:97-101).
+//   csr kernels      CSR view of the mask.
+#include <algorithm>
+
+#include "bsa_attn.cuh"
+
+namespace bsa {
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <typename T>
+__global__ void pack_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int64_t H,
+                            int64_t ntok, int d, Layout L, int permuted,
+                            __nv_bfloat16* __restrict__ out) {
+  // one thread per 8 output elements (d % 8 == 0)
+  const int64_t per_row = d / 8;
+  const int64_t total = H * ntok * per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c8 = i % per_row;
+    const int64_t hr = i / per_row;
+    const int64_t r = hr % ntok, h = hr / ntok;
+    const int64_t src = permuted ? r : L.part_src(r);
+    const T* p = x + h * sH + src * sT + c8 * 8;
+    float v[8];
+    if constexpr (sizeof(T) == 4) {
+      const float4 a = *reinterpret_cast<const float4*>(p);
+      const float4 b = *reinterpret_cast<const float4*>(p + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      uint4 o;
+      __nv_bfloat162 t;
+      t = __floats2bfloat162_rn(v[0], v[1]); o.x = *reinterpret_cast<uint32_t*>(&t);
+      t = __floats2bfloat162_rn(v[2], v[3]); o.y = *reinterpret_cast<uint32_t*>(&t);
+      t = __floats2bfloat162_rn(v[4], v[5]); o.z = *reinterpret_cast<uint32_t*>(&t);
+      t = __floats2bfloat162_rn(v[6], v[7]); o.w = *reinterpret_cast<uint32_t*>(&t);
+      *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = o;
+    } else {
+      *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = *reinterpret_cast<const uint4*>(p);
+    }
+  }
+}
+
+__global__ void counts_kernel(const uint8_t* __restrict__ bits, int64_t rows, int64_t row_bytes,
+                              int32_t* __restrict__ counts) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint8_t* b = bits + r * row_bytes;
+  int c = 0;
+  for (int64_t i = 0; i < row_bytes; ++i) c += __popc((unsigned)b[i]);
+  counts[r] = c;
+}
+
+// items per head: nst special tiles (rows of 128) then nq patch q-blocks
+__global__ void __launch_bounds__(1024)
+    schedule_kernel(const int32_t* __restrict__ counts, int64_t nq, int64_t nst, int64_t nsc,
+                    int64_t spec_cost, int64_t max_cost, int32_t* __restrict__ items) {
+  extern __shared__ int32_t hist[];  // max_cost + 1 bins
+  const int64_t h = blockIdx.x;
+  const int64_t M = nst + nq;
+  for (int64_t c = threadIdx.x; c <= max_cost; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const int64_t cost = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
+    atomicAdd(&hist[min(cost, max_cost)], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t run = 0;  // descending cost: longest first
+    for (int64_t c = max_cost; c >= 0; --c) {
+      const int32_t n = hist[c];
+      hist[c] = run;
+      run += n;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const int64_t cost = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
+    const int32_t pos = atomicAdd(&hist[min(cost, max_cost)], 1);
+    items[h * M + pos] = (int32_t)(h * M + i);
+  }
+}
+
+__global__ void area_kernel(const uint8_t* __restrict__ bits, int64_t H, int64_t nq, int64_t nk,
+                            int64_t row_bytes, int64_t tp, int64_t bq, int64_t bk,
+                            unsigned long long* __restrict__ area) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= H * nq) return;
+  const int64_t h = r / nq, qb = r % nq;
+  const uint8_t* b = bits + r * row_bytes;
+  int64_t c = 0;
+  for (int64_t i = 0; i < row_bytes; ++i) c += __popc((unsigned)b[i]);
+  const int64_t last = nk - 1;
+  const bool last_sel = (b[last >> 3] >> (last & 7)) & 1;
+  const int64_t ktail = tp - last * bk;
+  const int64_t keys = c * bk - (last_sel ? (bk - ktail) : 0);
+  const int64_t qsz = min(bq, tp - qb * bq);
+  atomicAdd(&area[h], (unsigned long long)(keys * qsz));
+}
+
+__global__ void __launch_bounds__(1024) csr_scan_kernel(const int32_t* __restrict__ counts,
+                                                        int64_t rows, int32_t* __restrict__ row_ptr) {
+  __shared__ int64_t part[1024];
+  const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = threadIdx.x * per, b1 = min(rows, b0 + per);
+  int64_t s = 0;
+  for (int64_t i = b0; i < b1; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int64_t t = part[i];
+      part[i] = run;
+      run += t;
+    }
+    row_ptr[rows] = (int32_t)run;
+  }
+  __syncthreads();
+  int64_t run = part[threadIdx.x];
+  for (int64_t i = b0; i < b1; ++i) {
+    row_ptr[i] = (int32_t)run;
+    run += counts[i];
+  }
+}
+
+__global__ void csr_fill_kernel(const uint8_t* __restrict__ bits, int64_t rows, int64_t row_bytes,
+                                int64_t nk, const int32_t* __restrict__ row_ptr,
+                                int32_t* __restrict__ col_idx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint8_t* b = bits + r * row_bytes;
+  int32_t o = row_ptr[r];
+  for (int64_t i = 0; i < row_bytes; ++i) {
+    unsigned v = b[i];
+    while (v) {
+      const int t = __ffs(v) - 1;
+      v &= v - 1;
+      const int64_t kb = i * 8 + t;
+      if (kb < nk) col_idx[o++] = (int32_t)kb;
+    }
+  }
+}
+
+static int check_qkv(const bsa_tensor* t, const char* name) {
+  if (!t || !t->data) return fail(BSA_EINVAL, "%s: null tensor", name);
+  if (t->dtype != BSA_F32 && t->dtype != BSA_BF16)
+    return fail(BSA_EINVAL, "%s: unsupported dtype code %d", name, t->dtype);
+  if (t->heads < 1 || t->tokens < 1 || t->dim < 1)
+    return fail(BSA_EINVAL, "%s has a zero-sized dimension", name);
+  return BSA_OK;
+}
+
+static int choose_path(const AttnGeom& G, int32_t in_dtype, int32_t flags) {
+  flags &= 0xF;  // path bits; BSA_FLAG_* live above
+  const bool tc_ok = in_dtype == BSA_BF16 && G.d == 64 && G.bq == 128 && G.bk == 64 &&
+                     G.T < (1LL << 31) && G.H < 65536;
+  if (flags == BSA_PATH_SIMT) return BSA_PATH_SIMT;
+  if (flags == BSA_PATH_TC) return tc_ok ? BSA_PATH_TC : -BSA_EUNSUPPORTED;
+  return tc_ok ? BSA_PATH_TC : BSA_PATH_SIMT;
+}
+
+struct TcWorkspace {
+  __nv_bfloat16 *qp, *kp, *vp;
+  int32_t *items, *counter, *counts;
+  size_t bytes;
+};
+
+static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G) {
+  TcWorkspace w;
+  char* p = (char*)base;
+  const size_t tens = align_up((size_t)(G.H * G.T * G.d) * 2, 256);
+  const int64_t nst = ceil_div(G.Ts, 128);
+  const int64_t n_items = G.H * (nst + G.nq);
+  w.qp = (__nv_bfloat16*)p; p += tens;
+  w.kp = (__nv_bfloat16*)p; p += tens;
+  w.vp = (__nv_bfloat16*)p; p += tens;
+  w.items = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
+  w.counter = (int32_t*)p; p += 256;
+  w.counts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq) * 4, 256);
+  w.bytes = (size_t)(p - (char*)base);
+  return w;
+}
+
+static int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
+                       cudaStream_t st) {
+  const int64_t total = G.H * G.T * (G.d / 8);
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  const bool bf = x->dtype == BSA_BF16;
+  const size_t es = bf ? 2 : 4;
+  if ((uintptr_t)x->data % 16 || (x->stride_token * es) % 16 || (x->stride_head * es) % 16)
+    return fail(BSA_EUNSUPPORTED, "q/k/v must be 16-byte aligned for the tensor-core path");
+  if (bf)
+    pack_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x->data,
+                                                     x->stride_head, x->stride_token, G.H, G.T,
+                                                     G.d, G.L, permuted, out);
+  else
+    pack_kernel<float><<<grid, 256, 0, st>>>((const float*)x->data, x->stride_head,
+                                             x->stride_token, G.H, G.T, G.d, G.L, permuted, out);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+}  // namespace bsa
+
+using namespace bsa;
+
+extern "C" {
+
+int bsa_sparse_attention_path(const bsa_layout* layout, int64_t dim, int32_t block_q,
+                              int32_t block_k, int32_t in_dtype, int32_t flags) {
+  if (!layout || dim < 1 || block_q < 1 || block_k < 1) return -BSA_EINVAL;
+  const AttnGeom G = make_geom(to_layout(layout), 1, (int)dim, block_q, block_k);
+  return choose_path(G, in_dtype, flags);
+}
+
+size_t bsa_sparse_attention_workspace(const bsa_layout* layout, int64_t heads, int64_t dim,
+                                      int32_t block_q, int32_t block_k, int32_t in_dtype,
+                                      int32_t inputs_permuted, int32_t flags) {
+  (void)inputs_permuted;
+  if (!layout || heads < 1 || dim < 1 || block_q < 1 || block_k < 1) return 0;
+  const AttnGeom G = make_geom(to_layout(layout), heads, (int)dim, block_q, block_k);
+  if (choose_path(G, in_dtype, flags) != BSA_PATH_TC) return 256;
+  return tc_ws_layout(nullptr, G).bytes + 256;
+}
+
+int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                         void* out, int32_t out_dtype, const bsa_layout* layout,
+                         int32_t block_q, int32_t block_k, const uint8_t* mask_bits,
+                         const int32_t* counts, float scale, int32_t inputs_permuted,
+                         int32_t shard, int32_t num_shards, int32_t flags, void* ws,
+                         size_t ws_bytes, void* stream) {
+  int rc = check_qkv(q, "q");
+  if (!rc) rc = check_qkv(k, "k");
+  if (!rc) rc = check_qkv(v, "v");
+  if (rc) return rc;
+  if (!layout || !out || !mask_bits) return fail(BSA_EINVAL, "sparse_attention: null pointer");
+  if (q->heads != k->heads || q->heads != v->heads || q->tokens != k->tokens ||
+      q->tokens != v->tokens || q->dim != k->dim || q->dim != v->dim)
+    return fail(BSA_EINVAL, "q/k/v shapes differ");
+  if (q->dtype != k->dtype || q->dtype != v->dtype)
+    return fail(BSA_EINVAL, "q/k/v dtypes differ");
+  if (out_dtype != BSA_F32 && out_dtype != BSA_BF16)
+    return fail(BSA_EINVAL, "unsupported output dtype %d", out_dtype);
+  const Layout L = to_layout(layout);
+  if (L.frames < 1 || L.P < 1 || L.S < 0) return fail(BSA_EINVAL, "invalid layout");
+  if (q->tokens != L.tokens())
+    return fail(BSA_EINVAL, "inputs have %lld tokens but layout describes %lld",
+                (long long)q->tokens, (long long)L.tokens());
+  if (block_q < 1 || block_k < 1) return fail(BSA_EINVAL, "block sizes must be >= 1");
+  if (num_shards < 1) num_shards = 1;
+  if (shard < 0 || shard >= num_shards) return fail(BSA_EINVAL, "shard %d of %d", shard, num_shards);
+  const AttnGeom G = make_geom(L, q->heads, (int)q->dim, block_q, block_k);
+  const int path = choose_path(G, q->dtype, flags);
+  if (path < 0)
+    return fail(BSA_EUNSUPPORTED,
+                "tensor-core path needs bf16 inputs, head_dim 64, block_q 128, block_k 64");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (path == BSA_PATH_SIMT)
+    return launch_simt_attention(q, k, v, out, out_dtype, G, mask_bits, inputs_permuted, scale,
+                                 shard, num_shards, st);
+
+  // ---------------- tensor-core path ----------------
+  if (!ws) return fail(BSA_EINVAL, "sparse_attention: workspace required");
+  TcWorkspace W = tc_ws_layout(ws, G);
+  if (ws_bytes < W.bytes) return fail(BSA_EINVAL, "sparse_attention: workspace too small");
+  rc = launch_pack(q, G, inputs_permuted, W.qp, st);
+  if (!rc) rc = launch_pack(k, G, inputs_permuted, W.kp, st);
+  if (!rc) rc = launch_pack(v, G, inputs_permuted, W.vp, st);
+  if (rc) return rc;
+  const int64_t rows = G.H * G.nq;
+  if (!counts) {
+    counts_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(mask_bits, rows,
+                                                                 G.mask_row_bytes, W.counts);
+    BSA_LAUNCH_CHECK();
+    counts = W.counts;
+  }
+  const int64_t nst = ceil_div(G.Ts, 128);
+  const int64_t nsc = ceil_div(G.Ts, 64);
+  const int64_t spec_cost = (ceil_div(G.T, 64) + 1) / 2;
+  const int64_t max_cost = std::max<int64_t>(spec_cost, (nsc + G.nk + 1) / 2);
+  const size_t hsmem = (size_t)(max_cost + 1) * 4;
+  if (hsmem > 200 * 1024) return fail(BSA_EUNSUPPORTED, "sequence too long for the scheduler");
+  BSA_CUDA_TRY(cudaFuncSetAttribute(schedule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)hsmem));
+  schedule_kernel<<<(unsigned)G.H, 1024, hsmem, st>>>(counts, G.nq, nst, nsc, spec_cost, max_cost,
+                                                      W.items);
+  BSA_LAUNCH_CHECK();
+  BSA_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 4, st));
+  TcArgs a;
+  a.qp = W.qp;
+  a.kp = W.kp;
+  a.vp = W.vp;
+  a.out = out;
+  a.out_bf16 = out_dtype == BSA_BF16;
+  a.permuted_out = inputs_permuted;
+  a.bits = mask_bits;
+  a.counts = counts;
+  a.items = W.items;
+  a.n_items = (int32_t)(G.H * (nst + G.nq));
+  a.work_counter = W.counter;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.shard = shard;
+  a.num_shards = num_shards;
+  a.timing = (flags & BSA_FLAG_TIMING) != 0;
+  return launch_tc_attention(G, a, st);
+}
+
+int bsa_mask_selected_area(const uint8_t* mask_bits, int64_t heads, int64_t patch_tokens,
+                           int32_t block_q, int32_t block_k, int64_t* area_out, void* stream) {
+  if (!mask_bits || !area_out || heads < 1 || patch_tokens < 1 || block_q < 1 || block_k < 1)
+    return fail(BSA_EINVAL, "mask_selected_area: invalid argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nq = ceil_div(patch_tokens, block_q), nk = ceil_div(patch_tokens, block_k);
+  BSA_CUDA_TRY(cudaMemsetAsync(area_out, 0, (size_t)heads * 8, st));
+  const int64_t rows = heads * nq;
+  area_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(
+      mask_bits, heads, nq, nk, ceil_div(nk, 8), patch_tokens, block_q, block_k,
+      (unsigned long long*)area_out);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+size_t bsa_mask_to_csr_workspace(int64_t heads, int64_t nq) {
+  return align_up((size_t)(heads * nq) * 4, 256);
+}
+
+int bsa_mask_to_csr(const uint8_t* mask_bits, int64_t heads, int64_t nq, int64_t nk,
+                    int32_t* row_ptr, int32_t* col_idx, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (!mask_bits || !row_ptr || !col_idx || !ws || heads < 1 || nq < 1 || nk < 1)
+    return fail(BSA_EINVAL, "mask_to_csr: invalid argument");
+  if (ws_bytes < bsa_mask_to_csr_workspace(heads, nq))
+    return fail(BSA_EINVAL, "mask_to_csr: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows = heads * nq, rb = ceil_div(nk, 8);
+  int32_t* counts = (int32_t*)ws;
+  counts_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(mask_bits, rows, rb, counts);
+  BSA_LAUNCH_CHECK();
+  csr_scan_kernel<<<1, 1024, 0, st>>>(counts, rows, row_ptr);
+  BSA_LAUNCH_CHECK();
+  csr_fill_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, st>>>(mask_bits, rows, rb, nk, row_ptr,
+                                                                 col_idx);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,633 @@
+// bsa_attn_tc.cu -- block-sparse FlashAttention forward on 5th-gen tensor cores.
+//
+// Replaces the reference kernel /root/reference/pkg/src/bsattn/sparse.py:101-205
+// (special strip + selected 64-token key blocks per 128-row query block,
+// online softmax) for bf16 inputs, head_dim 64, block_q 128, block_k 64.
+//
+// Persistent, warp-specialised CTA (one per SM, 192 threads):
+//   warp 4      producer: fetches LPT-ordered work items (atomic counter),
+//               TMA-loads the 128x64 Q tile and, per 128-key tile, two
+//               64-token K chunks and two V chunks (any two selected blocks,
+//               gathered by coordinates) into a 4-stage SW128 smem ring.
+//   warp 5      MMA issuer (one thread): S = Q K^T (tcgen05.mma kind::f16,
+//               M=128, N=128|64, fp32 accumulate in TMEM, double buffered)
+//               and O += P V with P read straight from TMEM (A operand),
+//               V from smem (MN-major B operand); tcgen05.commit -> mbarriers.
+//   warps 0-3   softmax / correction / epilogue: thread t owns query row t
+//               (TMEM lane t): tcgen05.ld the S row, mask ragged chunks, exp2
+//               with lazy (threshold 2^8) rescaling of O in TMEM, bf16 P back
+//               to TMEM via tcgen05.st, final O / l to global memory in the
+//               caller's (interleaved) token order.
+// TMEM: S0|S1 (2x128 cols) P0|P1 (2x64) O (64) = 448 of 512 columns.
+#include <cuda.h>
+
+#include "bsa_attn.cuh"
+
+namespace bsa {
+namespace tc {
+
+constexpr int BQ = 128, CH = 64, D = 64, NST = 4;
+constexpr int Q_BYTES = BQ * D * 2;          // 16 KB
+constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB
+constexpr int KV_BYTES = 2 * CHUNK_BYTES;    // 16 KB per K (or V) stage
+constexpr int NUM_THREADS = 192;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr int OFF_V = OFF_K + NST * KV_BYTES;
+constexpr int OFF_BAR = OFF_V + NST * KV_BYTES;
+constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
+
+constexpr uint32_t TM_S = 0, TM_P = 256, TM_O = 384;
+
+// barrier slots (8 bytes each) inside the barrier region
+enum {
+  B_QFULL = 0,          // [2]
+  B_QEMPTY = 2,         // [2]
+  B_KFULL = 4,          // [NST]
+  B_VFULL = 4 + NST,    // [NST]
+  B_KVEMPTY = 4 + 2 * NST,  // [NST]
+  B_SFULL = 4 + 3 * NST,    // [2]
+  B_SEMPTY = B_SFULL + 2,   // [2]
+  B_PFULL = B_SEMPTY + 2,   // [2]
+  B_PFREE = B_PFULL + 2,    // [2]
+  B_OFULL = B_PFREE + 2,    // [1]
+  B_OEMPTY = B_OFULL + 1,   // [1]
+  B_IFULL = B_OEMPTY + 1,   // [2]
+  B_IEMPTY = B_IFULL + 2,   // [2]
+  B_COUNT = B_IEMPTY + 2
+};
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// ties later uses of tcgen05.ld results to after tcgen05.wait::ld
+__device__ __forceinline__ void reg_fence16(uint32_t* r) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
+}
+__device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
+  tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// UMMA shared-memory descriptor: SWIZZLE_128B, version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor kind::f16: bf16 x bf16 -> f32
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------------------
+// work item decoding
+// ---------------------------------------------------------------------------
+struct Item {
+  int64_t h;
+  int64_t qb;      // -1 for a special-row tile
+  int64_t row0;    // first partitioned query row
+  int rows;        // valid query rows
+  int nchunks;     // 64-key chunks in the key stream
+  int last_len;    // length of the final chunk (ragged tails)
+  int nsc;         // leading contiguous chunks (special strip / all keys)
+  int spec_last;   // length of the last contiguous chunk
+};
+
+__device__ __forceinline__ Item decode(const AttnGeom& G, int32_t code, const int32_t* counts,
+                                       const uint8_t* bits) {
+  Item it;
+  const int64_t nst = ceil_div(G.Ts, BQ);
+  const int64_t M = nst + G.nq;
+  it.h = code / M;
+  const int64_t li = code % M;
+  if (li < nst) {
+    it.qb = -1;
+    it.row0 = li * BQ;
+    it.rows = (int)min((int64_t)BQ, G.Ts - it.row0);
+    it.nsc = (int)ceil_div(G.T, CH);
+    it.spec_last = (int)(G.T - (int64_t)(it.nsc - 1) * CH);
+    it.nchunks = it.nsc;
+    it.last_len = it.spec_last;
+  } else {
+    it.qb = li - nst;
+    it.row0 = G.Ts + it.qb * BQ;
+    it.rows = (int)min((int64_t)BQ, G.Tp - it.qb * BQ);
+    it.nsc = (int)ceil_div(G.Ts, CH);
+    it.spec_last = it.nsc ? (int)(G.Ts - (int64_t)(it.nsc - 1) * CH) : CH;
+    const int cnt = counts[it.h * G.nq + it.qb];
+    it.nchunks = it.nsc + cnt;
+    // ragged last patch block, if selected, is always the final chunk
+    const int64_t lastb = G.nk - 1;
+    const uint8_t lb = bits[(it.h * G.nq + it.qb) * G.mask_row_bytes + (lastb >> 3)];
+    const bool last_sel = (lb >> (lastb & 7)) & 1;
+    it.last_len = last_sel ? (int)(G.Tp - lastb * CH) : CH;
+    if (cnt == 0) it.last_len = it.spec_last;
+  }
+  return it;
+}
+
+__device__ __forceinline__ int chunk_len(const Item& it, int c) {
+  if (c < it.nsc - 1) return CH;
+  if (c == it.nsc - 1) return it.nchunks == it.nsc ? it.last_len : it.spec_last;
+  return c == it.nchunks - 1 ? it.last_len : CH;
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  volatile int32_t* item_ring = (volatile int32_t*)(smem + OFF_BAR + 8 * B_COUNT);
+  uint32_t* tmem_holder = (uint32_t*)(smem + OFF_BAR + 8 * B_COUNT + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(BAR(B_QFULL + i), 1);
+      mbar_init(BAR(B_QEMPTY + i), 1);
+      mbar_init(BAR(B_SFULL + i), 1);
+      mbar_init(BAR(B_SEMPTY + i), 4);
+      mbar_init(BAR(B_PFULL + i), 4);
+      mbar_init(BAR(B_PFREE + i), 1);
+      mbar_init(BAR(B_IFULL + i), 1);
+      mbar_init(BAR(B_IEMPTY + i), 5);
+    }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(BAR(B_KFULL + s), 1);
+      mbar_init(BAR(B_VFULL + s), 1);
+      mbar_init(BAR(B_KVEMPTY + s), 1);
+    }
+    mbar_init(BAR(B_OFULL), 1);
+    mbar_init(BAR(B_OEMPTY), 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 4 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  const int64_t n_work =
+      A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards : A.n_items;
+
+  if (warp == 4) {
+    // ======================= producer =======================
+    if (lane == 0) {
+      uint32_t it = 0, g = 0;
+      while (true) {
+        const int64_t w = atomicAdd(A.work_counter, 1);
+        int32_t code = -1;
+        if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
+        const uint32_t slot = it & 1;
+        mbar_wait(BAR(B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
+        item_ring[slot] = code;
+        mbar_arrive(BAR(B_IFULL + slot));
+        if (code < 0) break;
+        const Item I = decode(G, code, A.counts, A.bits);
+        mbar_wait(BAR(B_QEMPTY + slot), ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(BAR(B_QFULL + slot), Q_BYTES);
+        tma_load_3d(sbase + OFF_Q + slot * Q_BYTES, &tm_q, BAR(B_QFULL + slot), 0, (int)I.row0,
+                    (int)I.h);
+        const uint8_t* mrow =
+            I.qb >= 0 ? A.bits + (I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
+        KeyChunker ck(G, I.qb, mrow, CH);
+        const int ntiles = (I.nchunks + 1) >> 1;
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const uint32_t st = g % NST;
+          mbar_wait(BAR(B_KVEMPTY + st), ((g / NST) & 1) ^ 1);
+          int64_t s0, s1 = -1;
+          int l0, l1 = 0;
+          ck.next(s0, l0);
+          const bool two = (2 * j + 1) < I.nchunks;
+          if (two) ck.next(s1, l1);
+          const uint32_t bytes = two ? KV_BYTES : CHUNK_BYTES;
+          const uint32_t kdst = sbase + OFF_K + st * KV_BYTES;
+          const uint32_t vdst = sbase + OFF_V + st * KV_BYTES;
+          mbar_expect_tx(BAR(B_KFULL + st), bytes);
+          tma_load_3d(kdst, &tm_k, BAR(B_KFULL + st), 0, (int)s0, (int)I.h);
+          if (two) tma_load_3d(kdst + CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s1, (int)I.h);
+          mbar_expect_tx(BAR(B_VFULL + st), bytes);
+          tma_load_3d(vdst, &tm_v, BAR(B_VFULL + st), 0, (int)s0, (int)I.h);
+          if (two) tma_load_3d(vdst + CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, (int)s1, (int)I.h);
+        }
+        ++it;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      uint32_t it = 0, g = 0;
+      const uint32_t id_s128 = idesc_bf16(128, 128, 0), id_s64 = idesc_bf16(128, 64, 0);
+      const uint32_t id_pv = idesc_bf16(128, 64, 1);
+      while (true) {
+        const uint32_t slot = it & 1;
+        mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
+        const int32_t code = item_ring[slot];
+        mbar_arrive(BAR(B_IEMPTY + slot));
+        if (code < 0) break;
+        const Item I = decode(G, code, A.counts, A.bits);
+        const int ntiles = (I.nchunks + 1) >> 1;
+        mbar_wait(BAR(B_QFULL + slot), (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qaddr = sbase + OFF_Q + slot * Q_BYTES;
+        auto issue_pv = [&](uint32_t gg, int jj) {
+          const uint32_t st = gg % NST, pb = gg & 1;
+          const bool two = (2 * jj + 1) < I.nchunks;
+          mbar_wait(BAR(B_PFULL + pb), (gg >> 1) & 1);
+          mbar_wait(BAR(B_VFULL + st), (gg / NST) & 1);
+          if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t vaddr = sbase + OFF_V + st * KV_BYTES;
+          const int ksteps = two ? 8 : 4;
+          for (int k = 0; k < ksteps; ++k) {
+            const uint64_t bd = sdesc(vaddr + k * 2048, 8192, 1024);
+            mma_ts(tmem + TM_O, tmem + TM_P + pb * 64 + k * 8, bd, id_pv,
+                   (jj > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(BAR(B_PFREE + pb));
+          tc_commit(BAR(B_KVEMPTY + st));
+        };
+        for (int j = 0; j < ntiles; ++j) {
+          const uint32_t gg = g + j;
+          const uint32_t st = gg % NST, sb = gg & 1;
+          const bool two = (2 * j + 1) < I.nchunks;
+          mbar_wait(BAR(B_KFULL + st), (gg / NST) & 1);
+          mbar_wait(BAR(B_SEMPTY + sb), ((gg >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t kaddr = sbase + OFF_K + st * KV_BYTES;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint64_t ad = sdesc(qaddr + k * 32, 16, 1024);
+            const uint64_t bd = sdesc(kaddr + k * 32, 16, 1024);
+            mma_ss(tmem + TM_S + sb * 128, ad, bd, two ? id_s128 : id_s64, k > 0 ? 1u : 0u);
+          }
+          tc_commit(BAR(B_SFULL + sb));
+          if (j == ntiles - 1) tc_commit(BAR(B_QEMPTY + slot));
+          if (j > 0) issue_pv(gg - 1, j - 1);
+        }
+        issue_pv(g + ntiles - 1, ntiles - 1);
+        tc_commit(BAR(B_OFULL));
+        g += ntiles;
+        ++it;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= softmax warps 0..3 =======================
+    const int row = threadIdx.x;  // TMEM lane == query row in the tile
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const float sl2 = A.scale_log2;
+    const float NEG_INF = -__int_as_float(0x7f800000);
+    uint32_t it = 0, g = 0;
+    while (true) {
+      const uint32_t slot = it & 1;
+      mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
+      const int32_t code = item_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(BAR(B_IEMPTY + slot));
+      if (code < 0) break;
+      const Item I = decode(G, code, A.counts, A.bits);
+      const int ntiles = (I.nchunks + 1) >> 1;
+      float m = NEG_INF, l = 0.0f;
+      for (int j = 0; j < ntiles; ++j) {
+        const uint32_t gg = g + j, sb = gg & 1;
+        const int len0 = chunk_len(I, 2 * j);
+        const int len1 = (2 * j + 1) < I.nchunks ? chunk_len(I, 2 * j + 1) : 0;
+        mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
+        tc_fence_after();
+        float s[128];
+        {
+          uint32_t sr[128];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_S + sb * 128 + c * 16, &sr[c * 16]);
+          if (len1 > 0) {
+#pragma unroll
+            for (int c = 4; c < 8; ++c)
+              tmem_ld16p(tmem + lane_off + TM_S + sb * 128 + c * 16, &sr[c * 16]);
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) reg_fence16(&sr[c * 16]);
+#pragma unroll
+          for (int e = 0; e < 128; ++e) s[e] = __uint_as_float(sr[e]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
+        // mask ragged chunks
+        if (len0 < CH || len1 < CH) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            if (e >= len0) s[e] = NEG_INF;
+            if (e >= len1) s[64 + e] = NEG_INF;
+          }
+        }
+        float mt = s[0];
+#pragma unroll
+        for (int e = 1; e < 128; ++e) mt = fmaxf(mt, s[e]);
+        const float mnew = fmaxf(m, mt * sl2);
+        const bool need = mnew > m + 8.0f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? ex2(m - mnew) : 1.0f;
+          if (j > 0) {
+            // O must be stable: wait for PV of the previous tile
+            mbar_wait(BAR(B_PFREE + ((gg - 1) & 1)), ((gg - 1) >> 1) & 1);
+            tc_fence_after();
+            uint32_t orr[64];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
+#pragma unroll
+            for (int e = 0; e < 64; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tmem_st16(tmem + lane_off + TM_O + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&orr[c * 16]));
+          }
+          if (need) {
+            l *= alpha;
+            m = mnew;
+          }
+        }
+        // P = exp2(s * scale_log2 - m), packed bf16 pairs
+        uint32_t pk[64];
+        float rs = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const float a = ex2(fmaf(s[2 * e], sl2, -m));
+          const float b = ex2(fmaf(s[2 * e + 1], sl2, -m));
+          rs += a + b;
+          pk[e] = pack_bf16(a, b);
+        }
+        l += rs;
+        // P buffer sb is free once the PV that read it (two tiles ago) is done
+        if (gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = pk[c * 16 + e];
+          tmem_st16(tmem + lane_off + TM_P + sb * 64 + c * 16, r);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(B_PFULL + sb));
+      }
+      // epilogue: O / l
+      mbar_wait(BAR(B_OFULL), it & 1);
+      tc_fence_after();
+      float o[64];
+      {
+        uint32_t orr[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) o[e] = __uint_as_float(orr[e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(BAR(B_OEMPTY));
+      if (row < I.rows) {
+        const int64_t pr = I.row0 + row;
+        const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
+        const float inv = 1.0f / l;
+        if (A.out_bf16) {
+          uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + (I.h * G.T + dst) * D);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 v;
+            v.x = pack_bf16(o[8 * c + 0] * inv, o[8 * c + 1] * inv);
+            v.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+            v.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+            v.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+            op[c] = v;
+          }
+        } else {
+          float4* op = reinterpret_cast<float4*>((float*)A.out + (I.h * G.T + dst) * D);
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            op[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
+                                o[4 * c + 3] * inv);
+        }
+      }
+      g += ntiles;
+      ++it;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)tc::D, (cuuint64_t)T, (cuuint64_t)H};
+  cuuint64_t strides[2] = {(cuuint64_t)tc::D * 2, (cuuint64_t)T * tc::D * 2};
+  cuuint32_t box[3] = {(cuuint32_t)tc::D, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BSA_OK;
+}
+
+size_t tc_smem_bytes() { return tc::SMEM_BYTES; }
+
+int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
+  CUtensorMap mq, mk, mv;
+  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);
+  if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
+  if (!rc) rc = make_map(&mv, a.vp, G.H, G.T, tc::CH);
+  if (rc) return rc;
+  BSA_CUDA_TRY(cudaFuncSetAttribute(tc::bsa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::SMEM_BYTES));
+  int dev = 0, sms = 148;
+  BSA_CUDA_TRY(cudaGetDevice(&dev));
+  BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t n_work = a.num_shards > 1
+                             ? (a.n_items - a.shard + a.num_shards - 1) / a.num_shards
+                             : a.n_items;
+  const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(1, n_work));
+  if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
+  tc::bsa_tc_kernel<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
+  BSA_LAUNCH_CHECK();
+  if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
+  return BSA_OK;
+}
+
+// events bracketing the most recent timed attention-kernel launch (per thread)
+cudaEvent_t timing_events(int which) {
+  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (!ev[0]) {
+    cudaEventCreate(&ev[0]);
+    cudaEventCreate(&ev[1]);
+  }
+  return ev[which];
+}
+
+}  // namespace bsa
+
+extern "C" float bsa_last_kernel_ms(void) {
+  float ms = -1.0f;
+  if (cudaEventSynchronize(bsa::timing_events(1)) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, bsa::timing_events(0), bsa::timing_events(1)) != cudaSuccess)
+    return -1.0f;
+  return ms;
+}
+
+namespace bsa {
+
+}  // namespace bsa

@@ -1,0 +1,918 @@
+// bsa_score.cu -- block-scoring stage on sm_100a.
+//
+// Replaces the reference mask predictor (/root/reference/pkg/src/bsattn/
+// maskpred.py:104-194 and tensorio.py:73-87) with three HBM/L2-bound kernels
+// that reproduce its fp32 arithmetic bit for bit:
+//
+//   pool_kernel     block_pool: out = (x0 + pairwise(x1..x_{n-1})) / n with
+//                   numpy's pairwise-sum tree; 8-byte/16-byte vector loads,
+//                   the patch gather folded into row addressing.
+//   scores_kernel   z = fl(fmaf-chain(qp, kp) * scale): a tiled batched GEMM
+//                   whose every output is ONE sequential fmaf chain over
+//                   k = 0..d-1 (OpenBLAS SkylakeX sgemm order at the configs).
+//   softsel_kernel  per (head, q-block) row: max, numpy exp, pairwise row
+//                   sum, IEEE divide (row_softmax), then select_blocks:
+//                   the tau crossing and the top-`take` threshold found by a
+//                   binary search over the fp32 key space with EXACT
+//                   fixed-point (2^-52 units) block reductions; rows where
+//                   exactness cannot be guaranteed (crossing element
+//                   < 2^-29, negative/huge user scores) are handed to
+//   fallback_kernel a full bitonic sort + sequential float64 cumsum, i.e.
+//                   the reference algorithm verbatim.
+//
+// All float arithmetic that must match the reference uses explicit _rn
+// intrinsics (no contraction), and the library is built without ftz.
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+
+#include "bsa_common.cuh"
+
+namespace bsa {
+
+// ===========================================================================
+// block_pool
+// ===========================================================================
+template <typename T, int VEC>
+struct PoolRows {
+  const T* base;     // x + h*sH + col
+  int64_t sT;
+  Layout L;
+  bool gather;
+  __device__ __forceinline__ void load(int64_t p, float (&v)[VEC]) const {
+    int64_t src = gather ? L.patch_src(p) : p;
+    const T* ptr = base + src * sT;
+    if constexpr (VEC == 4) {
+      Vec4<T>::load(ptr, v);
+    } else {
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) v[c] = to_f32(ptr[c]);
+    }
+  }
+};
+
+// numpy pairwise_sum of the m values at patch rows first..first+m-1 (m<=128)
+template <typename T, int VEC>
+__device__ __forceinline__ void pw_leaf(const PoolRows<T, VEC>& R, int64_t first, int64_t m,
+                                        float (&res)[VEC]) {
+  if (m < 8) {
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) res[c] = 0.0f;
+    for (int64_t i = 0; i < m; ++i) {
+      float v[VEC];
+      R.load(first + i, v);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) res[c] = __fadd_rn(res[c], v[c]);
+    }
+    return;
+  }
+  float r[8][VEC];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) R.load(first + j, r[j]);
+  int64_t i = 8;
+  const int64_t stop = m - (m % 8);
+  for (; i < stop; i += 8) {
+    float v[8][VEC];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) R.load(first + i + j, v[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) r[j][c] = __fadd_rn(r[j][c], v[j][c]);
+  }
+#pragma unroll
+  for (int c = 0; c < VEC; ++c)
+    res[c] = __fadd_rn(__fadd_rn(__fadd_rn(r[0][c], r[1][c]), __fadd_rn(r[2][c], r[3][c])),
+                       __fadd_rn(__fadd_rn(r[4][c], r[5][c]), __fadd_rn(r[6][c], r[7][c])));
+  for (; i < m; ++i) {
+    float v[VEC];
+    R.load(first + i, v);
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) res[c] = __fadd_rn(res[c], v[c]);
+  }
+}
+
+// general pairwise (m > 128 splits like numpy: n2 = m/2 rounded down to a multiple of 8)
+template <typename T, int VEC>
+__device__ __noinline__ void pw_rec(const PoolRows<T, VEC>& R, int64_t first, int64_t m,
+                                    float* res) {
+  float out[VEC];
+  if (m <= 128) {
+    pw_leaf<T, VEC>(R, first, m, out);
+  } else {
+    int64_t half = m / 2;
+    half -= half % 8;
+    float a[VEC], b[VEC];
+    pw_rec<T, VEC>(R, first, half, a);
+    pw_rec<T, VEC>(R, first + half, m - half, b);
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) out[c] = __fadd_rn(a[c], b[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) res[c] = out[c];
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int64_t sH,
+                                                   int64_t sT, int64_t H, int64_t n, int d,
+                                                   int block, Layout L, int gather,
+                                                   float* __restrict__ out, int64_t nb) {
+  const int lanes_per_row = min(32, (d + VEC - 1) / VEC);
+  const int rows_per_warp = 32 / lanes_per_row;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / lanes_per_row, lig = lane % lanes_per_row;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int64_t pr = warp * rows_per_warp + sub;  // pooled row id in [0, H*nb)
+  if (sub >= rows_per_warp || pr >= H * nb) return;
+  const int64_t h = pr / nb, b = pr % nb;
+  const int64_t r0 = b * block;
+  const int64_t len = min((int64_t)block, n - r0);
+  const float fl = (float)len;
+  for (int col = lig * VEC; col < d; col += lanes_per_row * VEC) {
+    PoolRows<T, VEC> R{x + h * sH + col, sT, L, gather != 0};
+    float x0[VEC];
+    R.load(r0, x0);
+    float s[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) s[c] = x0[c];
+    if (len > 1) {
+      float rest[VEC];
+      if (len - 1 <= 128) pw_leaf<T, VEC>(R, r0 + 1, len - 1, rest);
+      else pw_rec<T, VEC>(R, r0 + 1, len - 1, rest);
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) s[c] = __fadd_rn(s[c], rest[c]);
+    }
+    float* o = out + pr * d + col;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) o[c] = __fdiv_rn(s[c], fl);
+  }
+}
+
+// ===========================================================================
+// pooled scores: z = fl(acc * scale), acc = sequential fmaf over k = 0..d-1
+// ===========================================================================
+constexpr int SC_TQ = 64, SC_TK = 128, SC_KC = 32;
+
+__global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ qp,
+                                                     const float* __restrict__ kp, int64_t nq,
+                                                     int64_t nk, int d, float scale,
+                                                     float* __restrict__ z, int64_t ldz) {
+  __shared__ __align__(16) float qs[SC_KC][SC_TQ];
+  __shared__ __align__(16) float ks[SC_KC][SC_TK];
+  const int tid = threadIdx.x;
+  const int64_t h = blockIdx.z;
+  const int64_t i0 = (int64_t)blockIdx.y * SC_TQ, j0 = (int64_t)blockIdx.x * SC_TK;
+  const float* qh = qp + h * nq * d;
+  const float* kh = kp + h * nk * d;
+  const int tr = tid / 16, tc = tid % 16;  // 4 rows x 8 cols per thread
+  float acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0f;
+
+  for (int c0 = 0; c0 < d; c0 += SC_KC) {
+    const int kc = min(SC_KC, d - c0);
+    __syncthreads();
+    {  // q tile: thread -> row i = tid % 64, cols cg*8..cg*8+7
+      const int i = tid % SC_TQ, cg = tid / SC_TQ;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cg * 8 + u;
+        float v = 0.0f;
+        if (i0 + i < nq && c < kc) v = qh[(i0 + i) * d + c0 + c];
+        qs[c][i] = v;
+      }
+    }
+    {  // k tile: thread -> row j = tid % 128, cols cg*16..cg*16+15
+      const int j = tid % SC_TK, cg = tid / SC_TK;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = cg * 16 + u;
+        float v = 0.0f;
+        if (j0 + j < nk && c < kc) v = kh[(j0 + j) * d + c0 + c];
+        ks[c][j] = v;
+      }
+    }
+    __syncthreads();
+    for (int c = 0; c < kc; ++c) {
+      const float4 qa = *reinterpret_cast<const float4*>(&qs[c][tr * 4]);
+      const float4 kb0 = *reinterpret_cast<const float4*>(&ks[c][tc * 8]);
+      const float4 kb1 = *reinterpret_cast<const float4*>(&ks[c][tc * 8 + 4]);
+      const float qv[4] = {qa.x, qa.y, qa.z, qa.w};
+      const float kv[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = __fmaf_rn(qv[a], kv[b], acc[a][b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t i = i0 + tr * 4 + a;
+    if (i >= nq) continue;
+    float* zr = z + (h * nq + i) * ldz;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int64_t j = j0 + tc * 8 + b;
+      if (j < nk) zr[j] = __fmul_rn(acc[a][b], scale);
+    }
+  }
+}
+
+// ===========================================================================
+// block-level reductions (256 threads)
+// ===========================================================================
+constexpr int SS_THREADS = 256;
+constexpr int SS_WARPS = SS_THREADS / 32;
+
+struct SelShared {
+  float fred[SS_WARPS];
+  unsigned long long ured[SS_WARPS];
+  unsigned int cred[SS_WARPS];
+  unsigned int cred2[SS_WARPS];
+  float total;
+  int flag;
+};
+
+__device__ __forceinline__ float block_max(float v, SelShared& sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh.fred[threadIdx.x / 32] = v;
+  __syncthreads();
+  float r = sh.fred[0];
+#pragma unroll
+  for (int w = 1; w < SS_WARPS; ++w) r = fmaxf(r, sh.fred[w]);
+  return r;
+}
+
+__device__ __forceinline__ void block_sum2(unsigned long long a, unsigned int b,
+                                           unsigned int c, SelShared& sh,
+                                           unsigned long long& ra, unsigned int& rb,
+                                           unsigned int& rc) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    sh.ured[threadIdx.x / 32] = a;
+    sh.cred[threadIdx.x / 32] = b;
+    sh.cred2[threadIdx.x / 32] = c;
+  }
+  __syncthreads();
+  ra = 0; rb = 0; rc = 0;
+#pragma unroll
+  for (int w = 0; w < SS_WARPS; ++w) {
+    ra += sh.ured[w];
+    rb += sh.cred[w];
+    rc += sh.cred2[w];
+  }
+}
+
+__device__ __forceinline__ void block_minmax_u(unsigned int& mn, unsigned int& mx,
+                                               SelShared& sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    sh.cred[threadIdx.x / 32] = mn;
+    sh.cred2[threadIdx.x / 32] = mx;
+  }
+  __syncthreads();
+  mn = sh.cred[0];
+  mx = sh.cred2[0];
+#pragma unroll
+  for (int w = 1; w < SS_WARPS; ++w) {
+    mn = min(mn, sh.cred[w]);
+    mx = max(mx, sh.cred2[w]);
+  }
+}
+
+// value of a non-negative finite float < 2 in units of 2^-52, exact for
+// p >= 2^-29 (the fp32 ulp is then >= 2^-52), truncated below that.
+__device__ __forceinline__ unsigned long long fx52(unsigned int key) {
+  const unsigned int E = key >> 23;
+  if (E == 0) return 0ull;
+  const unsigned long long m = (unsigned long long)((key & 0x7fffffu) | 0x800000u);
+  const int sh = (int)E - 98;
+  if (sh >= 0) return m << sh;
+  return sh > -40 ? (m >> (-sh)) : 0ull;
+}
+
+constexpr unsigned int KEY_TINY = 98u << 23;   // bits of 2^-29
+constexpr unsigned int KEY_TWO = 128u << 23;   // bits of 2.0f
+
+// mass (2^-52 units) and count of keys >= t, plus count of keys == t
+__device__ __forceinline__ void mass_at_or_above(const unsigned int* keys, int64_t nk,
+                                                 unsigned int t, SelShared& sh,
+                                                 unsigned long long& mass,
+                                                 unsigned int& cnt, unsigned int& eq) {
+  unsigned long long m = 0;
+  unsigned int c = 0, e = 0;
+  for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
+    const unsigned int k = keys[j];
+    if (k >= t) { m += fx52(k); ++c; }
+    e += (k == t);
+  }
+  block_sum2(m, c, e, sh, mass, cnt, eq);
+}
+
+__device__ __forceinline__ void count_at_or_above(const unsigned int* keys, int64_t nk,
+                                                  unsigned int t, SelShared& sh,
+                                                  unsigned int& cnt, unsigned int& eq) {
+  unsigned int c = 0, e = 0;
+  for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
+    const unsigned int k = keys[j];
+    c += (k >= t);
+    e += (k == t);
+  }
+  unsigned long long dummy;
+  block_sum2(0ull, c, e, sh, dummy, cnt, eq);
+}
+
+// exclusive scan of one int per thread (256 threads)
+__device__ __forceinline__ unsigned int block_excl_scan(unsigned int v, unsigned int* tmp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x / 32;
+  unsigned int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  __syncthreads();
+  if (lane == 31) tmp[w] = incl;
+  __syncthreads();
+  unsigned int base = 0;
+  for (int i = 0; i < w; ++i) base += tmp[i];
+  return base + incl - v;
+}
+
+// ===========================================================================
+// softmax + select
+// ===========================================================================
+// numpy pairwise sum over a contiguous smem row (single thread)
+__device__ float pw_smem(const float* a, int64_t n) {
+  if (n < 8) {
+    float r = 0.0f;
+    for (int64_t i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    float r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __fadd_rn(res, a[i]);
+    return res;
+  }
+  // iterative post-order over numpy's split tree
+  struct Frame { int64_t off, n; int state; float left; };
+  Frame st[40];
+  int sp = 0;
+  st[0] = {0, n, 0, 0.0f};
+  float ret = 0.0f;
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      // leaf
+      const float* b = a + f.off;
+      const int64_t m = f.n;
+      float res;
+      if (m < 8) {
+        res = 0.0f;
+        for (int64_t i = 0; i < m; ++i) res = __fadd_rn(res, b[i]);
+      } else {
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = b[j];
+        int64_t i = 8;
+        for (; i < m - (m % 8); i += 8)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], b[i + j]);
+        res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+        for (; i < m; ++i) res = __fadd_rn(res, b[i]);
+      }
+      ret = res;
+      --sp;
+      continue;
+    }
+    int64_t half = f.n / 2;
+    half -= half % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[++sp] = {f.off, half, 0, 0.0f};
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[++sp] = {f.off + half, f.n - half, 0, 0.0f};
+    } else {
+      ret = __fadd_rn(f.left, ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+// keys[] aliases the probability row (bits of non-negative floats).
+// Returns false (row -> fallback) when the fast path cannot be exact.
+__device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau,
+                                int64_t k_floor, SelShared& sh, unsigned int* scan_tmp,
+                                uint8_t* __restrict__ bits_row, int32_t* take_out) {
+  // 1. validity: all keys non-negative (sign clear), finite, < 2
+  unsigned int mn = 0xffffffffu, mx = 0u;
+  for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
+    unsigned int k = keys[j];
+    mn = min(mn, k);
+    mx = max(mx, k);
+  }
+  block_minmax_u(mn, mx, sh);
+  if (mx >= KEY_TWO) return false;  // negative (sign bit), >= 2, inf or nan
+
+  // 2. cdf_len
+  int64_t cdf_len = 1;
+  unsigned int vstar = 0;
+  int64_t istar = 0;
+  bool have_star = false;
+  if (tau > 0.0) {
+    unsigned long long m_all;
+    unsigned int c_all, e_dummy;
+    mass_at_or_above(keys, nk, mn, sh, m_all, c_all, e_dummy);
+    if ((double)m_all * 0x1p-52 < tau) {
+      // total mass below tau: every prefix stays below, whole row selected
+      if (mn < KEY_TINY || m_all >= (1ull << 53)) return false;
+      cdf_len = nk;
+    } else {
+      // largest key t with mass(keys >= t) >= tau
+      unsigned int lo = mn;                 // mass(>= lo) >= tau
+      unsigned long long hi = (unsigned long long)mx + 1;  // mass(>= hi) == 0 < tau
+      while (hi - lo > 1) {
+        unsigned int mid = (unsigned int)(lo + ((hi - lo) >> 1));
+        unsigned long long m;
+        unsigned int c, e;
+        mass_at_or_above(keys, nk, mid, sh, m, c, e);
+        if ((double)m * 0x1p-52 >= tau) lo = mid; else hi = mid;
+      }
+      vstar = lo;
+      if (vstar < KEY_TINY) return false;
+      unsigned long long m_ge, m_gt;
+      unsigned int c_ge, c_gt, ties, e2;
+      mass_at_or_above(keys, nk, vstar, sh, m_ge, c_ge, ties);
+      mass_at_or_above(keys, nk, vstar + 1, sh, m_gt, c_gt, e2);
+      if (m_ge >= (1ull << 53)) return false;
+      const unsigned long long vfx = fx52(vstar);
+      // smallest i >= 1 with m_gt + i * v >= tau (all partial sums exact)
+      int64_t i = 1;
+      {
+        double need = (tau - (double)m_gt * 0x1p-52) / ((double)vfx * 0x1p-52);
+        int64_t guess = (int64_t)need;
+        if (guess < 1) guess = 1;
+        if (guess > (int64_t)ties) guess = ties;
+        i = guess;
+        while (i > 1 && (double)(m_gt + (unsigned long long)(i - 1) * vfx) * 0x1p-52 >= tau) --i;
+        while (i < (int64_t)ties && (double)(m_gt + (unsigned long long)i * vfx) * 0x1p-52 < tau) ++i;
+      }
+      if ((double)(m_gt + (unsigned long long)i * vfx) * 0x1p-52 < tau) return false;
+      if ((double)m_gt * 0x1p-52 >= tau) return false;
+      istar = i;
+      have_star = true;
+      cdf_len = (int64_t)c_gt + i;
+      if (cdf_len > nk) cdf_len = nk;
+    }
+  }
+  int64_t take = cdf_len > k_floor ? cdf_len : k_floor;
+  if (take > nk) take = nk;
+
+  // 3. threshold for the first `take` ranked blocks
+  unsigned int vt;
+  int64_t need;
+  if (take == nk) {
+    vt = 0u;
+    need = nk;  // everything (ties at 0 included)
+  } else if (have_star && take == cdf_len) {
+    vt = vstar;
+    unsigned int c_gt, e2;
+    count_at_or_above(keys, nk, vstar + 1, sh, c_gt, e2);
+    need = take - (int64_t)c_gt;
+  } else {
+    unsigned int lo = mn;
+    unsigned long long hi = (unsigned long long)mx + 1;
+    while (hi - lo > 1) {
+      unsigned int mid = (unsigned int)(lo + ((hi - lo) >> 1));
+      unsigned int c, e;
+      count_at_or_above(keys, nk, mid, sh, c, e);
+      if ((int64_t)c >= take) lo = mid; else hi = mid;
+    }
+    vt = lo;
+    unsigned int c_gt, e2;
+    if (vt == 0xffffffffu) c_gt = 0;
+    else count_at_or_above(keys, nk, vt + 1, sh, c_gt, e2);
+    need = take - (int64_t)c_gt;
+  }
+
+  // 4. bits: key > vt, or key == vt among the first `need` ties by index
+  const int64_t nbytes = (nk + 7) / 8;
+  const int64_t per = (nbytes + SS_THREADS - 1) / SS_THREADS;  // bytes per thread
+  const int64_t b0 = threadIdx.x * per, b1 = min(nbytes, b0 + per);
+  unsigned int my_ties = 0;
+  for (int64_t by = b0; by < b1; ++by)
+    for (int bit = 0; bit < 8; ++bit) {
+      int64_t j = by * 8 + bit;
+      if (j < nk && keys[j] == vt) ++my_ties;
+    }
+  unsigned int rank = block_excl_scan(my_ties, scan_tmp);
+  for (int64_t by = b0; by < b1; ++by) {
+    unsigned int byte = 0;
+    for (int bit = 0; bit < 8; ++bit) {
+      int64_t j = by * 8 + bit;
+      if (j >= nk) break;
+      unsigned int k = keys[j];
+      bool on = k > vt;
+      if (k == vt) {
+        on = (int64_t)rank < need;
+        ++rank;
+      }
+      byte |= (unsigned int)on << bit;
+    }
+    bits_row[by] = (uint8_t)byte;
+  }
+  if (threadIdx.x == 0) *take_out = (int32_t)take;
+  (void)istar;
+  return true;
+}
+
+template <bool SOFTMAX, bool SELECT>
+__global__ void __launch_bounds__(SS_THREADS)
+    softsel_kernel(float* __restrict__ src, int64_t ld, int64_t rows, int64_t nk, double tau,
+                   int64_t k_floor, float* __restrict__ probs_out, uint8_t* __restrict__ bits,
+                   int32_t* __restrict__ counts, int32_t* __restrict__ fb_list,
+                   int32_t* __restrict__ fb_count) {
+  extern __shared__ __align__(16) float row[];
+  __shared__ SelShared sh;
+  __shared__ unsigned int scan_tmp[SS_WARPS];
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  float* g = src + r * ld;
+  for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) row[j] = g[j];
+  __syncthreads();
+  if constexpr (SOFTMAX) {
+    float lmax = -__int_as_float(0x7f800000);
+    for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) lmax = fmaxf(lmax, row[j]);
+    const float mx = block_max(lmax, sh);
+    for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) row[j] = np_expf(__fsub_rn(row[j], mx));
+    __syncthreads();
+    if (threadIdx.x == 0) sh.total = __fadd_rn(0.0f, pw_smem(row, nk));
+    __syncthreads();
+    const float tot = sh.total;
+    for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
+      const float p = __fdiv_rn(row[j], tot);
+      row[j] = p;
+      if (probs_out) probs_out[r * nk + j] = p;
+    }
+    __syncthreads();
+  }
+  if constexpr (!SELECT) {
+    for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) g[j] = row[j];
+    return;
+  }
+  // normalise -0.0 to +0.0 so bit order == value order (argsort(-s) ties them)
+  for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS)
+    if (row[j] == 0.0f) row[j] = 0.0f;
+  __syncthreads();
+  const int64_t nbytes = (nk + 7) / 8;
+  const bool ok = select_row_fast(reinterpret_cast<const unsigned int*>(row), nk, tau, k_floor,
+                                  sh, scan_tmp, bits + r * nbytes, counts + r);
+  if (!ok) {
+    // hand the row (as probabilities) to the exact fallback kernel
+    if constexpr (SOFTMAX)
+      for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) g[j] = row[j];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int slot = atomicAdd(fb_count, 1);
+      fb_list[slot] = (int32_t)r;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exact fallback: bitonic sort of (rank key, index) + sequential f64 cumsum
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned int ordered_desc(float p) {
+  if (p == 0.0f) p = 0.0f;
+  unsigned int u = __float_as_uint(p);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // ascending float order
+  return ~u;                                          // descending
+}
+
+__global__ void __launch_bounds__(SS_THREADS)
+    fallback_kernel(const float* __restrict__ src, int64_t ld, int64_t nk, double tau,
+                    int64_t k_floor, uint8_t* __restrict__ bits, int32_t* __restrict__ counts,
+                    const int32_t* __restrict__ fb_list, const int32_t* __restrict__ fb_count,
+                    unsigned long long* __restrict__ scratch, int64_t npow2) {
+  extern __shared__ unsigned int bm[];  // ceil(nk/32) words: selected bitmap
+  __shared__ int64_t take_sh;
+  const int n_fb = *fb_count;
+  unsigned long long* s = scratch + (int64_t)blockIdx.x * npow2;
+  const int64_t nbytes = (nk + 7) / 8;
+  for (int f = blockIdx.x; f < n_fb; f += gridDim.x) {
+    const int64_t r = fb_list[f];
+    const float* p = src + r * ld;
+    for (int64_t j = threadIdx.x; j < npow2; j += SS_THREADS)
+      s[j] = j < nk ? (((unsigned long long)ordered_desc(p[j]) << 32) | (unsigned long long)j)
+                    : ~0ull;
+    __syncthreads();
+    for (int64_t size = 2; size <= npow2; size <<= 1) {
+      for (int64_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int64_t i = threadIdx.x; i < npow2 / 2; i += SS_THREADS) {
+          const int64_t lo = 2 * i - (i & (stride - 1));
+          const int64_t hi = lo + stride;
+          const bool up = ((lo & size) == 0);
+          unsigned long long a = s[lo], b = s[hi];
+          if ((a > b) == up) { s[lo] = b; s[hi] = a; }
+        }
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      double cum = 0.0;
+      int64_t below = 0;
+      for (int64_t i = 0; i < nk; ++i) {
+        const int64_t j = (int64_t)(s[i] & 0xffffffffull);
+        cum += (double)p[j];
+        if (cum < tau) ++below;
+      }
+      int64_t cdf_len = below + 1 < nk ? below + 1 : nk;
+      int64_t take = cdf_len > k_floor ? cdf_len : k_floor;
+      if (take > nk) take = nk;
+      take_sh = take;
+      counts[r] = (int32_t)take;
+    }
+    __syncthreads();
+    const int64_t take = take_sh;
+    const int64_t nwords = (nk + 31) / 32;
+    for (int64_t w = threadIdx.x; w < nwords; w += SS_THREADS) bm[w] = 0u;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < take; i += SS_THREADS) {
+      const unsigned int j = (unsigned int)(s[i] & 0xffffffffull);
+      atomicOr(&bm[j >> 5], 1u << (j & 31));
+    }
+    __syncthreads();
+    uint8_t* out = bits + r * nbytes;
+    for (int64_t b = threadIdx.x; b < nbytes; b += SS_THREADS)
+      out[b] = (uint8_t)((bm[b >> 2] >> ((b & 3) * 8)) & 0xffu);
+    __syncthreads();
+  }
+}
+
+}  // namespace bsa
+
+// ===========================================================================
+// host launchers + C ABI
+// ===========================================================================
+namespace bsa {
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// z = fl(a * scale) (tensorio.py:83), the first step of row_softmax
+__global__ void scale_kernel(const float* __restrict__ a, int64_t n, float scale,
+                             float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __fmul_rn(a[i], scale);
+}
+
+static int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+constexpr int FB_GRID = 64;
+
+// select workspace: [fb_count int32 (256 B slot)] [fb_list int32 rows] [scratch u64 FB_GRID*npow2]
+static size_t select_ws_bytes(int64_t rows, int64_t nk) {
+  return 256 + align_up((size_t)rows * 4, 256) + (size_t)FB_GRID * (size_t)next_pow2(nk) * 8;
+}
+
+static int check_tensor(const bsa_tensor* t, const char* name) {
+  if (!t || !t->data) return fail(BSA_EINVAL, "%s: null tensor", name);
+  if (t->dtype != BSA_F32 && t->dtype != BSA_BF16)
+    return fail(BSA_EINVAL, "%s: unsupported dtype code %d", name, t->dtype);
+  if (t->heads < 1 || t->tokens < 1 || t->dim < 1)
+    return fail(BSA_EINVAL, "%s has a zero-sized dimension: (%lld, %lld, %lld)", name,
+                (long long)t->heads, (long long)t->tokens, (long long)t->dim);
+  return BSA_OK;
+}
+
+template <typename T>
+static int launch_pool_t(const bsa_tensor* x, const Layout& L, bool gather, int64_t n,
+                         int32_t block, float* out, cudaStream_t st) {
+  const int d = (int)x->dim;
+  const int64_t nb = ceil_div(n, block);
+  const bool vec_ok = (d % 4 == 0) && ((uintptr_t)x->data % (4 * sizeof(T)) == 0) &&
+                      ((x->stride_token * (int64_t)sizeof(T)) % (4 * sizeof(T)) == 0) &&
+                      ((x->stride_head * (int64_t)sizeof(T)) % (4 * sizeof(T)) == 0);
+  const int vec = vec_ok ? 4 : 1;
+  const int lanes = std::min(32, (d + vec - 1) / vec);
+  const int rows_per_warp = 32 / lanes;
+  const int64_t total = x->heads * nb;
+  const int64_t warps = ceil_div(total, rows_per_warp);
+  const int64_t grid = ceil_div(warps, 8);
+  if (vec_ok)
+    pool_kernel<T, 4><<<(unsigned)grid, 256, 0, st>>>(
+        (const T*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
+        gather ? 1 : 0, out, nb);
+  else
+    pool_kernel<T, 1><<<(unsigned)grid, 256, 0, st>>>(
+        (const T*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
+        gather ? 1 : 0, out, nb);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+static int launch_pool(const bsa_tensor* x, const bsa_layout* gather, int32_t block, float* out,
+                       cudaStream_t st, int64_t* n_out) {
+  int rc = check_tensor(x, "x");
+  if (rc) return rc;
+  if (block < 1) return fail(BSA_EINVAL, "block size must be >= 1, got %d", block);
+  Layout L;
+  int64_t n;
+  if (gather) {
+    L = to_layout(gather);
+    if (L.frames < 1 || L.P < 1 || L.S < 0) return fail(BSA_EINVAL, "invalid layout");
+    if (x->tokens != L.tokens())
+      return fail(BSA_EINVAL, "inputs have %lld tokens but layout describes %lld",
+                  (long long)x->tokens, (long long)L.tokens());
+    n = L.n_patch();
+  } else {
+    n = x->tokens;
+    L = patch_only_layout(n);
+  }
+  if (n_out) *n_out = n;
+  if (x->dtype == BSA_F32) return launch_pool_t<float>(x, L, gather != nullptr, n, block, out, st);
+  return launch_pool_t<__nv_bfloat16>(x, L, gather != nullptr, n, block, out, st);
+}
+
+static int launch_scores(const float* qp, const float* kp, int64_t H, int64_t nq, int64_t nk,
+                         int64_t d, float scale, float* z, int64_t ldz, cudaStream_t st) {
+  if (nq > 65535LL * SC_TQ || H > 65535)
+    return fail(BSA_EUNSUPPORTED, "pooled_scores: grid too large (nq=%lld, heads=%lld)",
+                (long long)nq, (long long)H);
+  dim3 grid((unsigned)ceil_div(nk, SC_TK), (unsigned)ceil_div(nq, SC_TQ), (unsigned)H);
+  scores_kernel<<<grid, 256, 0, st>>>(qp, kp, nq, nk, (int)d, scale, z, ldz);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+template <bool SOFTMAX, bool SELECT>
+static int launch_softsel(float* src, int64_t ld, int64_t rows, int64_t nk, double tau,
+                          int64_t k_floor, float* probs_out, uint8_t* bits, int32_t* counts,
+                          void* ws, cudaStream_t st) {
+  const size_t smem = align_up((size_t)nk * 4, 16);
+  if (smem > 200 * 1024)
+    return fail(BSA_EUNSUPPORTED, "nk=%lld key blocks per row exceeds the on-chip row buffer",
+                (long long)nk);
+  auto kern = softsel_kernel<SOFTMAX, SELECT>;
+  BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int32_t* fb_count = (int32_t*)ws;
+  int32_t* fb_list = (int32_t*)((char*)ws + 256);
+  unsigned long long* scratch =
+      (unsigned long long*)((char*)ws + 256 + align_up((size_t)rows * 4, 256));
+  if (SELECT) BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
+  kern<<<(unsigned)rows, SS_THREADS, smem, st>>>(src, ld, rows, nk, tau, k_floor, probs_out, bits,
+                                                  counts, fb_list, fb_count);
+  BSA_LAUNCH_CHECK();
+  if (SELECT) {
+    const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
+    BSA_CUDA_TRY(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(fsmem, 16)));
+    fallback_kernel<<<FB_GRID, SS_THREADS, std::max<size_t>(fsmem, 16), st>>>(
+        src, ld, nk, tau, k_floor, bits, counts, fb_list, fb_count, scratch, next_pow2(nk));
+    BSA_LAUNCH_CHECK();
+  }
+  return BSA_OK;
+}
+
+}  // namespace bsa
+
+using namespace bsa;
+
+extern "C" {
+
+int bsa_block_pool(const bsa_tensor* x, const bsa_layout* patch_gather, int32_t block,
+                   float* out, void* stream) {
+  if (!out) return fail(BSA_EINVAL, "block_pool: null output");
+  return launch_pool(x, patch_gather, block, out, (cudaStream_t)stream, nullptr);
+}
+
+size_t bsa_pooled_scores_workspace(int64_t heads, int64_t nq, int64_t nk) {
+  (void)heads; (void)nq; (void)nk;
+  return 256;
+}
+
+int bsa_pooled_scores(const float* qp, const float* kp, int64_t heads, int64_t nq, int64_t nk,
+                      int64_t dim, float scale, float* probs, void* ws, size_t ws_bytes,
+                      void* stream) {
+  (void)ws; (void)ws_bytes;
+  if (!qp || !kp || !probs) return fail(BSA_EINVAL, "pooled_scores: null pointer");
+  if (heads < 1 || nq < 1 || nk < 1 || dim < 1)
+    return fail(BSA_EINVAL, "pooled_scores: zero-sized dimension");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_scores(qp, kp, heads, nq, nk, dim, scale, probs, nk, st);
+  if (rc) return rc;
+  return launch_softsel<true, false>(probs, nk, heads * nq, nk, 0.0, 1, nullptr, nullptr,
+                                     nullptr, nullptr, st);
+}
+
+int bsa_row_softmax(const float* a, int64_t rows, int64_t cols, float scale, float* out,
+                    void* stream) {
+  if (!a || !out) return fail(BSA_EINVAL, "row_softmax: null pointer");
+  if (rows < 1 || cols < 1)
+    return fail(BSA_EINVAL, "a has a zero-sized dimension: (%lld, %lld)", (long long)rows,
+                (long long)cols);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = rows * cols;
+  scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 32), 256, 0, st>>>(a, n, scale,
+                                                                                     out);
+  BSA_LAUNCH_CHECK();
+  return launch_softsel<true, false>(out, cols, rows, cols, 0.0, 1, nullptr, nullptr, nullptr,
+                                     nullptr, st);
+}
+
+size_t bsa_select_workspace(int64_t heads, int64_t nq, int64_t nk) {
+  return select_ws_bytes(heads * nq, nk);
+}
+
+int bsa_select_blocks(const float* probs, int64_t heads, int64_t nq, int64_t nk, double tau,
+                      int64_t k_floor, uint8_t* mask_bits, int32_t* counts, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (!probs || !mask_bits || !counts) return fail(BSA_EINVAL, "select_blocks: null pointer");
+  if (heads < 1 || nq < 1 || nk < 1) return fail(BSA_EINVAL, "select_blocks: zero-sized dimension");
+  if (!(tau >= 0.0 && tau <= 1.0)) return fail(BSA_EINVAL, "tau must be in [0, 1], got %g", tau);
+  if (k_floor < 1) return fail(BSA_EINVAL, "k_floor must be >= 1, got %lld", (long long)k_floor);
+  if (ws_bytes < select_ws_bytes(heads * nq, nk))
+    return fail(BSA_EINVAL, "select_blocks: workspace too small");
+  return launch_softsel<false, true>(const_cast<float*>(probs), nk, heads * nq, nk, tau, k_floor,
+                                     nullptr, mask_bits, counts, ws, (cudaStream_t)stream);
+}
+
+size_t bsa_predict_mask_workspace(int64_t heads, int64_t patch_tokens, int64_t dim,
+                                  int32_t block_q, int32_t block_k) {
+  if (heads < 1 || patch_tokens < 1 || dim < 1 || block_q < 1 || block_k < 1) return 0;
+  const int64_t nq = ceil_div(patch_tokens, block_q), nk = ceil_div(patch_tokens, block_k);
+  return align_up((size_t)(heads * nq * dim) * 4, 256) + align_up((size_t)(heads * nk * dim) * 4, 256) +
+         align_up((size_t)(heads * nq * nk) * 4, 256) + select_ws_bytes(heads * nq, nk);
+}
+
+int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* patch_gather,
+                     int32_t block_q, int32_t block_k, float scale, double tau,
+                     int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
+                     void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_tensor(q, "q_patches");
+  if (!rc) rc = check_tensor(k, "k_patches");
+  if (rc) return rc;
+  if (!mask_bits || !counts || !ws) return fail(BSA_EINVAL, "predict_mask: null pointer");
+  if (q->heads != k->heads || q->dim != k->dim || q->tokens != k->tokens)
+    return fail(BSA_EINVAL, "q/k shapes differ");
+  if (block_q < 1 || block_k < 1)
+    return fail(BSA_EINVAL, "block sizes must be >= 1, got %d/%d", block_q, block_k);
+  if (!(tau >= 0.0 && tau <= 1.0)) return fail(BSA_EINVAL, "tau must be in [0, 1], got %g", tau);
+  const int64_t H = q->heads, d = q->dim;
+  const int64_t tp = patch_gather ? to_layout(patch_gather).n_patch() : q->tokens;
+  const int64_t nq = ceil_div(tp, block_q), nk = ceil_div(tp, block_k);
+  if (k_floor < 1 || k_floor > nk)
+    return fail(BSA_EINVAL, "k_floor must be in [1, %lld], got %lld", (long long)nk,
+                (long long)k_floor);
+  if (ws_bytes < bsa_predict_mask_workspace(H, tp, d, block_q, block_k))
+    return fail(BSA_EINVAL, "predict_mask: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  float* qp = (float*)w;
+  w += align_up((size_t)(H * nq * d) * 4, 256);
+  float* kp = (float*)w;
+  w += align_up((size_t)(H * nk * d) * 4, 256);
+  float* z = (float*)w;
+  w += align_up((size_t)(H * nq * nk) * 4, 256);
+  int64_t n1 = 0, n2 = 0;
+  rc = launch_pool(q, patch_gather, block_q, qp, st, &n1);
+  if (!rc) rc = launch_pool(k, patch_gather, block_k, kp, st, &n2);
+  if (!rc) rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
+  if (!rc)
+    rc = launch_softsel<true, true>(z, nk, H * nq, nk, tau, k_floor, probs_out, mask_bits, counts,
+                                    w, st);
+  return rc;
+}
+
+}  // extern "C"

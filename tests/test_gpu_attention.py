@@ -1,0 +1,214 @@
+"""Attention stage on the B200 vs the reference's golden outputs and the
+float64 oracle.
+
+Tolerances (BASELINE.json north_star):
+  fp32 path (CUDA-core kernel):  max |o - o_ref| <= 1e-4 (the reference's own
+                                 tests use 1e-5 vs float64; we assert 1e-5 on
+                                 the small cases too);
+  bf16 path (tcgen05 kernel):    max |o - o_ref| / max |o_ref| <= 2e-2, with
+                                 o_ref the float64 oracle on the same
+                                 bf16-rounded inputs.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from golden_inputs import CASES_ATTN, make_qkv
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+BF16_REL_TOL = 2e-2
+FP32_ABS_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def bsa():
+    import paper_2509_07120_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    import oracle as o
+    return o
+
+
+def _to_bf16(*arrs):
+    import torch
+    return [torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.bfloat16) for a in arrs]
+
+
+def _rel(out, ref):
+    return float(np.abs(out - ref).max() / np.abs(ref).max())
+
+
+def _random_mask(rng, g, heads, keep):
+    blocks = rng.random((heads, g.nq_blocks, g.nk_blocks)) < keep
+    empty = ~blocks.any(axis=2)
+    hi, qi = np.nonzero(empty)
+    blocks[hi, qi, rng.integers(g.nk_blocks, size=hi.size)] = True
+    return blocks
+
+
+@pytest.mark.parametrize("case", CASES_ATTN, ids=[c["name"] for c in CASES_ATTN])
+def test_fp32_matches_reference_golden(bsa, case):
+    z = np.load(os.path.join(GOLDEN, f"attn_{case['name']}.npz"))
+    lay = bsa.TokenLayout(case["frames"], case["patches"], case["specials"])
+    q, k, v = make_qkv(case["heads"], lay.total_tokens, case["d"], case["seed"])
+    g = bsa.BlockGeometry(lay.patch_tokens, case["block_q"], case["block_k"])
+    pidx = bsa.patch_token_indices(lay)
+    mask = bsa.predict_mask(q[:, pidx], k[:, pidx], bsa.MaskPolicy(case["tau"], case["rho"], g))
+    assert np.array_equal(mask.device_bits().cpu().numpy(), z["mask_bits"])
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask)
+    assert bsa.attention_path(job) == "simt"
+    out = bsa.sparse_attention(job)
+    ref = z["out"] if "out" in z else None
+    if ref is not None:
+        assert np.abs(out - ref).max() <= 1e-5
+    else:
+        rows = z["rows"]
+        assert np.abs(out[:, rows] - z["out_rows"]).max() <= FP32_ABS_TOL
+        assert abs(float(out.astype(np.float64).sum()) - float(z["out_sum"])) <= 1e-2
+    assert np.isfinite(out).all()
+
+
+@pytest.mark.parametrize("spec", [5, 0, 3])
+@pytest.mark.parametrize("patches", [300, 1369])
+def test_tc_bf16_vs_f64_oracle(bsa, oracle, spec, patches):
+    frames = 2 if patches == 1369 else 3
+    lay = bsa.TokenLayout(frames, patches, spec)
+    q, k, v = make_qkv(2, lay.total_tokens, 64, 31 + spec + patches)
+    qd, kd, vd = _to_bf16(q, k, v)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    mask = bsa.predict_mask(qd, kd, bsa.MaskPolicy(0.4, 0.8, g), layout=lay)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, mask)
+    assert bsa.attention_path(job) == "tc"
+    out = bsa.sparse_attention(job).float().cpu().numpy()
+    qb, kb, vb = (t.float().cpu().numpy() for t in (qd, kd, vd))
+    ref = oracle.masked_attention_f64(qb, kb, vb, frames, patches, spec, mask.blocks, 128, 64)
+    assert _rel(out, ref) <= BF16_REL_TOL
+
+
+@pytest.mark.parametrize("keep", [0.05, 0.5, 1.0])
+def test_tc_random_masks(bsa, oracle, keep):
+    rng = np.random.default_rng(int(keep * 100))
+    lay = bsa.TokenLayout(3, 700, 5)
+    q, k, v = make_qkv(3, lay.total_tokens, 64, 77)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    blocks = _random_mask(rng, g, 3, keep)
+    qd, kd, vd = _to_bf16(q, k, v)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, bsa.BlockMask(blocks, g))
+    out = bsa.sparse_attention(job).float().cpu().numpy()
+    qb, kb, vb = (t.float().cpu().numpy() for t in (qd, kd, vd))
+    ref = oracle.masked_attention_f64(qb, kb, vb, 3, 700, 5, blocks, 128, 64)
+    assert _rel(out, ref) <= BF16_REL_TOL
+
+
+def test_tc_full_mask_equals_dense(bsa):
+    """Zero sparsity == dense attention (acceptance C1) on the tensor-core path."""
+    import torch
+    import torch.nn.functional as F
+    lay = bsa.TokenLayout(2, 1000, 5)
+    q, k, v = make_qkv(4, lay.total_tokens, 64, 5)
+    qd, kd, vd = _to_bf16(q, k, v)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, bsa.full_mask(g, 4))
+    out = bsa.sparse_attention(job).float()
+    ref = F.scaled_dot_product_attention(qd.float()[None], kd.float()[None], vd.float()[None])[0]
+    assert float((out - ref).abs().max() / ref.abs().max()) <= BF16_REL_TOL
+
+
+def test_tc_deterministic_and_permutation_transparent(bsa):
+    import torch
+    lay = bsa.TokenLayout(2, 500, 4)
+    q, k, v = make_qkv(2, lay.total_tokens, 64, 8)
+    qd, kd, vd = _to_bf16(q, k, v)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    mask = bsa.predict_mask(qd, kd, bsa.MaskPolicy(0.5, 0.7, g), layout=lay)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, mask)
+    a = bsa.sparse_attention(job)
+    b = bsa.sparse_attention(job)
+    assert torch.equal(a, b)
+    perm, inv = bsa.partition_permutation(lay)
+    pt = torch.from_numpy(perm).cuda()
+    pre = bsa.AttentionInputs(qd[:, pt], kd[:, pt], vd[:, pt])
+    c = bsa.sparse_attention(bsa.SparseAttentionJob(pre, lay, mask), inputs_permuted=True)
+    assert torch.equal(c[:, torch.from_numpy(inv).cuda()], a)
+
+
+def test_tc_shards_cover_everything(bsa):
+    import torch
+    lay = bsa.TokenLayout(2, 600, 5)
+    q, k, v = make_qkv(2, lay.total_tokens, 64, 9)
+    qd, kd, vd = _to_bf16(q, k, v)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    mask = bsa.predict_mask(qd, kd, bsa.MaskPolicy(0.4, 0.8, g), layout=lay)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, mask)
+    full = bsa.sparse_attention(job)
+    acc = torch.zeros_like(full)
+    for s in range(3):
+        part = bsa.sparse_attention(job, shard=s, num_shards=3)
+        acc += part
+    assert torch.equal(acc, full)
+
+
+def test_special_rows_exact_under_any_mask(bsa):
+    """Special query rows ignore the mask: they equal dense attention."""
+    rng = np.random.default_rng(3)
+    lay = bsa.TokenLayout(2, 70, 5)
+    q, k, v = make_qkv(2, lay.total_tokens, 16, 4)
+    g = bsa.BlockGeometry(lay.patch_tokens, 32, 16)
+    blocks = _random_mask(rng, g, 2, 0.25)
+    inp = bsa.AttentionInputs(q, k, v)
+    out = bsa.sparse_attention(bsa.SparseAttentionJob(inp, lay, bsa.BlockMask(blocks, g)))
+    dense = bsa.dense_attention(inp)
+    spec = [f * lay.tokens_per_frame + s for f in range(2) for s in range(5)]
+    np.testing.assert_allclose(out[:, spec], dense[:, spec], atol=1e-5)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_simt_random_layouts_vs_oracle(bsa, oracle, seed):
+    """The reference's random-mask test geometry (test_sparse.py:74-90)."""
+    rng = np.random.default_rng(100 + seed)
+    lay = bsa.TokenLayout(int(rng.integers(1, 4)), int(rng.integers(40, 120)),
+                          int(rng.choice([0, 3, 5])))
+    q, k, v = make_qkv(2, lay.total_tokens, 16, 200 + seed)
+    g = bsa.BlockGeometry(lay.patch_tokens, 48, 16)
+    blocks = _random_mask(rng, g, 2, 0.4)
+    out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay,
+                                                      bsa.BlockMask(blocks, g)))
+    ref = oracle.masked_attention_f64(q, k, v, lay.frames, lay.patches_per_frame,
+                                      lay.specials_per_frame, blocks, 48, 16)
+    assert np.abs(out - ref).max() <= 1e-5
+
+
+def test_flop_estimate_and_stats(bsa):
+    n = 4096
+    lay = bsa.TokenLayout(1, n, 0)
+    q, k, v = make_qkv(1, n, 8, 13)
+    g = bsa.BlockGeometry(n, 128, 64)
+    blocks = np.zeros((1, g.nq_blocks, g.nk_blocks), dtype=bool)
+    blocks[:, :, :16] = True
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, bsa.BlockMask(blocks, g))
+    est = bsa.flop_estimate(job)
+    assert est.theoretical_speedup == pytest.approx(4.0)
+    assert job.mask.achieved_sparsity()[0] == pytest.approx(0.75)
+    plain = bsa.sparse_attention(job)
+    out, reports = bsa.sparse_attention_stats(job)
+    assert plain.tobytes() == out.tobytes()
+    assert reports[0].theoretical_speedup == pytest.approx(4.0)
+
+
+def test_validation_errors(bsa):
+    lay = bsa.TokenLayout(1, 64, 0)
+    q, k, v = make_qkv(1, 64, 8, 9)
+    with pytest.raises(ValueError, match="patch tokens"):
+        bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay,
+                               bsa.full_mask(bsa.BlockGeometry(96, 32, 16), 1))
+    q2, k2, v2 = make_qkv(2, 64, 8, 10)
+    with pytest.raises(ValueError, match="heads"):
+        bsa.SparseAttentionJob(bsa.AttentionInputs(q2, k2, v2), lay,
+                               bsa.full_mask(bsa.BlockGeometry(64, 32, 16), 1))
