@@ -158,6 +158,21 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (x <= ~8): round-to-nearest split x = j + f,
+// f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel err 7.7e-5, well
+// below the bf16 rounding of P), exponent added as an integer.
+constexpr int EXP_POLY_EVERY = 4;
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float j = t - 12582912.0f;
+  const float f = x - j;
+  float p = fmaf(0.05508868f, f, 0.24260405f);
+  p = fmaf(p, f, 0.6932762f);
+  p = fmaf(p, f, 0.99992895f);
+  const int ji = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (ji << 23));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -440,9 +455,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (e >= len1) s[64 + e] = NEG_INF;
           }
         }
-        float mt = s[0];
+        float mx8[8];
 #pragma unroll
-        for (int e = 1; e < 128; ++e) mt = fmaxf(mt, s[e]);
+        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[8 + i]);
+#pragma unroll
+        for (int e = 16; e < 128; e += 8)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[e + i]);
+        const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
         const float mnew = fmaxf(m, mt * sl2);
         const bool need = mnew > m + 8.0f;
         if (__any_sync(0xffffffffu, need)) {
@@ -468,27 +489,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             m = mnew;
           }
         }
-        // P = exp2(s * scale_log2 - m), packed bf16 pairs
-        uint32_t pk[64];
-        float rs = 0.0f;
-#pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          const float a = ex2(fmaf(s[2 * e], sl2, -m));
-          const float b = ex2(fmaf(s[2 * e + 1], sl2, -m));
-          rs += a + b;
-          pk[e] = pack_bf16(a, b);
-        }
-        l += rs;
         // P buffer sb is free once the PV that read it (two tiles ago) is done
         if (gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
         tc_fence_after();
+        // P = exp2(s * scale_log2 - m) as packed bf16 pairs, streamed to TMEM
+        // 32 columns at a time; 1 pair in EXP_POLY_EVERY runs on the FMA pipe
+        const float nm = -m;
+        float rs8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) rs8[i] = 0.0f;
+        const int nchunk = len1 > 0 ? 4 : 2;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
+          if (c >= nchunk) break;
           uint32_t r[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = pk[c * 16 + e];
+          for (int e = 0; e < 16; ++e) {
+            const float x0 = fmaf(s[c * 32 + 2 * e], sl2, nm);
+            const float x1 = fmaf(s[c * 32 + 2 * e + 1], sl2, nm);
+            float a, b;
+            if ((e % EXP_POLY_EVERY) == EXP_POLY_EVERY - 1) {
+              a = exp2_poly(x0);
+              b = exp2_poly(x1);
+            } else {
+              a = ex2(x0);
+              b = ex2(x1);
+            }
+            rs8[e & 7] += a + b;
+            r[e] = pack_bf16(a, b);
+          }
           tmem_st16(tmem + lane_off + TM_P + sb * 64 + c * 16, r);
         }
+        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();

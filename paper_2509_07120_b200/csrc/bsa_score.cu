@@ -92,24 +92,46 @@ __device__ __forceinline__ void pw_leaf(const PoolRows<T, VEC>& R, int64_t first
   }
 }
 
-// general pairwise (m > 128 splits like numpy: n2 = m/2 rounded down to a multiple of 8)
+// general pairwise (m > 128 splits like numpy: n2 = m/2 rounded down to a
+// multiple of 8), evaluated as an explicit post-order walk (no device
+// recursion): leaves in left-to-right order, partial sums on a small stack.
 template <typename T, int VEC>
 __device__ __noinline__ void pw_rec(const PoolRows<T, VEC>& R, int64_t first, int64_t m,
                                     float* res) {
-  float out[VEC];
-  if (m <= 128) {
-    pw_leaf<T, VEC>(R, first, m, out);
-  } else {
-    int64_t half = m / 2;
-    half -= half % 8;
-    float a[VEC], b[VEC];
-    pw_rec<T, VEC>(R, first, half, a);
-    pw_rec<T, VEC>(R, first + half, m - half, b);
+  struct Frame { int64_t off, n; int state; };
+  Frame st[48];
+  float vals[48][VEC];   // value stack: finished left halves / leaves
+  int sp = 0, vp = 0;
+  st[0] = {first, m, 0};
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      float leaf[VEC];
+      pw_leaf<T, VEC>(R, f.off, f.n, leaf);
 #pragma unroll
-    for (int c = 0; c < VEC; ++c) out[c] = __fadd_rn(a[c], b[c]);
+      for (int c = 0; c < VEC; ++c) vals[vp][c] = leaf[c];
+      ++vp;
+      --sp;
+      continue;
+    }
+    int64_t half = f.n / 2;
+    half -= half % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[++sp] = {f.off, half, 0};
+    } else if (f.state == 1) {
+      f.state = 2;
+      st[++sp] = {f.off + half, f.n - half, 0};
+    } else {
+      // combine the two most recent values: left + right
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) vals[vp - 2][c] = __fadd_rn(vals[vp - 2][c], vals[vp - 1][c]);
+      --vp;
+      --sp;
+    }
   }
 #pragma unroll
-  for (int c = 0; c < VEC; ++c) res[c] = out[c];
+  for (int c = 0; c < VEC; ++c) res[c] = vals[0][c];
 }
 
 template <typename T, int VEC>
