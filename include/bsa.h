@@ -92,8 +92,9 @@ int bsa_pooled_scores(const float* qp, const float* kp, int64_t heads, int64_t n
 
 /* row_softmax (tensorio.py:73-87): out = softmax(a * scale) per row of a
  * (rows, cols) fp32 matrix, reference arithmetic (numpy exp, pairwise sum). */
+size_t bsa_row_softmax_workspace(int64_t rows, int64_t cols);
 int bsa_row_softmax(const float* a, int64_t rows, int64_t cols, float scale, float* out,
-                    void* stream);
+                    void* ws, size_t ws_bytes, void* stream);
 
 /* select_blocks (maskpred.py:142-174).  probs (H,nq,nk) fp32 contiguous ->
  * mask_bits (H*nq rows of ceil(nk/8) bytes) and counts[H*nq] (selected

@@ -59,7 +59,8 @@ def _declare(L):
         "bsa_block_pool": ([pt, pl, i32, vp, vp], ctypes.c_int),
         "bsa_pooled_scores_workspace": ([i64, i64, i64], sz),
         "bsa_pooled_scores": ([vp, vp, i64, i64, i64, i64, f32, vp, vp, sz, vp], ctypes.c_int),
-        "bsa_row_softmax": ([vp, i64, i64, f32, vp, vp], ctypes.c_int),
+        "bsa_row_softmax_workspace": ([i64, i64], sz),
+        "bsa_row_softmax": ([vp, i64, i64, f32, vp, vp, sz, vp], ctypes.c_int),
         "bsa_select_workspace": ([i64, i64, i64], sz),
         "bsa_select_blocks": ([vp, i64, i64, i64, f64, i64, vp, vp, vp, sz, vp], ctypes.c_int),
         "bsa_predict_mask_workspace": ([i64, i64, i64, i32, i32], sz),
@@ -85,7 +86,8 @@ def exported_symbols():
     """Names include/bsa.h declares (checked by the CPU test-suite)."""
     return [
         "bsa_version", "bsa_last_error", "bsa_device_sm_count", "bsa_block_pool",
-        "bsa_pooled_scores_workspace", "bsa_pooled_scores", "bsa_row_softmax",
+        "bsa_pooled_scores_workspace", "bsa_pooled_scores", "bsa_row_softmax_workspace",
+        "bsa_row_softmax",
         "bsa_select_workspace", "bsa_select_blocks", "bsa_predict_mask_workspace",
         "bsa_predict_mask", "bsa_sparse_attention_workspace", "bsa_sparse_attention",
         "bsa_sparse_attention_path", "bsa_last_kernel_ms", "bsa_mask_selected_area", "bsa_mask_to_csr_workspace",

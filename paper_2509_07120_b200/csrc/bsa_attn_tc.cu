@@ -4,21 +4,23 @@
 // (special strip + selected 64-token key blocks per 128-row query block,
 // online softmax) for bf16 inputs, head_dim 64, block_q 128, block_k 64.
 //
-// Persistent, warp-specialised CTA (one per SM, 192 threads):
+// Persistent, warp-specialised CTAs, TWO per SM (so two softmax warpgroups
+// share each SM's issue slots and tensor core), 192 threads each:
 //   warp 4      producer: fetches LPT-ordered work items (atomic counter),
-//               TMA-loads the 128x64 Q tile and, per 128-key tile, two
-//               64-token K chunks and two V chunks (any two selected blocks,
-//               gathered by coordinates) into a 4-stage SW128 smem ring.
+//               TMA-loads the 128x64 Q tile and, per key tile, the 64-token
+//               K and V chunk of the next selected block (gathered by TMA
+//               coordinates) into a 4-stage SW128 smem ring.
 //   warp 5      MMA issuer (one thread): S = Q K^T (tcgen05.mma kind::f16,
-//               M=128, N=128|64, fp32 accumulate in TMEM, double buffered)
-//               and O += P V with P read straight from TMEM (A operand),
-//               V from smem (MN-major B operand); tcgen05.commit -> mbarriers.
+//               M=128, N=64, fp32 in TMEM, double buffered) and O += P V with
+//               P read from TMEM (A operand) and V from smem (MN-major B);
+//               tcgen05.commit -> mbarriers.
 //   warps 0-3   softmax / correction / epilogue: thread t owns query row t
 //               (TMEM lane t): tcgen05.ld the S row, mask ragged chunks, exp2
-//               with lazy (threshold 2^8) rescaling of O in TMEM, bf16 P back
-//               to TMEM via tcgen05.st, final O / l to global memory in the
-//               caller's (interleaved) token order.
-// TMEM: S0|S1 (2x128 cols) P0|P1 (2x64) O (64) = 448 of 512 columns.
+//               (half on MUFU, half as an FMA-pipe polynomial, f32x2 packed
+//               math), lazy (2^8) rescaling of O in TMEM, bf16 P back to TMEM
+//               with tcgen05.st, final O / l to global memory in the caller's
+//               (interleaved) token order.
+// TMEM (256 of 512 columns per CTA): S0|S1 (2x64) P0|P1 (2x32) O (64).
 #include <cuda.h>
 
 #include "bsa_attn.cuh"
@@ -28,23 +30,24 @@ namespace tc {
 
 constexpr int BQ = 128, CH = 64, D = 64, NST = 4;
 constexpr int Q_BYTES = BQ * D * 2;          // 16 KB
-constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB
-constexpr int KV_BYTES = 2 * CHUNK_BYTES;    // 16 KB per K (or V) stage
+constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB (one K or V tile)
 constexpr int NUM_THREADS = 192;
+constexpr int CTAS_PER_SM = 2;
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-constexpr int OFF_V = OFF_K + NST * KV_BYTES;
-constexpr int OFF_BAR = OFF_V + NST * KV_BYTES;
-constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
+constexpr int OFF_V = OFF_K + NST * CHUNK_BYTES;
+constexpr int OFF_BAR = OFF_V + NST * CHUNK_BYTES;
+constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;  // barriers/ring + alignment slack
+constexpr uint32_t TMEM_COLS = 256;
 
-constexpr uint32_t TM_S = 0, TM_P = 256, TM_O = 384;
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 192;
 
 // barrier slots (8 bytes each) inside the barrier region
 enum {
-  B_QFULL = 0,          // [2]
-  B_QEMPTY = 2,         // [2]
-  B_KFULL = 4,          // [NST]
-  B_VFULL = 4 + NST,    // [NST]
+  B_QFULL = 0,              // [2]
+  B_QEMPTY = 2,             // [2]
+  B_KFULL = 4,              // [NST]
+  B_VFULL = 4 + NST,        // [NST]
   B_KVEMPTY = 4 + 2 * NST,  // [NST]
   B_SFULL = 4 + 3 * NST,    // [2]
   B_SEMPTY = B_SFULL + 2,   // [2]
@@ -56,6 +59,7 @@ enum {
   B_IEMPTY = B_IFULL + 2,   // [2]
   B_COUNT = B_IEMPTY + 2
 };
+static_assert(B_COUNT * 8 + 32 <= 512, "barrier region");
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -119,7 +123,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -128,7 +132,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -140,6 +144,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 // ties later uses of tcgen05.ld results to after tcgen05.wait::ld
 __device__ __forceinline__ void reg_fence16(uint32_t* r) {
   asm volatile(""
@@ -147,31 +154,28 @@ __device__ __forceinline__ void reg_fence16(uint32_t* r) {
                  "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
                  "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
 }
-__device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* r) {
-  tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
-}
-__device__ __forceinline__ void tmem_wait_st() {
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe (x <= ~8): round-to-nearest split x = j + f,
-// f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel err 7.7e-5, well
-// below the bf16 rounding of P), exponent added as an integer.
-constexpr int EXP_POLY_EVERY = 4;
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;
-  const float j = t - 12582912.0f;
-  const float f = x - j;
-  float p = fmaf(0.05508868f, f, 0.24260405f);
-  p = fmaf(p, f, 0.6932762f);
-  p = fmaf(p, f, 0.99992895f);
-  const int ji = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (ji << 23));
+// 2^x for a pair on the FMA pipe (x <= ~8): round-to-nearest split
+// x = j + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel err 7.7e-5,
+// far below the bf16 rounding of P), exponent added as an integer.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+  float2 p = __ffma2_rn(make_float2(0.05508868f, 0.05508868f), f,
+                        make_float2(0.24260405f, 0.24260405f));
+  p = __ffma2_rn(p, f, make_float2(0.6932762f, 0.6932762f));
+  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  // (t_bits << 23) == (j << 23) mod 2^32 because t = 1.5*2^23 + j
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -202,10 +206,10 @@ struct Item {
   int64_t qb;      // -1 for a special-row tile
   int64_t row0;    // first partitioned query row
   int rows;        // valid query rows
-  int nchunks;     // 64-key chunks in the key stream
-  int last_len;    // length of the final chunk (ragged tails)
-  int nsc;         // leading contiguous chunks (special strip / all keys)
-  int spec_last;   // length of the last contiguous chunk
+  int nchunks;     // 64-key tiles in the key stream
+  int last_len;    // length of the final tile (ragged tails)
+  int nsc;         // leading contiguous tiles (special strip / all keys)
+  int spec_last;   // length of the last contiguous tile
 };
 
 __device__ __forceinline__ Item decode(const AttnGeom& G, int32_t code, const int32_t* counts,
@@ -231,7 +235,7 @@ __device__ __forceinline__ Item decode(const AttnGeom& G, int32_t code, const in
     it.spec_last = it.nsc ? (int)(G.Ts - (int64_t)(it.nsc - 1) * CH) : CH;
     const int cnt = counts[it.h * G.nq + it.qb];
     it.nchunks = it.nsc + cnt;
-    // ragged last patch block, if selected, is always the final chunk
+    // the ragged last patch block, if selected, is always the final tile
     const int64_t lastb = G.nk - 1;
     const uint8_t lb = bits[(it.h * G.nq + it.qb) * G.mask_row_bytes + (lastb >> 3)];
     const bool last_sel = (lb >> (lastb & 7)) & 1;
@@ -250,7 +254,7 @@ __device__ __forceinline__ int chunk_len(const Item& it, int c) {
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -284,8 +288,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 5) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_holder))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)), "n"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -323,24 +327,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint8_t* mrow =
             I.qb >= 0 ? A.bits + (I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
         KeyChunker ck(G, I.qb, mrow, CH);
-        const int ntiles = (I.nchunks + 1) >> 1;
-        for (int j = 0; j < ntiles; ++j, ++g) {
+        for (int j = 0; j < I.nchunks; ++j, ++g) {
           const uint32_t st = g % NST;
           mbar_wait(BAR(B_KVEMPTY + st), ((g / NST) & 1) ^ 1);
-          int64_t s0, s1 = -1;
-          int l0, l1 = 0;
+          int64_t s0;
+          int l0;
           ck.next(s0, l0);
-          const bool two = (2 * j + 1) < I.nchunks;
-          if (two) ck.next(s1, l1);
-          const uint32_t bytes = two ? KV_BYTES : CHUNK_BYTES;
-          const uint32_t kdst = sbase + OFF_K + st * KV_BYTES;
-          const uint32_t vdst = sbase + OFF_V + st * KV_BYTES;
-          mbar_expect_tx(BAR(B_KFULL + st), bytes);
-          tma_load_3d(kdst, &tm_k, BAR(B_KFULL + st), 0, (int)s0, (int)I.h);
-          if (two) tma_load_3d(kdst + CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s1, (int)I.h);
-          mbar_expect_tx(BAR(B_VFULL + st), bytes);
-          tma_load_3d(vdst, &tm_v, BAR(B_VFULL + st), 0, (int)s0, (int)I.h);
-          if (two) tma_load_3d(vdst + CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, (int)s1, (int)I.h);
+          mbar_expect_tx(BAR(B_KFULL + st), CHUNK_BYTES);
+          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0,
+                      (int)I.h);
+          mbar_expect_tx(BAR(B_VFULL + st), CHUNK_BYTES);
+          tma_load_3d(sbase + OFF_V + st * CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, (int)s0,
+                      (int)I.h);
         }
         ++it;
       }
@@ -350,7 +348,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ======================= MMA issuer =======================
     if (lane == 0) {
       uint32_t it = 0, g = 0;
-      const uint32_t id_s128 = idesc_bf16(128, 128, 0), id_s64 = idesc_bf16(128, 64, 0);
+      const uint32_t id_s = idesc_bf16(128, 64, 0);
       const uint32_t id_pv = idesc_bf16(128, 64, 1);
       while (true) {
         const uint32_t slot = it & 1;
@@ -359,22 +357,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_arrive(BAR(B_IEMPTY + slot));
         if (code < 0) break;
         const Item I = decode(G, code, A.counts, A.bits);
-        const int ntiles = (I.nchunks + 1) >> 1;
+        const int ntiles = I.nchunks;
         mbar_wait(BAR(B_QFULL + slot), (it >> 1) & 1);
         tc_fence_after();
         const uint32_t qaddr = sbase + OFF_Q + slot * Q_BYTES;
         auto issue_pv = [&](uint32_t gg, int jj) {
           const uint32_t st = gg % NST, pb = gg & 1;
-          const bool two = (2 * jj + 1) < I.nchunks;
           mbar_wait(BAR(B_PFULL + pb), (gg >> 1) & 1);
           mbar_wait(BAR(B_VFULL + st), (gg / NST) & 1);
           if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
           tc_fence_after();
-          const uint32_t vaddr = sbase + OFF_V + st * KV_BYTES;
-          const int ksteps = two ? 8 : 4;
-          for (int k = 0; k < ksteps; ++k) {
+          const uint32_t vaddr = sbase + OFF_V + st * CHUNK_BYTES;
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k) {
             const uint64_t bd = sdesc(vaddr + k * 2048, 8192, 1024);
-            mma_ts(tmem + TM_O, tmem + TM_P + pb * 64 + k * 8, bd, id_pv,
+            mma_ts(tmem + TM_O, tmem + TM_P + pb * 32 + k * 8, bd, id_pv,
                    (jj > 0 || k > 0) ? 1u : 0u);
           }
           tc_commit(BAR(B_PFREE + pb));
@@ -383,16 +380,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int j = 0; j < ntiles; ++j) {
           const uint32_t gg = g + j;
           const uint32_t st = gg % NST, sb = gg & 1;
-          const bool two = (2 * j + 1) < I.nchunks;
           mbar_wait(BAR(B_KFULL + st), (gg / NST) & 1);
           mbar_wait(BAR(B_SEMPTY + sb), ((gg >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t kaddr = sbase + OFF_K + st * KV_BYTES;
+          const uint32_t kaddr = sbase + OFF_K + st * CHUNK_BYTES;
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             const uint64_t ad = sdesc(qaddr + k * 32, 16, 1024);
             const uint64_t bd = sdesc(kaddr + k * 32, 16, 1024);
-            mma_ss(tmem + TM_S + sb * 128, ad, bd, two ? id_s128 : id_s64, k > 0 ? 1u : 0u);
+            mma_ss(tmem + TM_S + sb * 64, ad, bd, id_s, k > 0 ? 1u : 0u);
           }
           tc_commit(BAR(B_SFULL + sb));
           if (j == ntiles - 1) tc_commit(BAR(B_QEMPTY + slot));
@@ -420,46 +416,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(BAR(B_IEMPTY + slot));
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
-      const int ntiles = (I.nchunks + 1) >> 1;
+      const int ntiles = I.nchunks;
       float m = NEG_INF, l = 0.0f;
       for (int j = 0; j < ntiles; ++j) {
         const uint32_t gg = g + j, sb = gg & 1;
-        const int len0 = chunk_len(I, 2 * j);
-        const int len1 = (2 * j + 1) < I.nchunks ? chunk_len(I, 2 * j + 1) : 0;
+        const int len = chunk_len(I, j);
         mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
         tc_fence_after();
-        float s[128];
-        {
-          uint32_t sr[128];
+        uint32_t sr[64];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_S + sb * 128 + c * 16, &sr[c * 16]);
-          if (len1 > 0) {
+        for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_S + sb * 64 + c * 16, &sr[c * 16]);
+        tmem_wait_ld();
 #pragma unroll
-            for (int c = 4; c < 8; ++c)
-              tmem_ld16p(tmem + lane_off + TM_S + sb * 128 + c * 16, &sr[c * 16]);
-          }
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < 8; ++c) reg_fence16(&sr[c * 16]);
-#pragma unroll
-          for (int e = 0; e < 128; ++e) s[e] = __uint_as_float(sr[e]);
-        }
+        for (int c = 0; c < 4; ++c) reg_fence16(&sr[c * 16]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
-        // mask ragged chunks
-        if (len0 < CH || len1 < CH) {
+        float s[64];
 #pragma unroll
-          for (int e = 0; e < 64; ++e) {
-            if (e >= len0) s[e] = NEG_INF;
-            if (e >= len1) s[64 + e] = NEG_INF;
-          }
+        for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(sr[e]);
+        if (len < CH) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (e >= len) s[e] = NEG_INF;
         }
         float mx8[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[8 + i]);
 #pragma unroll
-        for (int e = 16; e < 128; e += 8)
+        for (int e = 16; e < 64; e += 8)
 #pragma unroll
           for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[e + i]);
         const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
@@ -474,15 +459,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc_fence_after();
             uint32_t orr[64];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
+            for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
 #pragma unroll
             for (int e = 0; e < 64; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              tmem_st16(tmem + lane_off + TM_O + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&orr[c * 16]));
+            for (int c = 0; c < 4; ++c) tmem_st16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
           }
           if (need) {
             l *= alpha;
@@ -492,35 +476,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // P buffer sb is free once the PV that read it (two tiles ago) is done
         if (gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
         tc_fence_after();
-        // P = exp2(s * scale_log2 - m) as packed bf16 pairs, streamed to TMEM
-        // 32 columns at a time; 1 pair in EXP_POLY_EVERY runs on the FMA pipe
-        const float nm = -m;
-        float rs8[8];
+        // P = exp2(s * scale_log2 - m) as packed bf16 pairs, streamed to TMEM;
+        // odd pairs on MUFU.EX2, even pairs as an FMA-pipe polynomial
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
+        float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) rs8[i] = 0.0f;
-        const int nchunk = len1 > 0 ? 4 : 2;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c >= nchunk) break;
+        for (int c = 0; c < 2; ++c) {
           uint32_t r[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const float x0 = fmaf(s[c * 32 + 2 * e], sl2, nm);
-            const float x1 = fmaf(s[c * 32 + 2 * e + 1], sl2, nm);
-            float a, b;
-            if ((e % EXP_POLY_EVERY) == EXP_POLY_EVERY - 1) {
-              a = exp2_poly(x0);
-              b = exp2_poly(x1);
+            const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]),
+                                        sl2v, nmv);
+            float2 p;
+            if (e & 1) {
+              p = make_float2(ex2(x.x), ex2(x.y));
             } else {
-              a = ex2(x0);
-              b = ex2(x1);
+              p = exp2_poly2(x);
             }
-            rs8[e & 7] += a + b;
-            r[e] = pack_bf16(a, b);
+            rs[e & 3] = __fadd2_rn(rs[e & 3], p);
+            r[e] = pack_bf16(p.x, p.y);
           }
-          tmem_st16(tmem + lane_off + TM_P + sb * 64 + c * 16, r);
+          tmem_st16(tmem + lane_off + TM_P + sb * 32 + c * 16, r);
         }
-        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        const float2 r01 = __fadd2_rn(rs[0], rs[1]), r23 = __fadd2_rn(rs[2], rs[3]);
+        const float2 rr = __fadd2_rn(r01, r23);
+        l += rr.x + rr.y;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -529,17 +510,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // epilogue: O / l
       mbar_wait(BAR(B_OFULL), it & 1);
       tc_fence_after();
-      float o[64];
-      {
-        uint32_t orr[64];
+      uint32_t orr[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16p(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
-        tmem_wait_ld();
+      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
+      tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
-#pragma unroll
-        for (int e = 0; e < 64; ++e) o[e] = __uint_as_float(orr[e]);
-      }
+      for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(B_OEMPTY));
@@ -552,18 +528,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             uint4 v;
-            v.x = pack_bf16(o[8 * c + 0] * inv, o[8 * c + 1] * inv);
-            v.y = pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-            v.z = pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-            v.w = pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+            v.x = pack_bf16(__uint_as_float(orr[8 * c + 0]) * inv, __uint_as_float(orr[8 * c + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(orr[8 * c + 2]) * inv, __uint_as_float(orr[8 * c + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(orr[8 * c + 4]) * inv, __uint_as_float(orr[8 * c + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(orr[8 * c + 6]) * inv, __uint_as_float(orr[8 * c + 7]) * inv);
             op[c] = v;
           }
         } else {
           float4* op = reinterpret_cast<float4*>((float*)A.out + (I.h * G.T + dst) * D);
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            op[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
-                                o[4 * c + 3] * inv);
+            op[c] = make_float4(__uint_as_float(orr[4 * c]) * inv, __uint_as_float(orr[4 * c + 1]) * inv,
+                                __uint_as_float(orr[4 * c + 2]) * inv, __uint_as_float(orr[4 * c + 3]) * inv);
         }
       }
       g += ntiles;
@@ -575,7 +551,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+                 : "memory");
   }
 }
 
@@ -618,6 +595,16 @@ static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, in
 
 size_t tc_smem_bytes() { return tc::SMEM_BYTES; }
 
+// events bracketing the most recent timed attention-kernel launch (per thread)
+cudaEvent_t timing_events(int which) {
+  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (!ev[0]) {
+    cudaEventCreate(&ev[0]);
+    cudaEventCreate(&ev[1]);
+  }
+  return ev[which];
+}
+
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   CUtensorMap mq, mk, mv;
   int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);
@@ -632,22 +619,13 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   const int64_t n_work = a.num_shards > 1
                              ? (a.n_items - a.shard + a.num_shards - 1) / a.num_shards
                              : a.n_items;
-  const int grid = (int)std::min<int64_t>(sms, std::max<int64_t>(1, n_work));
+  const int grid =
+      (int)std::min<int64_t>((int64_t)sms * tc::CTAS_PER_SM, std::max<int64_t>(1, n_work));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
   tc::bsa_tc_kernel<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
   BSA_LAUNCH_CHECK();
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
   return BSA_OK;
-}
-
-// events bracketing the most recent timed attention-kernel launch (per thread)
-cudaEvent_t timing_events(int which) {
-  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
-  if (!ev[0]) {
-    cudaEventCreate(&ev[0]);
-    cudaEventCreate(&ev[1]);
-  }
-  return ev[which];
 }
 
 }  // namespace bsa
@@ -659,7 +637,3 @@ extern "C" float bsa_last_kernel_ms(void) {
     return -1.0f;
   return ms;
 }
-
-namespace bsa {
-
-}  // namespace bsa

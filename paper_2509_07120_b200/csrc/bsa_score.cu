@@ -37,13 +37,26 @@ template <typename T, int VEC>
 struct PoolRows {
   const T* base;     // x + h*sH + col
   int64_t sT;
-  Layout L;
+  uint32_t P, S, spec_off;  // patch->source remap (32-bit: tokens < 2^31)
   bool gather;
   __device__ __forceinline__ void load(int64_t p, float (&v)[VEC]) const {
-    int64_t src = gather ? L.patch_src(p) : p;
+    int64_t src = p;
+    if (gather) {
+      const uint32_t f = (uint32_t)p / P;
+      src = (int64_t)f * (P + S) + spec_off + ((uint32_t)p - f * P);
+    }
     const T* ptr = base + src * sT;
     if constexpr (VEC == 4) {
       Vec4<T>::load(ptr, v);
+    } else if constexpr (VEC == 2) {
+      if constexpr (sizeof(T) == 4) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(ptr));
+        v[0] = t.x; v[1] = t.y;
+      } else {
+        const unsigned int t = __ldg(reinterpret_cast<const unsigned int*>(ptr));
+        const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&t));
+        v[0] = f2.x; v[1] = f2.y;
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < VEC; ++c) v[c] = to_f32(ptr[c]);
@@ -134,7 +147,7 @@ __device__ __noinline__ void pw_rec(const PoolRows<T, VEC>& R, int64_t first, in
   for (int c = 0; c < VEC; ++c) res[c] = vals[0][c];
 }
 
-template <typename T, int VEC>
+template <typename T, int VEC, bool LONG>
 __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int64_t sH,
                                                    int64_t sT, int64_t H, int64_t n, int d,
                                                    int block, Layout L, int gather,
@@ -151,7 +164,8 @@ __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int6
   const int64_t len = min((int64_t)block, n - r0);
   const float fl = (float)len;
   for (int col = lig * VEC; col < d; col += lanes_per_row * VEC) {
-    PoolRows<T, VEC> R{x + h * sH + col, sT, L, gather != 0};
+    PoolRows<T, VEC> R{x + h * sH + col, sT, (uint32_t)L.P, (uint32_t)L.S,
+                       (uint32_t)(L.specials_first ? L.S : 0), gather != 0};
     float x0[VEC];
     R.load(r0, x0);
     float s[VEC];
@@ -159,8 +173,8 @@ __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int6
     for (int c = 0; c < VEC; ++c) s[c] = x0[c];
     if (len > 1) {
       float rest[VEC];
-      if (len - 1 <= 128) pw_leaf<T, VEC>(R, r0 + 1, len - 1, rest);
-      else pw_rec<T, VEC>(R, r0 + 1, len - 1, rest);
+      if constexpr (LONG) pw_rec<T, VEC>(R, r0 + 1, len - 1, rest);
+      else pw_leaf<T, VEC>(R, r0 + 1, len - 1, rest);
 #pragma unroll
       for (int c = 0; c < VEC; ++c) s[c] = __fadd_rn(s[c], rest[c]);
     }
@@ -173,7 +187,7 @@ __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int6
 // ===========================================================================
 // pooled scores: z = fl(acc * scale), acc = sequential fmaf over k = 0..d-1
 // ===========================================================================
-constexpr int SC_TQ = 64, SC_TK = 128, SC_KC = 32;
+constexpr int SC_TQ = 128, SC_TK = 128, SC_KC = 32;
 
 __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ qp,
                                                      const float* __restrict__ kp, int64_t nq,
@@ -186,52 +200,45 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
   const int64_t i0 = (int64_t)blockIdx.y * SC_TQ, j0 = (int64_t)blockIdx.x * SC_TK;
   const float* qh = qp + h * nq * d;
   const float* kh = kp + h * nk * d;
-  const int tr = tid / 16, tc = tid % 16;  // 4 rows x 8 cols per thread
-  float acc[4][8];
+  const int tr = tid / 16, tc = tid % 16;  // 8 rows x 8 cols per thread
+  float acc[8][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 8; ++b) acc[a][b] = 0.0f;
 
   for (int c0 = 0; c0 < d; c0 += SC_KC) {
     const int kc = min(SC_KC, d - c0);
     __syncthreads();
-    {  // q tile: thread -> row i = tid % 64, cols cg*8..cg*8+7
+    {  // both tiles: thread -> row i = tid % 128, cols cg*16..cg*16+15
       const int i = tid % SC_TQ, cg = tid / SC_TQ;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = cg * 8 + u;
-        float v = 0.0f;
-        if (i0 + i < nq && c < kc) v = qh[(i0 + i) * d + c0 + c];
-        qs[c][i] = v;
-      }
-    }
-    {  // k tile: thread -> row j = tid % 128, cols cg*16..cg*16+15
-      const int j = tid % SC_TK, cg = tid / SC_TK;
+      const bool qok = i0 + i < nq, kok = j0 + i < nk;
+      const float* qrow = qh + (i0 + i) * d + c0;
+      const float* krow = kh + (j0 + i) * d + c0;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int c = cg * 16 + u;
-        float v = 0.0f;
-        if (j0 + j < nk && c < kc) v = kh[(j0 + j) * d + c0 + c];
-        ks[c][j] = v;
+        qs[c][i] = (qok && c < kc) ? qrow[c] : 0.0f;
+        ks[c][i] = (kok && c < kc) ? krow[c] : 0.0f;
       }
     }
     __syncthreads();
     for (int c = 0; c < kc; ++c) {
-      const float4 qa = *reinterpret_cast<const float4*>(&qs[c][tr * 4]);
-      const float4 kb0 = *reinterpret_cast<const float4*>(&ks[c][tc * 8]);
-      const float4 kb1 = *reinterpret_cast<const float4*>(&ks[c][tc * 8 + 4]);
-      const float qv[4] = {qa.x, qa.y, qa.z, qa.w};
-      const float kv[8] = {kb0.x, kb0.y, kb0.z, kb0.w, kb1.x, kb1.y, kb1.z, kb1.w};
+      const float4 qa = *reinterpret_cast<const float4*>(&qs[c][tr * 8]);
+      const float4 qb = *reinterpret_cast<const float4*>(&qs[c][tr * 8 + 4]);
+      const float4 ka = *reinterpret_cast<const float4*>(&ks[c][tc * 8]);
+      const float4 kb = *reinterpret_cast<const float4*>(&ks[c][tc * 8 + 4]);
+      const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+      const float kv[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 8; ++b) acc[a][b] = __fmaf_rn(qv[a], kv[b], acc[a][b]);
     }
   }
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t i = i0 + tr * 4 + a;
+  for (int a = 0; a < 8; ++a) {
+    const int64_t i = i0 + tr * 8 + a;
     if (i >= nq) continue;
     float* zr = z + (h * nq + i) * ldz;
 #pragma unroll
@@ -379,73 +386,87 @@ __device__ __forceinline__ unsigned int block_excl_scan(unsigned int v, unsigned
 // ===========================================================================
 // softmax + select
 // ===========================================================================
-// numpy pairwise sum over a contiguous smem row (single thread)
-__device__ float pw_smem(const float* a, int64_t n) {
-  if (n < 8) {
-    float r = 0.0f;
-    for (int64_t i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
-    return r;
-  }
-  if (n <= 128) {
-    float r[8];
+// Largest key t in [lo, hi) whose "at or above t" statistic still meets the
+// target: MASS -> exact fixed-point mass(keys >= t) >= tau, else
+// count(keys >= t) >= take.  Requires the predicate true at lo and false at
+// hi; both statistics are monotone non-increasing in t.  Each round tests 8
+// thresholds at once (one pass over the row, one block reduction), so the
+// 2^k-wide key range shrinks 9x per round.
+constexpr int NPROBE = 8;
+struct ProbeShared {
+  unsigned long long mass[SS_WARPS][NPROBE];
+  unsigned int cnt[SS_WARPS][NPROBE];
+};
+
+template <bool MASS>
+__device__ unsigned int search_keys(const unsigned int* keys, int64_t nk, unsigned int lo,
+                                    unsigned long long hi, double tau, int64_t take,
+                                    SelShared& sh) {
+  __shared__ ProbeShared ps;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  while (hi - lo > 1) {
+    const unsigned long long span = hi - lo;
+    unsigned int t[NPROBE];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
+    for (int i = 0; i < NPROBE; ++i) {
+      unsigned long long off = span * (unsigned long long)(i + 1) / (NPROBE + 1);
+      if (off < 1) off = 1;
+      t[i] = (unsigned int)(lo + off);
+    }
+    unsigned int c[NPROBE];
+    unsigned long long ms[NPROBE];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
-    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __fadd_rn(res, a[i]);
-    return res;
-  }
-  // iterative post-order over numpy's split tree
-  struct Frame { int64_t off, n; int state; float left; };
-  Frame st[40];
-  int sp = 0;
-  st[0] = {0, n, 0, 0.0f};
-  float ret = 0.0f;
-  while (sp >= 0) {
-    Frame& f = st[sp];
-    if (f.n <= 128) {
-      // leaf
-      const float* b = a + f.off;
-      const int64_t m = f.n;
-      float res;
-      if (m < 8) {
-        res = 0.0f;
-        for (int64_t i = 0; i < m; ++i) res = __fadd_rn(res, b[i]);
-      } else {
-        float r[8];
+    for (int i = 0; i < NPROBE; ++i) { c[i] = 0; ms[i] = 0; }
+    for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
+      const unsigned int k = keys[j];
+      const unsigned long long f = MASS ? fx52(k) : 0ull;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = b[j];
-        int64_t i = 8;
-        for (; i < m - (m % 8); i += 8)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], b[i + j]);
-        res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-        for (; i < m; ++i) res = __fadd_rn(res, b[i]);
+      for (int i = 0; i < NPROBE; ++i) {
+        const bool ge = k >= t[i];
+        c[i] += ge;
+        if (MASS) ms[i] += ge ? f : 0ull;
       }
-      ret = res;
-      --sp;
-      continue;
     }
-    int64_t half = f.n / 2;
-    half -= half % 8;
-    if (f.state == 0) {
-      f.state = 1;
-      st[++sp] = {f.off, half, 0, 0.0f};
-    } else if (f.state == 1) {
-      f.left = ret;
-      f.state = 2;
-      st[++sp] = {f.off + half, f.n - half, 0, 0.0f};
-    } else {
-      ret = __fadd_rn(f.left, ret);
-      --sp;
+#pragma unroll
+    for (int i = 0; i < NPROBE; ++i) {
+      c[i] = __reduce_add_sync(0xffffffffu, c[i]);
+      if (MASS) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ms[i] += __shfl_xor_sync(0xffffffffu, ms[i], o);
+      }
     }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NPROBE; ++i) {
+        ps.cnt[w][i] = c[i];
+        if (MASS) ps.mass[w][i] = ms[i];
+      }
+    }
+    __syncthreads();
+    // every thread evaluates the same predicate sequence -> uniform update
+    unsigned long long nlo = lo, nhi = hi;
+#pragma unroll
+    for (int i = 0; i < NPROBE; ++i) {
+      unsigned int ct = 0;
+      unsigned long long mt = 0;
+#pragma unroll
+      for (int ww = 0; ww < SS_WARPS; ++ww) {
+        ct += ps.cnt[ww][i];
+        if (MASS) mt += ps.mass[ww][i];
+      }
+      const bool ok = MASS ? ((double)mt * 0x1p-52 >= tau) : ((int64_t)ct >= take);
+      if (ok) {
+        if (t[i] > nlo) nlo = t[i];
+      } else {
+        if (t[i] < nhi) nhi = t[i];
+      }
+    }
+    lo = (unsigned int)nlo;
+    hi = nhi;
   }
-  return ret;
+  (void)sh;
+  return lo;
 }
 
 // keys[] aliases the probability row (bits of non-negative floats).
@@ -477,17 +498,8 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
       if (mn < KEY_TINY || m_all >= (1ull << 53)) return false;
       cdf_len = nk;
     } else {
-      // largest key t with mass(keys >= t) >= tau
-      unsigned int lo = mn;                 // mass(>= lo) >= tau
-      unsigned long long hi = (unsigned long long)mx + 1;  // mass(>= hi) == 0 < tau
-      while (hi - lo > 1) {
-        unsigned int mid = (unsigned int)(lo + ((hi - lo) >> 1));
-        unsigned long long m;
-        unsigned int c, e;
-        mass_at_or_above(keys, nk, mid, sh, m, c, e);
-        if ((double)m * 0x1p-52 >= tau) lo = mid; else hi = mid;
-      }
-      vstar = lo;
+      // largest key t with mass(keys >= t) >= tau (8-ary search)
+      vstar = search_keys<true>(keys, nk, mn, (unsigned long long)mx + 1, tau, 0, sh);
       if (vstar < KEY_TINY) return false;
       unsigned long long m_ge, m_gt;
       unsigned int c_ge, c_gt, ties, e2;
@@ -529,15 +541,7 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
     count_at_or_above(keys, nk, vstar + 1, sh, c_gt, e2);
     need = take - (int64_t)c_gt;
   } else {
-    unsigned int lo = mn;
-    unsigned long long hi = (unsigned long long)mx + 1;
-    while (hi - lo > 1) {
-      unsigned int mid = (unsigned int)(lo + ((hi - lo) >> 1));
-      unsigned int c, e;
-      count_at_or_above(keys, nk, mid, sh, c, e);
-      if ((int64_t)c >= take) lo = mid; else hi = mid;
-    }
-    vt = lo;
+    vt = search_keys<false>(keys, nk, mn, (unsigned long long)mx + 1, 0.0, take, sh);
     unsigned int c_gt, e2;
     if (vt == 0xffffffffu) c_gt = 0;
     else count_at_or_above(keys, nk, vt + 1, sh, c_gt, e2);
@@ -575,19 +579,123 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// numpy pairwise-sum "plan" for a row of n values: the leaves (<= 128 values
+// each) of numpy's split tree in left-to-right order plus a post-order
+// program (leaf index = push, -1 = add the top two).  Leaves are summed in
+// parallel, the short program is replayed by one thread: the same tree, so
+// the same rounding, as numpy's recursive pairwise_sum.
+// plan: [n_leaves, n_ops, (off, len) * n_leaves, ops * n_ops]
+// ---------------------------------------------------------------------------
+__host__ __device__ inline void pw_plan_walk(int64_t n, int32_t* plan, int32_t* n_leaves,
+                                             int32_t* n_ops) {
+  struct Frame { int64_t off, n; int state; };
+  Frame st[64];
+  int sp = 0;
+  int32_t nl = 0, no = 0;
+  st[0] = {0, n, 0};
+  // first pass counts; when plan != nullptr, also writes
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      if (plan) {
+        plan[2 + 2 * nl] = (int32_t)f.off;
+        plan[3 + 2 * nl] = (int32_t)f.n;
+      }
+      ++nl;
+      --sp;
+      continue;
+    }
+    int64_t half = f.n / 2;
+    half -= half % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      st[++sp] = {f.off, half, 0};
+    } else if (f.state == 1) {
+      f.state = 2;
+      st[++sp] = {f.off + half, f.n - half, 0};
+    } else {
+      --sp;
+    }
+  }
+  // second walk emits the post-order program (needs n_leaves for the offset)
+  if (plan) {
+    int32_t* ops = plan + 2 + 2 * nl;
+    int32_t leaf = 0;
+    sp = 0;
+    st[0] = {0, n, 0};
+    while (sp >= 0) {
+      Frame& f = st[sp];
+      if (f.n <= 128) {
+        ops[no++] = leaf++;
+        --sp;
+        continue;
+      }
+      int64_t half = f.n / 2;
+      half -= half % 8;
+      if (f.state == 0) {
+        f.state = 1;
+        st[++sp] = {f.off, half, 0};
+      } else if (f.state == 1) {
+        f.state = 2;
+        st[++sp] = {f.off + half, f.n - half, 0};
+      } else {
+        ops[no++] = -1;
+        --sp;
+      }
+    }
+    plan[0] = nl;
+    plan[1] = no;
+  } else {
+    no = 2 * nl - 1;
+  }
+  if (n_leaves) *n_leaves = nl;
+  if (n_ops) *n_ops = no;
+}
+
+__global__ void pw_plan_kernel(int64_t n, int32_t* plan) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) pw_plan_walk(n, plan, nullptr, nullptr);
+}
+
+// numpy pairwise_sum leaf (n <= 128) over contiguous smem values
+__device__ __forceinline__ float pw_leaf_smem(const float* a, int n) {
+  if (n < 8) {
+    float r = 0.0f;
+    for (int i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
+    return r;
+  }
+  float r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
+  float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __fadd_rn(res, a[i]);
+  return res;
+}
+
 template <bool SOFTMAX, bool SELECT>
 __global__ void __launch_bounds__(SS_THREADS)
     softsel_kernel(float* __restrict__ src, int64_t ld, int64_t rows, int64_t nk, double tau,
                    int64_t k_floor, float* __restrict__ probs_out, uint8_t* __restrict__ bits,
                    int32_t* __restrict__ counts, int32_t* __restrict__ fb_list,
-                   int32_t* __restrict__ fb_count) {
+                   int32_t* __restrict__ fb_count, const int32_t* __restrict__ plan_g,
+                   int plan_ints) {
   extern __shared__ __align__(16) float row[];
   __shared__ SelShared sh;
   __shared__ unsigned int scan_tmp[SS_WARPS];
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
+  const int64_t nk_pad = (nk + 3) & ~(int64_t)3;
+  int32_t* plan = reinterpret_cast<int32_t*>(row + nk_pad);
+  float* leafsum = reinterpret_cast<float*>(plan + plan_ints);
   float* g = src + r * ld;
   for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) row[j] = g[j];
+  if (SOFTMAX)
+    for (int j = threadIdx.x; j < plan_ints; j += SS_THREADS) plan[j] = plan_g[j];
   __syncthreads();
   if constexpr (SOFTMAX) {
     float lmax = -__int_as_float(0x7f800000);
@@ -595,7 +703,25 @@ __global__ void __launch_bounds__(SS_THREADS)
     const float mx = block_max(lmax, sh);
     for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) row[j] = np_expf(__fsub_rn(row[j], mx));
     __syncthreads();
-    if (threadIdx.x == 0) sh.total = __fadd_rn(0.0f, pw_smem(row, nk));
+    const int n_leaves = plan[0], n_ops = plan[1];
+    for (int i = threadIdx.x; i < n_leaves; i += SS_THREADS)
+      leafsum[i] = pw_leaf_smem(row + plan[2 + 2 * i], plan[3 + 2 * i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int32_t* ops = plan + 2 + 2 * n_leaves;
+      float stk[40];
+      int sp = 0;
+      for (int k = 0; k < n_ops; ++k) {
+        const int op = ops[k];
+        if (op >= 0) {
+          stk[sp++] = leafsum[op];
+        } else {
+          stk[sp - 2] = __fadd_rn(stk[sp - 2], stk[sp - 1]);
+          --sp;
+        }
+      }
+      sh.total = __fadd_rn(0.0f, stk[0]);
+    }
     __syncthreads();
     const float tot = sh.total;
     for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
@@ -723,10 +849,20 @@ static int64_t next_pow2(int64_t n) {
 
 constexpr int FB_GRID = 64;
 
-// select workspace: [fb_count int32 (256 B slot)] [fb_list int32 rows] [scratch u64 FB_GRID*npow2]
-static size_t select_ws_bytes(int64_t rows, int64_t nk) {
-  return 256 + align_up((size_t)rows * 4, 256) + (size_t)FB_GRID * (size_t)next_pow2(nk) * 8;
+static int64_t plan_ints_for(int64_t nk) {
+  int32_t nl = 0, no = 0;
+  pw_plan_walk(nk, nullptr, &nl, &no);
+  return 2 + 2 * (int64_t)nl + no;
 }
+
+// softsel workspace: [fb_count (256 B)] [pairwise plan] then, with selection,
+// [fb_list int32 rows] [bitonic scratch u64 FB_GRID * npow2(nk)]
+static size_t softsel_ws_bytes(int64_t rows, int64_t nk, bool select) {
+  size_t b = 256 + align_up((size_t)plan_ints_for(nk) * 4, 256);
+  if (select) b += align_up((size_t)rows * 4, 256) + (size_t)FB_GRID * (size_t)next_pow2(nk) * 8;
+  return b;
+}
+static size_t select_ws_bytes(int64_t rows, int64_t nk) { return softsel_ws_bytes(rows, nk, true); }
 
 static int check_tensor(const bsa_tensor* t, const char* name) {
   if (!t || !t->data) return fail(BSA_EINVAL, "%s: null tensor", name);
@@ -738,28 +874,41 @@ static int check_tensor(const bsa_tensor* t, const char* name) {
   return BSA_OK;
 }
 
+template <typename T, int VEC>
+static void launch_pool_v(const bsa_tensor* x, const Layout& L, bool gather, int64_t n,
+                          int32_t block, float* out, cudaStream_t st) {
+  const int d = (int)x->dim;
+  const int64_t nb = ceil_div(n, block);
+  const int lanes = std::min(32, (d + VEC - 1) / VEC);
+  const int rows_per_warp = 32 / lanes;
+  const int64_t warps = ceil_div(x->heads * nb, rows_per_warp);
+  const unsigned grid = (unsigned)ceil_div(warps, 8);
+  if (block - 1 > 128)
+    pool_kernel<T, VEC, true><<<grid, 256, 0, st>>>((const T*)x->data, x->stride_head,
+                                                    x->stride_token, x->heads, n, d, block, L,
+                                                    gather ? 1 : 0, out, nb);
+  else
+    pool_kernel<T, VEC, false><<<grid, 256, 0, st>>>((const T*)x->data, x->stride_head,
+                                                     x->stride_token, x->heads, n, d, block, L,
+                                                     gather ? 1 : 0, out, nb);
+}
+
 template <typename T>
 static int launch_pool_t(const bsa_tensor* x, const Layout& L, bool gather, int64_t n,
                          int32_t block, float* out, cudaStream_t st) {
   const int d = (int)x->dim;
-  const int64_t nb = ceil_div(n, block);
-  const bool vec_ok = (d % 4 == 0) && ((uintptr_t)x->data % (4 * sizeof(T)) == 0) &&
-                      ((x->stride_token * (int64_t)sizeof(T)) % (4 * sizeof(T)) == 0) &&
-                      ((x->stride_head * (int64_t)sizeof(T)) % (4 * sizeof(T)) == 0);
-  const int vec = vec_ok ? 4 : 1;
-  const int lanes = std::min(32, (d + vec - 1) / vec);
-  const int rows_per_warp = 32 / lanes;
-  const int64_t total = x->heads * nb;
-  const int64_t warps = ceil_div(total, rows_per_warp);
-  const int64_t grid = ceil_div(warps, 8);
-  if (vec_ok)
-    pool_kernel<T, 4><<<(unsigned)grid, 256, 0, st>>>(
-        (const T*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
-        gather ? 1 : 0, out, nb);
-  else
-    pool_kernel<T, 1><<<(unsigned)grid, 256, 0, st>>>(
-        (const T*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
-        gather ? 1 : 0, out, nb);
+  if (L.tokens() >= (1LL << 31)) return fail(BSA_EUNSUPPORTED, "sequence longer than 2^31 tokens");
+  auto aligned = [&](int vec) {
+    const size_t bytes = vec * sizeof(T);
+    return d % vec == 0 && (uintptr_t)x->data % bytes == 0 &&
+           (x->stride_token * (int64_t)sizeof(T)) % bytes == 0 &&
+           (x->stride_head * (int64_t)sizeof(T)) % bytes == 0;
+  };
+  // one warp-row per pooled row: lanes cover the head dim with 2 (d <= 64)
+  // or 4 (d <= 128) columns each, i.e. fully coalesced 128/256-byte rows
+  if (d <= 64 && aligned(2)) launch_pool_v<T, 2>(x, L, gather, n, block, out, st);
+  else if (aligned(4)) launch_pool_v<T, 4>(x, L, gather, n, block, out, st);
+  else launch_pool_v<T, 1>(x, L, gather, n, block, out, st);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
@@ -802,19 +951,32 @@ template <bool SOFTMAX, bool SELECT>
 static int launch_softsel(float* src, int64_t ld, int64_t rows, int64_t nk, double tau,
                           int64_t k_floor, float* probs_out, uint8_t* bits, int32_t* counts,
                           void* ws, cudaStream_t st) {
-  const size_t smem = align_up((size_t)nk * 4, 16);
+  if (!ws) return fail(BSA_EINVAL, "softmax/select: workspace required");
+  int32_t nl = 0, no = 0;
+  pw_plan_walk(nk, nullptr, &nl, &no);
+  const int plan_ints = 2 + 2 * nl + no;
+  const size_t smem = align_up((size_t)((nk + 3) & ~3LL) * 4 + (size_t)plan_ints * 4 +
+                                   (size_t)nl * 4, 16);
   if (smem > 200 * 1024)
     return fail(BSA_EUNSUPPORTED, "nk=%lld key blocks per row exceeds the on-chip row buffer",
                 (long long)nk);
   auto kern = softsel_kernel<SOFTMAX, SELECT>;
   BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int32_t* fb_count = (int32_t*)ws;
-  int32_t* fb_list = (int32_t*)((char*)ws + 256);
-  unsigned long long* scratch =
-      (unsigned long long*)((char*)ws + 256 + align_up((size_t)rows * 4, 256));
+  char* w = (char*)ws;
+  int32_t* fb_count = (int32_t*)w;
+  w += 256;
+  int32_t* plan = (int32_t*)w;
+  w += align_up((size_t)plan_ints * 4, 256);
+  int32_t* fb_list = (int32_t*)w;
+  w += align_up((size_t)rows * 4, 256);
+  unsigned long long* scratch = (unsigned long long*)w;
+  if (SOFTMAX) {
+    pw_plan_kernel<<<1, 1, 0, st>>>(nk, plan);
+    BSA_LAUNCH_CHECK();
+  }
   if (SELECT) BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
   kern<<<(unsigned)rows, SS_THREADS, smem, st>>>(src, ld, rows, nk, tau, k_floor, probs_out, bits,
-                                                  counts, fb_list, fb_count);
+                                                  counts, fb_list, fb_count, plan, plan_ints);
   BSA_LAUNCH_CHECK();
   if (SELECT) {
     const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
@@ -840,37 +1002,43 @@ int bsa_block_pool(const bsa_tensor* x, const bsa_layout* patch_gather, int32_t 
 }
 
 size_t bsa_pooled_scores_workspace(int64_t heads, int64_t nq, int64_t nk) {
-  (void)heads; (void)nq; (void)nk;
-  return 256;
+  return softsel_ws_bytes(heads * nq, nk, false);
 }
 
 int bsa_pooled_scores(const float* qp, const float* kp, int64_t heads, int64_t nq, int64_t nk,
                       int64_t dim, float scale, float* probs, void* ws, size_t ws_bytes,
                       void* stream) {
-  (void)ws; (void)ws_bytes;
   if (!qp || !kp || !probs) return fail(BSA_EINVAL, "pooled_scores: null pointer");
   if (heads < 1 || nq < 1 || nk < 1 || dim < 1)
     return fail(BSA_EINVAL, "pooled_scores: zero-sized dimension");
+  if (!ws || ws_bytes < softsel_ws_bytes(heads * nq, nk, false))
+    return fail(BSA_EINVAL, "pooled_scores: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_scores(qp, kp, heads, nq, nk, dim, scale, probs, nk, st);
   if (rc) return rc;
   return launch_softsel<true, false>(probs, nk, heads * nq, nk, 0.0, 1, nullptr, nullptr,
-                                     nullptr, nullptr, st);
+                                     nullptr, ws, st);
+}
+
+size_t bsa_row_softmax_workspace(int64_t rows, int64_t cols) {
+  return softsel_ws_bytes(rows, cols, false);
 }
 
 int bsa_row_softmax(const float* a, int64_t rows, int64_t cols, float scale, float* out,
-                    void* stream) {
+                    void* ws, size_t ws_bytes, void* stream) {
   if (!a || !out) return fail(BSA_EINVAL, "row_softmax: null pointer");
   if (rows < 1 || cols < 1)
     return fail(BSA_EINVAL, "a has a zero-sized dimension: (%lld, %lld)", (long long)rows,
                 (long long)cols);
+  if (!ws || ws_bytes < softsel_ws_bytes(rows, cols, false))
+    return fail(BSA_EINVAL, "row_softmax: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = rows * cols;
   scale_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 32), 256, 0, st>>>(a, n, scale,
                                                                                      out);
   BSA_LAUNCH_CHECK();
   return launch_softsel<true, false>(out, cols, rows, cols, 0.0, 1, nullptr, nullptr, nullptr,
-                                     nullptr, st);
+                                     ws, st);
 }
 
 size_t bsa_select_workspace(int64_t heads, int64_t nq, int64_t nk) {

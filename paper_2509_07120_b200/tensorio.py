@@ -22,7 +22,9 @@ def row_softmax(a, scale: float = 1.0):
         raise ValueError(f"row_softmax expects a 2-D input, got shape {tuple(t.shape)}")
     t = t.contiguous()
     out = torch.empty_like(t)
-    N.check(N.lib().bsa_row_softmax(t.data_ptr(), t.shape[0], t.shape[1],
-                                    float(np.float32(scale)), out.data_ptr(), N.stream_ptr()),
+    L = N.lib()
+    ws = N.workspace(L.bsa_row_softmax_workspace(t.shape[0], t.shape[1]), t.device)
+    N.check(L.bsa_row_softmax(t.data_ptr(), t.shape[0], t.shape[1], float(np.float32(scale)),
+                              out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
             "row_softmax")
     return _out(out, was_np)
