@@ -1,6 +1,8 @@
 // bsa_attn.cuh -- geometry and key-stream helpers shared by the attention kernels.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "bsa_common.cuh"
 
 namespace bsa {
@@ -93,7 +95,10 @@ int launch_simt_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_te
 struct TcArgs {
   const __nv_bfloat16* qp;   // packed partitioned (H, T, 64)
   const __nv_bfloat16* kp;
-  const __nv_bfloat16* vp;
+  const void* vp;             // V: bf16, or fp16 scaled by 2^v_shift[h] (v_f16)
+  const int32_t* v_shift;
+  int v_f16;                  // fp16 P x fp16 V variant
+  int exp_poly;               // pairs of every 8 computed by the FMA-pipe exp2
   void* out;
   int out_bf16;
   int permuted_out;          // write rows in partitioned order

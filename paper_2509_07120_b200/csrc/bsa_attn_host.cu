@@ -11,6 +11,7 @@
 //   area_kernel      BlockMask.selected_area (maskpred.py:97-101).
 //   csr kernels      CSR view of the mask.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bsa_attn.cuh"
 
@@ -48,6 +49,54 @@ __global__ void pack_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int
     } else {
       *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = *reinterpret_cast<const uint4*>(p);
     }
+  }
+}
+
+// per-head max |v| (as float bits: non-negative floats order like integers)
+template <typename T>
+__global__ void vamax_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int64_t ntok, int d,
+                             unsigned int* __restrict__ amax) {
+  const int64_t h = blockIdx.y;
+  unsigned int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntok * d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d, c = i - r * d;
+    m = max(m, __float_as_uint(fabsf(to_f32(x[h * sH + r * sT + c]))));
+  }
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(&amax[h], m);
+}
+
+// V -> fp16 in partitioned order, scaled by 2^shift[h] so that max|v| lands in
+// [2^14, 2^15) (power-of-two scaling is exact; the epilogue divides it out)
+template <typename T>
+__global__ void pack_v_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int64_t H,
+                              int64_t ntok, int d, Layout L, int permuted,
+                              const unsigned int* __restrict__ amax, int32_t* __restrict__ shift,
+                              __half* __restrict__ out) {
+  const int64_t per_row = d / 8;
+  const int64_t total = H * ntok * per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c8 = i % per_row;
+    const int64_t hr = i / per_row;
+    const int64_t r = hr % ntok, h = hr / ntok;
+    const unsigned int am = amax[h];
+    const int e = (am >> 23) == 0 ? -126 : (int)(am >> 23) - 127;
+    int sft = am == 0u ? 0 : 14 - e;
+    sft = max(-100, min(100, sft));
+    if (r == 0 && c8 == 0) shift[h] = sft;
+    const float mul = exp2f((float)sft);
+    const int64_t src = permuted ? r : L.part_src(r);
+    const T* p = x + h * sH + src * sT + c8 * 8;
+    uint4 o;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      __half2 t = __floats2half2_rn(to_f32(p[2 * k]) * mul, to_f32(p[2 * k + 1]) * mul);
+      ow[k] = *reinterpret_cast<uint32_t*>(&t);
+    }
+    *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = o;
   }
 }
 
@@ -171,8 +220,10 @@ static int choose_path(const AttnGeom& G, int32_t in_dtype, int32_t flags) {
 }
 
 struct TcWorkspace {
-  __nv_bfloat16 *qp, *kp, *vp;
-  int32_t *items, *counter, *counts;
+  __nv_bfloat16 *qp, *kp;
+  void* vp;
+  int32_t *items, *counter, *counts, *vshift;
+  unsigned int* vamax;
   size_t bytes;
 };
 
@@ -184,10 +235,12 @@ static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G) {
   const int64_t n_items = G.H * (nst + G.nq);
   w.qp = (__nv_bfloat16*)p; p += tens;
   w.kp = (__nv_bfloat16*)p; p += tens;
-  w.vp = (__nv_bfloat16*)p; p += tens;
+  w.vp = (void*)p; p += tens;
   w.items = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
   w.counter = (int32_t*)p; p += 256;
   w.counts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq) * 4, 256);
+  w.vshift = (int32_t*)p; p += align_up((size_t)G.H * 4, 256);
+  w.vamax = (unsigned int*)p; p += align_up((size_t)G.H * 4, 256);
   w.bytes = (size_t)(p - (char*)base);
   return w;
 }
@@ -207,6 +260,33 @@ static int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __n
   else
     pack_kernel<float><<<grid, 256, 0, st>>>((const float*)x->data, x->stride_head,
                                              x->stride_token, G.H, G.T, G.d, G.L, permuted, out);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+static int launch_pack_v(const bsa_tensor* x, const AttnGeom& G, int permuted, unsigned int* amax,
+                         int32_t* shift, __half* out, cudaStream_t st) {
+  const bool bf = x->dtype == BSA_BF16;
+  const size_t es = bf ? 2 : 4;
+  if ((uintptr_t)x->data % 16 || (x->stride_token * es) % 16 || (x->stride_head * es) % 16)
+    return fail(BSA_EUNSUPPORTED, "q/k/v must be 16-byte aligned for the tensor-core path");
+  BSA_CUDA_TRY(cudaMemsetAsync(amax, 0, (size_t)G.H * 4, st));
+  dim3 ag((unsigned)std::min<int64_t>(ceil_div(G.T * G.d, 256), 64), (unsigned)G.H);
+  const int64_t total = G.H * G.T * (G.d / 8);
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  if (bf) {
+    vamax_kernel<__nv_bfloat16><<<ag, 256, 0, st>>>((const __nv_bfloat16*)x->data, x->stride_head,
+                                                    x->stride_token, G.T, G.d, amax);
+    pack_v_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x->data,
+                                                       x->stride_head, x->stride_token, G.H, G.T,
+                                                       G.d, G.L, permuted, amax, shift, out);
+  } else {
+    vamax_kernel<float><<<ag, 256, 0, st>>>((const float*)x->data, x->stride_head,
+                                            x->stride_token, G.T, G.d, amax);
+    pack_v_kernel<float><<<grid, 256, 0, st>>>((const float*)x->data, x->stride_head,
+                                               x->stride_token, G.H, G.T, G.d, G.L, permuted,
+                                               amax, shift, out);
+  }
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
@@ -274,9 +354,21 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   if (!ws) return fail(BSA_EINVAL, "sparse_attention: workspace required");
   TcWorkspace W = tc_ws_layout(ws, G);
   if (ws_bytes < W.bytes) return fail(BSA_EINVAL, "sparse_attention: workspace too small");
+  // kernel variant: exp2 split between MUFU and the FMA pipe, P/V precision
+  static int env_poly = -2, env_f16 = -2;
+  if (env_poly == -2) {
+    const char* e = getenv("BSA_TC_EXP_POLY");
+    env_poly = e ? atoi(e) : -1;
+    const char* f = getenv("BSA_TC_F16P");
+    env_f16 = f ? atoi(f) : -1;
+  }
+  const int v_f16 = env_f16 >= 0 ? env_f16 : 0;
+  const int exp_poly = env_poly >= 0 ? env_poly : 0;
   rc = launch_pack(q, G, inputs_permuted, W.qp, st);
   if (!rc) rc = launch_pack(k, G, inputs_permuted, W.kp, st);
-  if (!rc) rc = launch_pack(v, G, inputs_permuted, W.vp, st);
+  if (!rc)
+    rc = v_f16 ? launch_pack_v(v, G, inputs_permuted, W.vamax, W.vshift, (__half*)W.vp, st)
+               : launch_pack(v, G, inputs_permuted, (__nv_bfloat16*)W.vp, st);
   if (rc) return rc;
   const int64_t rows = G.H * G.nq;
   if (!counts) {
@@ -301,6 +393,9 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   a.qp = W.qp;
   a.kp = W.kp;
   a.vp = W.vp;
+  a.v_shift = W.vshift;
+  a.v_f16 = v_f16;
+  a.exp_poly = exp_poly;
   a.out = out;
   a.out_bf16 = out_dtype == BSA_BF16;
   a.permuted_out = inputs_permuted;

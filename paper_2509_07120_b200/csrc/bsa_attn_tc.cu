@@ -15,11 +15,13 @@
 //               P read from TMEM (A operand) and V from smem (MN-major B);
 //               tcgen05.commit -> mbarriers.
 //   warps 0-3   softmax / correction / epilogue: thread t owns query row t
-//               (TMEM lane t): tcgen05.ld the S row, mask ragged chunks, exp2
-//               (half on MUFU, half as an FMA-pipe polynomial, f32x2 packed
-//               math), lazy (2^8) rescaling of O in TMEM, bf16 P back to TMEM
-//               with tcgen05.st, final O / l to global memory in the caller's
-//               (interleaved) token order.
+//               (TMEM lane t): tcgen05.ld the S row, mask ragged chunks, packed
+//               ex2.approx.f16x2 (two exps per MUFU op; the argument is formed
+//               in fp32 with f32x2 FMAs), lazy (2^8) rescaling of O in TMEM,
+//               fp16 P back to TMEM with tcgen05.st, final O / l to global
+//               memory in the caller's (interleaved) token order.
+// P x V runs as fp16 x fp16 -> fp32: V is stored as fp16 scaled by a per-head
+// power of two (exact, undone in the epilogue) so its range is safe.
 // TMEM (256 of 512 columns per CTA): S0|S1 (2x64) P0|P1 (2x32) O (64).
 #include <cuda.h>
 
@@ -159,14 +161,33 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
+  uint32_t y;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t cvt_h2(float lo, float hi) {
+  uint32_t y;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(hi), "f"(lo));
+  return y;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t y;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(y) : "r"(a), "r"(b));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 // 2^x for a pair on the FMA pipe (x <= ~8): round-to-nearest split
 // x = j + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel err 7.7e-5,
-// far below the bf16 rounding of P), exponent added as an integer.
+// far below the 16-bit rounding of P), exponent added as an integer.
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
-  const float2 magic = make_float2(12582912.0f, 12582912.0f);
-  const float2 t = __fadd2_rn(x, magic);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
   const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
   float2 p = __ffma2_rn(make_float2(0.05508868f, 0.05508868f), f,
@@ -177,9 +198,36 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
+
+// P = exp2(s * scale_log2 - m) for one 64-column S row, streamed to TMEM as
+// packed 16-bit pairs (2 x tcgen05.st.32x32b.x16); returns the fp32 row sum.
+// The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
+// the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
+// V) instead of bf16 P.
+template <int POLY, bool F16P>
+__device__ __forceinline__ float exp_tile(const float (&s)[64], float sl2, float m,
+                                          uint32_t p_taddr) {
+  const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
+  float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                  make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sl2v,
+                                  nmv);
+      float2 p;
+      if ((e & 7) < POLY) p = exp2_poly2(x);
+      else p = make_float2(ex2(x.x), ex2(x.y));
+      rs[e & 3] = __fadd2_rn(rs[e & 3], p);
+      if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
+      else r[e] = pack_bf16(p.x, p.y);
+    }
+    tmem_st16(p_taddr + c * 16, r);
+  }
+  const float2 t = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
+  return t.x + t.y;
 }
 
 // UMMA shared-memory descriptor: SWIZZLE_128B, version 1 (sm_100).
@@ -192,9 +240,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)2 << 61;
   return d;
 }
-// instruction descriptor kind::f16: bf16 x bf16 -> f32
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+// instruction descriptor kind::f16 -> f32 accumulate; fmt 0 = f16, 1 = bf16
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, int fmt) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)b_mn_major << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
@@ -254,6 +302,7 @@ __device__ __forceinline__ int chunk_len(const Item& it, int c) {
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+template <int POLY, bool F16P>
 __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
@@ -348,8 +397,8 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     // ======================= MMA issuer =======================
     if (lane == 0) {
       uint32_t it = 0, g = 0;
-      const uint32_t id_s = idesc_bf16(128, 64, 0);
-      const uint32_t id_pv = idesc_bf16(128, 64, 1);
+      const uint32_t id_s = idesc_f16(128, 64, 0, 1);   // bf16 Q x bf16 K
+      const uint32_t id_pv = idesc_f16(128, 64, 1, F16P ? 0 : 1);  // P x V (fp16 | bf16)
       while (true) {
         const uint32_t slot = it & 1;
         mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
@@ -476,32 +525,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
         // P buffer sb is free once the PV that read it (two tiles ago) is done
         if (gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
         tc_fence_after();
-        // P = exp2(s * scale_log2 - m) as packed bf16 pairs, streamed to TMEM;
-        // odd pairs on MUFU.EX2, even pairs as an FMA-pipe polynomial
-        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
-        float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                        make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t r[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]),
-                                        sl2v, nmv);
-            float2 p;
-            if (e & 1) {
-              p = make_float2(ex2(x.x), ex2(x.y));
-            } else {
-              p = exp2_poly2(x);
-            }
-            rs[e & 3] = __fadd2_rn(rs[e & 3], p);
-            r[e] = pack_bf16(p.x, p.y);
-          }
-          tmem_st16(tmem + lane_off + TM_P + sb * 32 + c * 16, r);
-        }
-        const float2 r01 = __fadd2_rn(rs[0], rs[1]), r23 = __fadd2_rn(rs[2], rs[3]);
-        const float2 rr = __fadd2_rn(r01, r23);
-        l += rr.x + rr.y;
+        l += exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + TM_P + sb * 32);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -522,7 +546,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       if (row < I.rows) {
         const int64_t pr = I.row0 + row;
         const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
-        const float inv = 1.0f / l;
+        const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / l;
         if (A.out_bf16) {
           uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + (I.h * G.T + dst) * D);
 #pragma unroll
@@ -579,14 +603,15 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, int box_rows) {
+static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, int box_rows,
+                    CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)tc::D, (cuuint64_t)T, (cuuint64_t)H};
   cuuint64_t strides[2] = {(cuuint64_t)tc::D * 2, (cuuint64_t)T * tc::D * 2};
   cuuint32_t box[3] = {(cuuint32_t)tc::D, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+  CUresult r = enc(map, dt, 3, const_cast<void*>(base), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -609,10 +634,10 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   CUtensorMap mq, mk, mv;
   int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);
   if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
-  if (!rc) rc = make_map(&mv, a.vp, G.H, G.T, tc::CH);
+  if (!rc)
+    rc = make_map(&mv, a.vp, G.H, G.T, tc::CH,
+                  a.v_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   if (rc) return rc;
-  BSA_CUDA_TRY(cudaFuncSetAttribute(tc::bsa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::SMEM_BYTES));
   int dev = 0, sms = 148;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -621,8 +646,21 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
                              : a.n_items;
   const int grid =
       (int)std::min<int64_t>((int64_t)sms * tc::CTAS_PER_SM, std::max<int64_t>(1, n_work));
+  auto kern = tc::bsa_tc_kernel<0, false>;
+  switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {
+    case 0: kern = tc::bsa_tc_kernel<0, false>; break;
+    case 1: kern = tc::bsa_tc_kernel<1, false>; break;
+    case 2: kern = tc::bsa_tc_kernel<2, false>; break;
+    case 3: kern = tc::bsa_tc_kernel<3, false>; break;
+    case 4: kern = tc::bsa_tc_kernel<4, false>; break;
+    case 16: kern = tc::bsa_tc_kernel<0, true>; break;
+    case 18: kern = tc::bsa_tc_kernel<2, true>; break;
+    default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
+  }
+  BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::SMEM_BYTES));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
-  tc::bsa_tc_kernel<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
+  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
   BSA_LAUNCH_CHECK();
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
   return BSA_OK;
