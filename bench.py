@@ -338,6 +338,15 @@ def cpu_reference(a, budget_s=20.0):
     done, t_attn = 0, 0.0
     t_start = time.perf_counter()
     chunk = max(1, threads)
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    # one BLAS thread per worker thread (the reference's best CPU setting:
+    # sparse_attention(threads=N) with OPENBLAS_NUM_THREADS=1)
+    ctx = threadpool_limits(limits=1, user_api="blas") if threadpool_limits else None
+    if ctx:
+        ctx.__enter__()
     while done < len(sample) and (time.perf_counter() - t_start) < budget_s * 0.6:
         items = [(0, qb) for qb in sample[done:done + chunk]]
         t1 = time.perf_counter()
@@ -345,6 +354,8 @@ def cpu_reference(a, budget_s=20.0):
                                      threads=threads, inputs_permuted=True, work=items)
         t_attn += time.perf_counter() - t1
         done += len(items)
+    if ctx:
+        ctx.__exit__(None, None, None)
     per_qblock = t_attn / max(done, 1)
     # special rows: 256-row chunk sample over all keys
     t2 = time.perf_counter()
