@@ -14,6 +14,9 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libbsa.so")
+# kernel A/B experiments only (scripts/): load another in-tree build of the library
+if os.environ.get("BSA_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_PKG, "csrc", "build", os.environ["BSA_LIB_VARIANT"], "libbsa.so")
 
 BSA_OK, BSA_EINVAL, BSA_EUNSUPPORTED, BSA_ECUDA = 0, 1, 2, 3
 BSA_F32, BSA_BF16 = 0, 1

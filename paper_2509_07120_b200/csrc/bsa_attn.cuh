@@ -110,6 +110,7 @@ struct TcArgs {
   float scale_log2;          // scale * log2(e)
   int shard, num_shards;
   int timing;                // record events around the launch (bsa_last_kernel_ms)
+  unsigned long long* trace; // debug: clock64 per pipeline event of CTA 0 (BSA_TC_TRACE), or null
 };
 
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);

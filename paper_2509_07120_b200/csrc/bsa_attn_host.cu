@@ -408,6 +408,14 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   a.shard = shard;
   a.num_shards = num_shards;
   a.timing = (flags & BSA_FLAG_TIMING) != 0;
+  a.trace = nullptr;
+  if (getenv("BSA_TC_TRACE")) {  // debug pipeline trace of CTA 0 (scripts/trace_analyze.py)
+    static unsigned long long* tbuf = nullptr;
+    const size_t tbytes = 20 * 512 * sizeof(unsigned long long);
+    if (!tbuf) BSA_CUDA_TRY(cudaMalloc(&tbuf, tbytes));
+    BSA_CUDA_TRY(cudaMemsetAsync(tbuf, 0, tbytes, st));
+    a.trace = tbuf;
+  }
   return launch_tc_attention(G, a, st);
 }
 

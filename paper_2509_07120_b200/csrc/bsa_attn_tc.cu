@@ -25,33 +25,71 @@
 // TMEM (256 of 512 columns per CTA): S0|S1 (2x64) P0|P1 (2x32) O (64).
 #include <cuda.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "bsa_attn.cuh"
 
 namespace bsa {
 namespace tc {
 
-constexpr int BQ = 128, CH = 64, D = 64, NST = 4;
+#ifndef BSA_TC_EXPERIMENT
+#define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
+#endif
+#ifndef BSA_TC_NK
+#define BSA_TC_NK 6
+#endif
+#ifndef BSA_TC_NV
+#define BSA_TC_NV 5
+#endif
+#ifndef BSA_TC_VLAG
+#define BSA_TC_VLAG 2
+#endif
+#ifndef BSA_TC_PVLAG
+#define BSA_TC_PVLAG 2
+#endif
+// K and V rings are separate: a K tile is released as soon as its S = QK^T
+// MMA completes, a V tile only after its PV MMA, so the producer issues K
+// VLAG tiles ahead of V and the MMA issuer runs S PVLAG tiles ahead of PV
+// (S(j) is computed while the softmax warps still work on tile j-1 or j-2).
+constexpr int BQ = 128, CH = 64, D = 64;
+constexpr int NK = BSA_TC_NK, NV = BSA_TC_NV, VLAG = BSA_TC_VLAG, PVLAG = BSA_TC_PVLAG;
 constexpr int Q_BYTES = BQ * D * 2;          // 16 KB
 constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB (one K or V tile)
 constexpr int NUM_THREADS = 192;
 constexpr int CTAS_PER_SM = 2;
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-constexpr int OFF_V = OFF_K + NST * CHUNK_BYTES;
-constexpr int OFF_BAR = OFF_V + NST * CHUNK_BYTES;
+constexpr int OFF_Q = 0;                     // one Q tile (refilled between work items)
+constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
+constexpr int OFF_BAR = OFF_V + NV * CHUNK_BYTES;
 constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;  // barriers/ring + alignment slack
+static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert(PVLAG >= 1 && PVLAG <= 2, "S is double buffered in TMEM");
 constexpr uint32_t TMEM_COLS = 256;
 
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = 192;
+#ifndef BSA_TC_QTMEM
+#define BSA_TC_QTMEM 1
+#endif
+// QT: the Q tile lives in TMEM and S = Q K^T reads it as the A operand
+// (tcgen05.mma .ts form), so per key tile the tensor core reads only K and V
+// from shared memory; P is written over its own S buffer.  Otherwise Q is a
+// TMA-loaded shared-memory operand and P has its own TMEM buffers.
+constexpr bool QT = BSA_TC_QTMEM != 0;
+constexpr int PV_LAG = QT ? 1 : PVLAG;  // QT: S(j) reuses the buffer PV(j-2) read
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = QT ? 128 : 192, TM_Q = 192;
+__host__ __device__ constexpr uint32_t p_col(uint32_t sb) {
+  return QT ? TM_S + sb * 64 : TM_P + sb * 32;
+}
 
 // barrier slots (8 bytes each) inside the barrier region
 enum {
-  B_QFULL = 0,              // [2]
-  B_QEMPTY = 2,             // [2]
-  B_KFULL = 4,              // [NST]
-  B_VFULL = 4 + NST,        // [NST]
-  B_KVEMPTY = 4 + 2 * NST,  // [NST]
-  B_SFULL = 4 + 3 * NST,    // [2]
+  B_QFULL = 0,              // [1]
+  B_QEMPTY = 1,             // [1]
+  B_KFULL = 2,              // [NK]
+  B_KEMPTY = B_KFULL + NK,  // [NK]
+  B_VFULL = B_KEMPTY + NK,  // [NV]
+  B_VEMPTY = B_VFULL + NV,  // [NV]
+  B_SFULL = B_VEMPTY + NV,  // [2]
   B_SEMPTY = B_SFULL + 2,   // [2]
   B_PFULL = B_SEMPTY + 2,   // [2]
   B_PFREE = B_PFULL + 2,    // [2]
@@ -72,7 +110,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+#ifndef BSA_TC_WAIT
+#define BSA_TC_WAIT 1
+#endif
+// mbarrier phase wait.  0: try_wait with a suspend-time hint (the thread may
+// sleep; slow wake-up), 1: try_wait without hint (hardware-bounded blocking
+// poll), 2: test_wait spin.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if BSA_TC_WAIT == 0
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
@@ -80,6 +125,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity), "r"(0x989680u)
       : "memory");
+#elif BSA_TC_WAIT == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -95,6 +157,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+// one lane of a converged warp (elect.sync): keeps the caller warp-uniform
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -299,6 +369,23 @@ __device__ __forceinline__ int chunk_len(const Item& it, int c) {
   return c == it.nchunks - 1 ? it.last_len : CH;
 }
 
+// debug pipeline trace (BSA_TC_TRACE): clock64 of event `ev` for key tile `idx`
+// of CTA 0; TRACE_TILES tiles per event
+constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
+// Compiled in only with -DBSA_TC_TRACE_BUILD: the clock reads split the
+// scheduler's basic blocks and cost ~20% in the production kernel.
+#ifdef BSA_TC_TRACE_BUILD
+#define BSA_TR(ev, idx)                                                              \
+  do {                                                                               \
+    if (A.trace && blockIdx.x == 0 && (idx) < (uint32_t)TRACE_TILES)                  \
+      A.trace[(ev) * TRACE_TILES + (idx)] = (unsigned long long)clock64();           \
+  } while (0)
+#else
+#define BSA_TR(ev, idx) \
+  do {                  \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -317,9 +404,9 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
+    mbar_init(BAR(B_QFULL), QT ? 4 : 1);
+    mbar_init(BAR(B_QEMPTY), 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(BAR(B_QFULL + i), 1);
-      mbar_init(BAR(B_QEMPTY + i), 1);
       mbar_init(BAR(B_SFULL + i), 1);
       mbar_init(BAR(B_SEMPTY + i), 4);
       mbar_init(BAR(B_PFULL + i), 4);
@@ -327,10 +414,13 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       mbar_init(BAR(B_IFULL + i), 1);
       mbar_init(BAR(B_IEMPTY + i), 5);
     }
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < NK; ++s) {
       mbar_init(BAR(B_KFULL + s), 1);
+      mbar_init(BAR(B_KEMPTY + s), 1);
+    }
+    for (int s = 0; s < NV; ++s) {
       mbar_init(BAR(B_VFULL + s), 1);
-      mbar_init(BAR(B_KVEMPTY + s), 1);
+      mbar_init(BAR(B_VEMPTY + s), 1);
     }
     mbar_init(BAR(B_OFULL), 1);
     mbar_init(BAR(B_OEMPTY), 4);
@@ -356,100 +446,150 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards : A.n_items;
 
   if (warp == 4) {
-    // ======================= producer =======================
-    if (lane == 0) {
-      uint32_t it = 0, g = 0;
-      while (true) {
-        const int64_t w = atomicAdd(A.work_counter, 1);
-        int32_t code = -1;
-        if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
-        const uint32_t slot = it & 1;
-        mbar_wait(BAR(B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
+    // ======================= producer (whole warp; one elected lane issues) =====
+    // Control flow and operands are warp-uniform, so they live in uniform
+    // registers and the TMA issue needs no per-instruction broadcast loop.
+    // Key tile j of the running stream: K(j) is issued VLAG tiles before V(j).
+    uint32_t it = 0, gk = 0, gv = 0;
+    int64_t vq[VLAG + 1];  // key-chunk starts of the K tiles whose V is pending
+    while (true) {
+      int64_t w = 0;
+      if (lane == 0) w = atomicAdd(A.work_counter, 1);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      int32_t code = -1;
+      if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
+      const uint32_t slot = it & 1;
+      mbar_wait(BAR(B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
+      if (elect_one()) {
         item_ring[slot] = code;
         mbar_arrive(BAR(B_IFULL + slot));
-        if (code < 0) break;
-        const Item I = decode(G, code, A.counts, A.bits);
-        mbar_wait(BAR(B_QEMPTY + slot), ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(BAR(B_QFULL + slot), Q_BYTES);
-        tma_load_3d(sbase + OFF_Q + slot * Q_BYTES, &tm_q, BAR(B_QFULL + slot), 0, (int)I.row0,
-                    (int)I.h);
-        const uint8_t* mrow =
-            I.qb >= 0 ? A.bits + (I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
-        KeyChunker ck(G, I.qb, mrow, CH);
-        for (int j = 0; j < I.nchunks; ++j, ++g) {
-          const uint32_t st = g % NST;
-          mbar_wait(BAR(B_KVEMPTY + st), ((g / NST) & 1) ^ 1);
-          int64_t s0;
-          int l0;
-          ck.next(s0, l0);
-          mbar_expect_tx(BAR(B_KFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0,
-                      (int)I.h);
+      }
+      __syncwarp();
+      if (code < 0) break;
+      const Item I = decode(G, code, A.counts, A.bits);
+      if constexpr (!QT) {
+        mbar_wait(BAR(B_QEMPTY), (it & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(BAR(B_QFULL), Q_BYTES);
+          tma_load_3d(sbase + OFF_Q, &tm_q, BAR(B_QFULL), 0, (int)I.row0, (int)I.h);
+        }
+        __syncwarp();
+      }
+      const uint8_t* mrow =
+          I.qb >= 0 ? A.bits + (I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
+      KeyChunker ck(G, I.qb, mrow, CH);
+      auto load_v = [&](int64_t s0) {
+        const uint32_t st = gv % NV;
+        mbar_wait(BAR(B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
+        if (elect_one()) {
           mbar_expect_tx(BAR(B_VFULL + st), CHUNK_BYTES);
           tma_load_3d(sbase + OFF_V + st * CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, (int)s0,
                       (int)I.h);
         }
-        ++it;
-      }
-    }
-    __syncwarp();
-  } else if (warp == 5) {
-    // ======================= MMA issuer =======================
-    if (lane == 0) {
-      uint32_t it = 0, g = 0;
-      const uint32_t id_s = idesc_f16(128, 64, 0, 1);   // bf16 Q x bf16 K
-      const uint32_t id_pv = idesc_f16(128, 64, 1, F16P ? 0 : 1);  // P x V (fp16 | bf16)
-      while (true) {
-        const uint32_t slot = it & 1;
-        mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
-        const int32_t code = item_ring[slot];
-        mbar_arrive(BAR(B_IEMPTY + slot));
-        if (code < 0) break;
-        const Item I = decode(G, code, A.counts, A.bits);
-        const int ntiles = I.nchunks;
-        mbar_wait(BAR(B_QFULL + slot), (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qaddr = sbase + OFF_Q + slot * Q_BYTES;
-        auto issue_pv = [&](uint32_t gg, int jj) {
-          const uint32_t st = gg % NST, pb = gg & 1;
-          mbar_wait(BAR(B_PFULL + pb), (gg >> 1) & 1);
-          mbar_wait(BAR(B_VFULL + st), (gg / NST) & 1);
-          if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t vaddr = sbase + OFF_V + st * CHUNK_BYTES;
+        __syncwarp();
+        ++gv;
+      };
+      for (int j = 0; j < I.nchunks; ++j) {
+        const uint32_t st = gk % NK;
+        int64_t s0;
+        int l0;
+        ck.next(s0, l0);
+        mbar_wait(BAR(B_KEMPTY + st), ((gk / NK) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(BAR(B_KFULL + st), CHUNK_BYTES);
+          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0,
+                      (int)I.h);
+          BSA_TR(0, gk);
+        }
+        __syncwarp();
+        ++gk;
 #pragma unroll
-          for (int k = 0; k < CH / 16; ++k) {
-            const uint64_t bd = sdesc(vaddr + k * 2048, 8192, 1024);
-            mma_ts(tmem + TM_O, tmem + TM_P + pb * 32 + k * 8, bd, id_pv,
-                   (jj > 0 || k > 0) ? 1u : 0u);
-          }
+        for (int q = VLAG; q > 0; --q) vq[q] = vq[q - 1];
+        vq[0] = s0;
+        if (j >= VLAG) load_v(vq[VLAG]);
+      }
+      // drain the V tiles still pending for this item
+#pragma unroll
+      for (int q = VLAG - 1; q >= 0; --q)
+        if (q < I.nchunks) load_v(vq[q]);
+      ++it;
+    }
+  } else if (warp == 5) {
+    // ======================= MMA issuer (whole warp; one elected lane issues) ===
+    // Shared-memory descriptors are built once; per tile only the stage offset
+    // (address >> 4, no carry out of the 14-bit field: smem < 256 KB) is added.
+    // S(j) is issued as soon as K(j) and the S buffer are ready; PV(j) trails
+    // it by PVLAG tiles.
+    uint32_t it = 0, gs = 0, gp = 0;
+    const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
+    const uint32_t id_pv = idesc_f16(128, 64, 1, F16P ? 0 : 1);       // P x V (fp16 | bf16)
+    const uint64_t dq = sdesc(sbase + OFF_Q, 16, 1024);
+    const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024);
+    const uint64_t dv0 = sdesc(sbase + OFF_V, 8192, 1024);
+    while (true) {
+      const uint32_t slot = it & 1;
+      mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
+      const int32_t code = item_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(BAR(B_IEMPTY + slot));
+      if (code < 0) break;
+      const Item I = decode(G, code, A.counts, A.bits);
+      const int ntiles = I.nchunks;
+      mbar_wait(BAR(B_QFULL), it & 1);
+      tc_fence_after();
+      auto issue_pv = [&](int jj) {
+        const uint32_t sv = gp % NV, pb = gp & 1;
+        mbar_wait(BAR(B_PFULL + pb), (gp >> 1) & 1);
+        mbar_wait(BAR(B_VFULL + sv), (gp / NV) & 1);
+        if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dv = dv0 + (uint64_t)((sv * CHUNK_BYTES) >> 4);
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k)
+            if (BSA_TC_EXPERIMENT != 2) mma_ts(tmem + TM_O, tmem + p_col(pb) + k * 8, dv + (uint64_t)(k * (2048 >> 4)),
+                   id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(B_PFREE + pb));
-          tc_commit(BAR(B_KVEMPTY + st));
-        };
-        for (int j = 0; j < ntiles; ++j) {
-          const uint32_t gg = g + j;
-          const uint32_t st = gg % NST, sb = gg & 1;
-          mbar_wait(BAR(B_KFULL + st), (gg / NST) & 1);
-          mbar_wait(BAR(B_SEMPTY + sb), ((gg >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t kaddr = sbase + OFF_K + st * CHUNK_BYTES;
+          tc_commit(BAR(B_VEMPTY + sv));
+          BSA_TR(2, gp);
+        }
+        __syncwarp();
+        ++gp;
+      };
+      for (int j = 0; j < ntiles; ++j) {
+        const uint32_t sk = gs % NK, sb = gs & 1;
+        mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
+        if (lane == 0) BSA_TR(3, gs);
+        // S buffer free: QT -> the PV that read P from it (tile gs-2) is done;
+        // else the softmax warps have copied S(gs-2) to registers
+        mbar_wait(BAR((QT ? B_PFREE : B_SEMPTY) + sb), ((gs >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
-            const uint64_t ad = sdesc(qaddr + k * 32, 16, 1024);
-            const uint64_t bd = sdesc(kaddr + k * 32, 16, 1024);
-            mma_ss(tmem + TM_S + sb * 64, ad, bd, id_s, k > 0 ? 1u : 0u);
+            if (BSA_TC_EXPERIMENT == 2) continue;
+            if constexpr (QT)
+              mma_ts(tmem + TM_S + sb * 64, tmem + TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
+                     k > 0 ? 1u : 0u);
+            else
+              mma_ss(tmem + TM_S + sb * 64, dq + (uint64_t)(2 * k), dk + (uint64_t)(2 * k), id_s,
+                     k > 0 ? 1u : 0u);
           }
           tc_commit(BAR(B_SFULL + sb));
-          if (j == ntiles - 1) tc_commit(BAR(B_QEMPTY + slot));
-          if (j > 0) issue_pv(gg - 1, j - 1);
+          tc_commit(BAR(B_KEMPTY + sk));
+          BSA_TR(1, gs);
+          if (!QT && j == ntiles - 1) tc_commit(BAR(B_QEMPTY));
         }
-        issue_pv(g + ntiles - 1, ntiles - 1);
-        tc_commit(BAR(B_OFULL));
-        g += ntiles;
-        ++it;
+        __syncwarp();
+        ++gs;
+        if (j >= PV_LAG) issue_pv(j - PV_LAG);
       }
+      for (int jj = ntiles > PV_LAG ? ntiles - PV_LAG : 0; jj < ntiles; ++jj) issue_pv(jj);
+      if (elect_one()) tc_commit(BAR(B_OFULL));
+      __syncwarp();
+      ++it;
     }
-    __syncwarp();
   } else {
     // ======================= softmax warps 0..3 =======================
     const int row = threadIdx.x;  // TMEM lane == query row in the tile
@@ -466,10 +606,35 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
+      if constexpr (QT) {
+        // this thread's query row of the packed partitioned Q -> TMEM lane `row`
+        // (32 columns of bf16 pairs: the A operand layout of S = Q K^T).  The
+        // previous item's S MMAs are complete: their S tiles were all consumed.
+        const int64_t pr = I.row0 + row;
+        uint32_t qr[32];
+        if (pr < G.T) {
+          const uint4* src = reinterpret_cast<const uint4*>(A.qp + (I.h * G.T + pr) * D);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = __ldg(src + c);
+            qr[4 * c] = v.x; qr[4 * c + 1] = v.y; qr[4 * c + 2] = v.z; qr[4 * c + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) qr[c] = 0u;
+        }
+        tmem_st16(tmem + lane_off + TM_Q, qr);
+        tmem_st16(tmem + lane_off + TM_Q + 16, qr + 16);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(B_QFULL));
+      }
       float m = NEG_INF, l = 0.0f;
       for (int j = 0; j < ntiles; ++j) {
         const uint32_t gg = g + j, sb = gg & 1;
         const int len = chunk_len(I, j);
+        if (lane == 0) BSA_TR(4 + warp, gg);
         mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
         tc_fence_after();
         uint32_t sr[64];
@@ -480,7 +645,10 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
         for (int c = 0; c < 4; ++c) reg_fence16(&sr[c * 16]);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
+        if (lane == 0) {
+          if (!QT) mbar_arrive(BAR(B_SEMPTY + sb));
+          BSA_TR(8 + warp, gg);
+        }
         float s[64];
 #pragma unroll
         for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(sr[e]);
@@ -523,13 +691,31 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
           }
         }
         // P buffer sb is free once the PV that read it (two tiles ago) is done
-        if (gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
+        // (QT: P(gg) overwrites S(gg), whose issue already waited for PV(gg-2))
+        if (!QT && gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
         tc_fence_after();
-        l += exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + TM_P + sb * 32);
+#if BSA_TC_EXPERIMENT == 1
+        {  // timing experiment: no exponentials (results are wrong)
+          uint32_t r[16];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]);
+            tmem_st16(tmem + lane_off + p_col(sb) + c * 16, r);
+          }
+          l += 1.0f;
+        }
+#else
+        l += exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
+#endif
+        if (lane == 0) BSA_TR(12 + warp, gg);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(B_PFULL + sb));
+        if (lane == 0) {
+          mbar_arrive(BAR(B_PFULL + sb));
+          BSA_TR(16 + warp, gg);
+        }
       }
       // epilogue: O / l
       mbar_wait(BAR(B_OFULL), it & 1);
@@ -663,6 +849,16 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
   BSA_LAUNCH_CHECK();
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
+  if (a.trace) {
+    // debug only: dump the CTA-0 pipeline trace (BSA_TC_TRACE=<file>)
+    BSA_CUDA_TRY(cudaStreamSynchronize(st));
+    static unsigned long long host[tc::TRACE_EVENTS * tc::TRACE_TILES];
+    BSA_CUDA_TRY(cudaMemcpy(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(getenv("BSA_TC_TRACE"), "wb")) {
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
+    }
+  }
   return BSA_OK;
 }
 
