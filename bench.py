@@ -15,9 +15,15 @@ Arms:
                      bounded sample of the same workload, extrapolated to a
                      full layer.
 
-Multi-GPU (torchrun, NCCL): every rank runs its own independent layer
-(replicas of the per-GPU workload: "scaling": "weak"); no collective on the
-data path; timing is the max over ranks.
+Multi-GPU (torchrun, NCCL), timing is the max over ranks:
+  --mode replicas (default)  every rank runs its own independent layer (the
+                     per-GPU workload replicated: "scaling": "weak"); no
+                     collective on the data path.
+  --mode sharded     ONE layer of --frames frames split over the ranks
+                     (paper_2509_07120_b200/shard.py): frame-sharded Q/K/V,
+                     NCCL all-gather of Q/K/V, row-split scoring + mask
+                     all-gather, LPT-sharded attention, sum all-reduce
+                     ("scaling": "strong").
 """
 
 from __future__ import annotations
@@ -56,6 +62,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
     return ap.parse_args()
 
 
@@ -68,7 +75,10 @@ def workload_config(a, extra=None):
         "block_q": 128, "block_k": 64, "tau": a.tau, "rho": a.rho,
         "l2": "inputs larger than L2 (3 x %.2f GB bf16 Q/K/V vs 126 MB L2)" %
               (a.heads * T * a.dim * 2 / 1e9),
-        "parallelism": f"replicas x{a.gpus} (one independent layer per GPU, no collective)",
+        "parallelism": (f"replicas x{a.gpus} (one independent layer per GPU, no collective)"
+                        if a.mode == "replicas" else
+                        f"sharded x{a.gpus} (one layer: frame-sharded inputs, NCCL all-gather "
+                        f"of Q/K/V, LPT-sharded rows, sum all-reduce)"),
     }
     if extra:
         cfg.update(extra)
@@ -154,12 +164,24 @@ def run_ours(a):
     T, H, d = lay.total_tokens, a.heads, a.dim
     g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
     pol = bsa.MaskPolicy(a.tau, a.rho, g)
+    sharded = a.mode == "sharded"
     gen = torch.Generator(device=dev)
-    gen.manual_seed(a.seed + 1000 * rank)
+    # replicas: an independent layer per rank; sharded: one layer, same seed
+    gen.manual_seed(a.seed + (0 if sharded else 1000 * rank))
     q, k, v = (torch.randn((H, T, d), generator=gen, device=dev, dtype=torch.float32)
                .to(torch.bfloat16) for _ in range(3))
+    if sharded:
+        from paper_2509_07120_b200.shard import ShardPlan, sharded_sparse_attention
+        plan = ShardPlan(lay, world)
+        t0, t1 = plan.token_range(rank)
+        q_in, k_in, v_in = (x[:, t0:t1].contiguous() for x in (q, k, v))
+    else:
+        q_in, k_in, v_in = q, k, v
 
     def step(qq, kk, vv, timing=False):
+        if sharded:
+            return sharded_sparse_attention(qq, kk, vv, lay, pol, inputs="sharded",
+                                            return_mask=True)
         mask = bsa.predict_mask(qq, kk, pol, layout=lay)
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
         return bsa.sparse_attention(job, timing=timing), mask
@@ -170,7 +192,7 @@ def run_ours(a):
         torch.cuda.synchronize()
 
     for _ in range(a.warmup):
-        out, mask = step(q, k, v)
+        out, mask = step(q_in, k_in, v_in)
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -178,7 +200,7 @@ def run_ours(a):
         barrier()
         e0.record(stream)
         for _ in range(a.steps):
-            out, mask = step(q, k, v)
+            out, mask = step(q_in, k_in, v_in)
         e1.record(stream)
         barrier()
     ms_total = e0.elapsed_time(e1)
@@ -191,7 +213,7 @@ def run_ours(a):
     # stage split + live kernel time of the dominant (tensor-core) kernel,
     # CUDA events on the launching stream, averaged over `steps` launches
     score_ms, kern_ms = [], []
-    for _ in range(a.steps):
+    for _ in range(a.steps if not sharded else 0):
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         mask = bsa.predict_mask(q, k, pol, layout=lay)
@@ -200,7 +222,8 @@ def run_ours(a):
         bsa.sparse_attention(job, timing=True)
         kern_ms.append(sp.last_kernel_ms())
         score_ms.append(s0.elapsed_time(s1))
-    kernel_ms = float(np.mean(kern_ms))
+    # sharded mode: per-GPU share of the layer's work over the whole step
+    kernel_ms = float(np.mean(kern_ms)) if kern_ms else ms_step * world
     area = mask.selected_area().astype(np.int64)
     Ts, Tp = lay.special_tokens, lay.patch_tokens
     # algorithmic work: 2 GEMMs (QK^T, PV) x 2 flop/MAC over allowed entries
@@ -217,11 +240,21 @@ def run_ours(a):
     peak_src = "measured burst cuBLAS bf16 (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks else \
         "fallback 1.59 PF/s (B200_PROFILING.md)"
     achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
+    traffic = None
+    if not sharded:
+        # DRAM bytes of one launch from the committed ncu --set full capture of
+        # this workload (profiles/), when it exists for the current kernel
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "tc_traffic.json")))
+            if tr.get("frames") == a.frames and tr.get("rho") == a.rho and tr.get("tau") == a.tau:
+                traffic = tr["dram_bytes_per_launch"]
+        except (OSError, ValueError, KeyError):
+            pass
 
     # dense baseline on the same GPU: library SDPA (cuDNN / flash) in bf16
     dense_ms = None
     dense_backend = None
-    if not a.no_dense and rank == 0:
+    if not a.no_dense and rank == 0 and not sharded:
         import torch.nn.functional as F
         qb, kb, vb = (t.unsqueeze(0) for t in (q, k, v))
         try:
@@ -254,8 +287,8 @@ def run_ours(a):
     # Q/K/V, scoring + attention, D2H of the full output, every step
     e2e = None
     if not a.no_e2e:
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-        hout = torch.empty((H, T, d), dtype=torch.bfloat16).pin_memory()
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q_in, k_in, v_in))
+        hout = torch.empty(tuple(q_in.shape), dtype=torch.bfloat16).pin_memory()
 
         def e2e_step():
             dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
@@ -275,9 +308,10 @@ def run_ours(a):
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": a.frames * world / (e2e_ms * 1e-3), "unit": "frames/s",
+        layers = 1 if sharded else world
+        e2e = {"value": a.frames * layers / (e2e_ms * 1e-3), "unit": "frames/s",
                "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 3 * H * T * d * 2, "d2h_bytes_per_step": H * T * d * 2}
+               "h2d_bytes_per_step": 3 * q_in.numel() * 2, "d2h_bytes_per_step": q_in.numel() * 2}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -286,24 +320,27 @@ def run_ours(a):
     if rank == 0:
         line = {
             "metric": "global-attn frames/s at N=200 (one layer, 518^2, 16x d64), bf16",
-            "value": a.frames * world / (ms_step * 1e-3),
+            "value": a.frames * (1 if sharded else world) / (ms_step * 1e-3),
             "unit": "frames/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_step,
             "ms_per_layer": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+            "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded Gaussian Q/K/V, VGGT token layout)",
             "config": workload_config(a, {"block_density": density}),
-            "stages_ms": {"predict_mask": float(np.mean(score_ms)),
-                          "attention_kernel": kernel_ms},
+            "stages_ms": ({"predict_mask": float(np.mean(score_ms)),
+                           "attention_kernel": kernel_ms} if not sharded else None),
             "dense_baseline": {"ms_per_layer": dense_ms, "backend": dense_backend,
                                "speedup_vs_dense": (dense_ms / ms_step) if dense_ms else None},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf,
-                         "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
                          "kernel": "bsa_tc_kernel", "algorithmic_flops_per_launch": flops,
                          "dense_flops": dense_flops, "peak_source": peak_src},
             "e2e": e2e,
-            "gpu_launches": 10 * a.steps,
+            # per step: 2 pool, scores, pw_plan, softsel, fallback, 3 pack,
+            # schedule, bsa_tc_kernel (ncu launch list, profiles/)
+            "gpu_launches": 11 * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
@@ -333,11 +370,12 @@ def cpu_reference(a, budget_s=20.0):
     nq = mask.shape[1]
     perm, _ = oracle.partition_perm(a.frames, P_PER_FRAME, S_PER_FRAME)
     qp, kp, vp = q[:, perm], k[:, perm], v[:, perm]
-    # attention sample: q-blocks spread over the sequence, run until the budget
-    sample = list(range(0, nq, max(1, nq // 64)))
+    # attention sample: q-blocks in a seeded random order (spread over the
+    # sequence), run until ~60% of the budget is spent
+    sample = [int(x) for x in np.random.default_rng(a.seed).permutation(nq)]
     done, t_attn = 0, 0.0
     t_start = time.perf_counter()
-    chunk = max(1, threads)
+    chunk = 8 * max(1, threads)  # one thread pool per chunk: keep it busy
     try:
         from threadpoolctl import threadpool_limits
     except ImportError:  # pragma: no cover
@@ -347,6 +385,11 @@ def cpu_reference(a, budget_s=20.0):
     ctx = threadpool_limits(limits=1, user_api="blas") if threadpool_limits else None
     if ctx:
         ctx.__enter__()
+    # untimed warm-up (thread pool, BLAS buffers, page faults)
+    oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, S_PER_FRAME, mask, 128, 64,
+                                 threads=threads, inputs_permuted=True,
+                                 work=[(0, qb) for qb in sample[:threads]])
+    t_start = time.perf_counter()
     while done < len(sample) and (time.perf_counter() - t_start) < budget_s * 0.6:
         items = [(0, qb) for qb in sample[done:done + chunk]]
         t1 = time.perf_counter()
@@ -357,15 +400,19 @@ def cpu_reference(a, budget_s=20.0):
     if ctx:
         ctx.__exit__(None, None, None)
     per_qblock = t_attn / max(done, 1)
-    # special rows: 256-row chunk sample over all keys
-    t2 = time.perf_counter()
-    rows = min(Ts, 256)
-    s = (qp[0, :rows] @ kp[0].T) * np.float32(1 / np.sqrt(a.dim))
-    s -= s.max(axis=1, keepdims=True)
-    np.exp(s, out=s)
-    s /= s.sum(axis=1, keepdims=True)
-    _ = s @ vp[0]
-    t_spec = (time.perf_counter() - t2) * (Ts / max(rows, 1))
+    # special rows (dense over all keys), 256-row chunks until ~25% of the budget
+    rows, t_spec_s = 0, 0.0
+    while rows < Ts and t_spec_s < budget_s * 0.25:
+        r1 = min(Ts, rows + 256)
+        t2 = time.perf_counter()
+        s = (qp[0, rows:r1] @ kp[0].T) * np.float32(1 / np.sqrt(a.dim))
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)
+        s /= s.sum(axis=1, keepdims=True)
+        _ = s @ vp[0]
+        t_spec_s += time.perf_counter() - t2
+        rows = r1
+    t_spec = t_spec_s * (Ts / max(rows, 1))
     per_head_s = t_score + per_qblock * nq + t_spec
     layer_s = per_head_s * a.heads
     return {

@@ -110,7 +110,19 @@ __global__ void counts_kernel(const uint8_t* __restrict__ bits, int64_t rows, in
   counts[r] = c;
 }
 
-// items per head: nst special tiles (rows of 128) then nq patch q-blocks
+// items per head: nst special tiles (rows of 128) then nq patch q-blocks.
+// Deterministic stable counting sort by descending cost: the histogram is
+// built in parallel, the placement by warp 0 walking the items in index
+// order 32 at a time (__match_any_sync ranks equal costs inside a chunk).
+// Determinism matters: every rank of a multi-GPU run builds this list
+// independently and takes every num_shards-th entry of it.
+__device__ __forceinline__ int64_t item_cost(const int32_t* counts, int64_t h, int64_t nq,
+                                             int64_t nst, int64_t nsc, int64_t spec_cost,
+                                             int64_t max_cost, int64_t i) {
+  const int64_t c = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
+  return min(c, max_cost);
+}
+
 __global__ void __launch_bounds__(1024)
     schedule_kernel(const int32_t* __restrict__ counts, int64_t nq, int64_t nst, int64_t nsc,
                     int64_t spec_cost, int64_t max_cost, int32_t* __restrict__ items) {
@@ -119,10 +131,8 @@ __global__ void __launch_bounds__(1024)
   const int64_t M = nst + nq;
   for (int64_t c = threadIdx.x; c <= max_cost; c += blockDim.x) hist[c] = 0;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    const int64_t cost = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
-    atomicAdd(&hist[min(cost, max_cost)], 1);
-  }
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x)
+    atomicAdd(&hist[item_cost(counts, h, nq, nst, nsc, spec_cost, max_cost, i)], 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     int32_t run = 0;  // descending cost: longest first
@@ -133,10 +143,23 @@ __global__ void __launch_bounds__(1024)
     }
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    const int64_t cost = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
-    const int32_t pos = atomicAdd(&hist[min(cost, max_cost)], 1);
-    items[h * M + pos] = (int32_t)(h * M + i);
+  if (threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    for (int64_t i0 = 0; i0 < M; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool valid = i < M;
+      const unsigned active = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const int cost = (int)item_cost(counts, h, nq, nst, nsc, spec_cost, max_cost, i);
+        const unsigned same = __match_any_sync(active, cost);
+        const int rank = __popc(same & ((1u << lane) - 1u));
+        const int32_t base = hist[cost];
+        items[h * M + base + rank] = (int32_t)(h * M + i);
+        __syncwarp(active);
+        if (rank == 0) hist[cost] = base + __popc(same);
+      }
+      __syncwarp();
+    }
   }
 }
 

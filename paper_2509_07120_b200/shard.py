@@ -1,0 +1,238 @@
+"""Multi-GPU split of block-sparse global attention.
+
+The reference is single-process: it parallelises (head, q-block) work items
+over a thread pool with contiguous chunks (/root/reference/pkg/src/bsattn/
+sparse.py:185-202).  Every such row is independent once its head's full K/V
+and pooled K are known, so the B200 path shards rows across GPUs with one
+process per GPU:
+
+1. **Gather** (only for frame-sharded inputs). Each rank holds the frames
+   of its slice of the sequence, as a VGGT stack run with frame parallelism
+   would produce them. One all-gather each of Q, K and V over NCCL/NVLink
+   rebuilds the full interleaved sequence on every rank.
+2. **Pool** the full Q and K locally. Pooling is HBM-bound and cheap, and a
+   k-block that straddles a rank boundary is pooled in exactly the
+   reference's order (maskpred.py:104-120), so no halo exchange is needed.
+3. **Score** only this rank's slice of q-block rows against all pooled keys
+   (pooled_scores + select_blocks, maskpred.py:123-174). All-gather the
+   bitset rows and counts, which are 18 MB at N=200.
+4. **Attend** this rank's share of the global LPT work list
+   (`bsa_sparse_attention(shard, num_shards)`); other rows are left zero.
+5. **Combine** with an all-reduce (sum). Rows are disjoint, so `x + 0 = x`
+   and the sum is exact. Each rank returns the rows of its own frames.
+
+Every row is computed by the same kernel with the same key order as on one
+GPU. The mask and the output are therefore bit-identical to the single-GPU
+result for any world size (tests/test_shard_host.py checks the host logic
+with gloo on CPU; tests/test_gpu_shard.py checks the device path).
+
+The compute steps go through a small ``ops`` object. The default is
+``DeviceOps`` (libbsa.so). CPU tests inject a checker-backed implementation;
+that injection is test infrastructure and the product never uses it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .layout import BlockGeometry, TokenLayout
+from .maskpred import BlockMask, MaskPolicy
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Ownership arithmetic for `world` ranks over one layer (host only)."""
+
+    layout: TokenLayout
+    world: int
+    block_q: int = 128
+    block_k: int = 64
+
+    def __post_init__(self):
+        if self.world < 1:
+            raise ValueError(f"world size must be >= 1, got {self.world}")
+        if self.layout.frames < self.world:
+            raise ValueError(
+                f"{self.layout.frames} frames cannot be split over {self.world} ranks")
+
+    @property
+    def geometry(self) -> BlockGeometry:
+        return BlockGeometry(self.layout.patch_tokens, self.block_q, self.block_k)
+
+    def frame_range(self, rank: int) -> tuple[int, int]:
+        """Contiguous frames [f0, f1) held by `rank` (balanced, lower ranks
+        take the remainder)."""
+        F, W = self.layout.frames, self.world
+        base, rem = divmod(F, W)
+        f0 = rank * base + min(rank, rem)
+        return f0, f0 + base + (1 if rank < rem else 0)
+
+    @property
+    def max_frames(self) -> int:
+        return -(-self.layout.frames // self.world)
+
+    @property
+    def tokens_per_frame(self) -> int:
+        return self.layout.patches_per_frame + self.layout.specials_per_frame
+
+    def token_range(self, rank: int) -> tuple[int, int]:
+        """Interleaved-order tokens [t0, t1) of `rank`'s frames (frame-major
+        layout, layout.py:27-66)."""
+        f0, f1 = self.frame_range(rank)
+        return f0 * self.tokens_per_frame, f1 * self.tokens_per_frame
+
+    @property
+    def rows_per_rank(self) -> int:
+        return -(-self.geometry.nq_blocks // self.world)
+
+    def qblock_range(self, rank: int) -> tuple[int, int]:
+        """Mask rows (q-blocks, every head) scored by `rank`."""
+        nq, per = self.geometry.nq_blocks, self.rows_per_rank
+        return min(nq, rank * per), min(nq, (rank + 1) * per)
+
+
+class DeviceOps:
+    """The product compute steps: sm_100a kernels through libbsa.so."""
+
+    def pool(self, x: torch.Tensor, layout: TokenLayout, block: int) -> torch.Tensor:
+        from . import _native as N
+
+        h, _, d = x.shape
+        n = layout.patch_tokens
+        out = torch.empty((h, -(-n // block), d), dtype=torch.float32, device=x.device)
+        N.check(N.lib().bsa_block_pool(N.tensor_desc(x), N.layout_desc(layout), int(block),
+                                       out.data_ptr(), N.stream_ptr()), "block_pool")
+        return out
+
+    def score_rows(self, qp_rows: torch.Tensor, kp: torch.Tensor, head_dim: int,
+                   policy: MaskPolicy):
+        """(bits (H, rows, ceil(nk/8)) uint8, counts (H, rows) int32)."""
+        from . import _native as N
+
+        qp_rows, kp = qp_rows.contiguous(), kp.contiguous()
+        h, nr, d = qp_rows.shape
+        nk = kp.shape[1]
+        rb = -(-nk // 8)
+        bits = torch.zeros((h, nr, rb), dtype=torch.uint8, device=qp_rows.device)
+        counts = torch.zeros((h, nr), dtype=torch.int32, device=qp_rows.device)
+        if nr == 0:
+            return bits, counts
+        L = N.lib()
+        scale = np.float32(1.0 / float(np.sqrt(head_dim)))
+        probs = torch.empty((h, nr, nk), dtype=torch.float32, device=qp_rows.device)
+        ws = N.workspace(L.bsa_pooled_scores_workspace(h, nr, nk), qp_rows.device)
+        N.check(L.bsa_pooled_scores(qp_rows.data_ptr(), kp.data_ptr(), h, nr, nk, d, float(scale),
+                                    probs.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
+                "pooled_scores")
+        ws = N.workspace(L.bsa_select_workspace(h, nr, nk), qp_rows.device)
+        N.check(L.bsa_select_blocks(probs.data_ptr(), h, nr, nk, float(policy.tau),
+                                    policy.min_blocks, bits.data_ptr(), counts.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), N.stream_ptr()), "select_blocks")
+        return bits, counts
+
+    def attend(self, q, k, v, layout: TokenLayout, mask: BlockMask, shard: int,
+               num_shards: int) -> torch.Tensor:
+        from .dense import AttentionInputs
+        from .sparse import SparseAttentionJob, sparse_attention
+
+        out = torch.zeros(q.shape, dtype=q.dtype, device=q.device)
+        job = SparseAttentionJob(AttentionInputs(q, k, v), layout, mask)
+        return sparse_attention(job, shard=shard, num_shards=num_shards, out=out)
+
+
+def _rank_world(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def _all_gather_cat(x: torch.Tensor, group, world: int, dim: int) -> torch.Tensor:
+    """All-gather equal-shaped tensors and concatenate along `dim`."""
+    if world == 1:
+        return x
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x.contiguous(), group=group)
+    return torch.cat(parts, dim=dim)
+
+
+def gather_sequence(x_local: torch.Tensor, plan: ShardPlan, rank: int, group=None) -> torch.Tensor:
+    """Rebuild the full interleaved (H, T, d) sequence from frame shards.
+
+    Shards are padded to `plan.max_frames` frames so the collective moves
+    equal-sized buffers; the padding is dropped after the gather."""
+    W = plan.world
+    t0, t1 = plan.token_range(rank)
+    if x_local.shape[1] != t1 - t0:
+        raise ValueError(f"rank {rank} holds {x_local.shape[1]} tokens, plan expects {t1 - t0}")
+    if W == 1:
+        return x_local
+    pad_tok = plan.max_frames * plan.tokens_per_frame
+    h, n, d = x_local.shape
+    buf = torch.zeros((h, pad_tok, d), dtype=x_local.dtype, device=x_local.device)
+    buf[:, :n] = x_local
+    full = _all_gather_cat(buf, group, W, dim=1)
+    pieces = []
+    for r in range(W):
+        a, b = plan.token_range(r)
+        pieces.append(full[:, r * pad_tok:r * pad_tok + (b - a)])
+    return torch.cat(pieces, dim=1)
+
+
+def sharded_predict_mask(q_full, k_full, layout: TokenLayout, policy: MaskPolicy, plan: ShardPlan,
+                         rank: int, group=None, ops=None) -> BlockMask:
+    """Each rank scores its q-block rows; the bitsets are all-gathered, so
+    every rank ends up with the full mask (bit-identical to predict_mask)."""
+    ops = ops or DeviceOps()
+    g = policy.geometry
+    d = q_full.shape[2]
+    qp = ops.pool(q_full, layout, g.block_q)
+    kp = ops.pool(k_full, layout, g.block_k)
+    qb0, qb1 = plan.qblock_range(rank)
+    bits, counts = ops.score_rows(qp[:, qb0:qb1], kp, d, policy)
+    h, nr, rb = bits.shape
+    per = plan.rows_per_rank
+    if nr < per:  # equal-sized collective buffers
+        bits = torch.cat([bits, bits.new_zeros((h, per - nr, rb))], dim=1)
+        counts = torch.cat([counts, counts.new_zeros((h, per - nr))], dim=1)
+    bits = _all_gather_cat(bits, group, plan.world, dim=1)[:, :g.nq_blocks]
+    counts = _all_gather_cat(counts, group, plan.world, dim=1)[:, :g.nq_blocks]
+    return BlockMask._from_device(bits.reshape(h * g.nq_blocks, rb).contiguous(),
+                                  counts.reshape(-1).contiguous(), h, g)
+
+
+def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, group=None,
+                             inputs: str = "sharded", ops=None, return_mask: bool = False):
+    """One block-sparse global-attention layer over every rank of `group`.
+
+    inputs="sharded":    q/k/v are this rank's frames (ShardPlan.frame_range);
+                         the result is this rank's frames of the output.
+    inputs="replicated": q/k/v are the full sequence on every rank; the
+                         result is the full output on every rank.
+    """
+    if inputs not in ("sharded", "replicated"):
+        raise ValueError(f"inputs must be 'sharded' or 'replicated', got {inputs!r}")
+    ops = ops or DeviceOps()
+    rank, world = _rank_world(group)
+    g = policy.geometry
+    plan = ShardPlan(layout, world, g.block_q, g.block_k)
+    if inputs == "sharded":
+        q_full = gather_sequence(q, plan, rank, group)
+        k_full = gather_sequence(k, plan, rank, group)
+        v_full = gather_sequence(v, plan, rank, group)
+    else:
+        q_full, k_full, v_full = q, k, v
+    if q_full.shape[1] != layout.total_tokens:
+        raise ValueError(
+            f"inputs have {q_full.shape[1]} tokens but layout describes {layout.total_tokens}")
+    mask = sharded_predict_mask(q_full, k_full, layout, policy, plan, rank, group, ops)
+    out = ops.attend(q_full, k_full, v_full, layout, mask, rank, world)
+    if world > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    if inputs == "sharded":
+        t0, t1 = plan.token_range(rank)
+        out = out[:, t0:t1].contiguous()
+    return (out, mask) if return_mask else out
