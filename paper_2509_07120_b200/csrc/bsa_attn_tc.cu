@@ -36,49 +36,62 @@ namespace tc {
 #ifndef BSA_TC_EXPERIMENT
 #define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
 #endif
+#ifndef BSA_TC_LAYOUT
+#define BSA_TC_LAYOUT 2
+#endif
+// Pipeline layouts (TMEM columns per CTA, CTAs per SM):
+//  1: 2 CTAs/SM, TMEM 256 = S0|S1 (2x64) P0|P1 (2x32) O (64); Q in smem.
+//  2: 2 CTAs/SM, TMEM 256 = S0|S1 (2x64, P written over S) O (64) Q (32);
+//     S = Q K^T reads Q from TMEM (.ts form).
+//  3: 3 CTAs/SM, TMEM 128 = S (64, P written over S) O (64); Q in smem.
+//     One S buffer, so each CTA runs S(j) -> softmax(j) -> PV(j) -> S(j+1)
+//     strictly in turn; three CTAs per SM (three softmax warps per SM
+//     sub-partition) hide each other's MMA and barrier latencies and keep
+//     the MUFU pipes busy.
+constexpr int LAYOUT = BSA_TC_LAYOUT;
+static_assert(LAYOUT >= 1 && LAYOUT <= 3, "layout");
+constexpr bool QT = LAYOUT == 2;          // Q tile in TMEM
+constexpr bool ALIAS_P = LAYOUT != 1;     // P overwrites its own S tile
+constexpr int NSB = LAYOUT == 3 ? 1 : 2;  // S buffers in TMEM
+constexpr int CTAS_PER_SM = LAYOUT == 3 ? 3 : 2;
+constexpr uint32_t TMEM_COLS = LAYOUT == 3 ? 128 : 256;
+
 #ifndef BSA_TC_NK
-#define BSA_TC_NK 6
+#define BSA_TC_NK (BSA_TC_LAYOUT == 3 ? 3 : 6)
 #endif
 #ifndef BSA_TC_NV
-#define BSA_TC_NV 5
+#define BSA_TC_NV (BSA_TC_LAYOUT == 3 ? 3 : 5)
 #endif
 #ifndef BSA_TC_VLAG
-#define BSA_TC_VLAG 2
+#define BSA_TC_VLAG (BSA_TC_LAYOUT == 3 ? 1 : 2)
 #endif
 #ifndef BSA_TC_PVLAG
 #define BSA_TC_PVLAG 2
 #endif
 // K and V rings are separate: a K tile is released as soon as its S = QK^T
 // MMA completes, a V tile only after its PV MMA, so the producer issues K
-// VLAG tiles ahead of V and the MMA issuer runs S PVLAG tiles ahead of PV
-// (S(j) is computed while the softmax warps still work on tile j-1 or j-2).
+// VLAG tiles ahead of V.  With two S buffers the MMA issuer runs S(j) ahead
+// of PV(j - PV_LAG) while the softmax warps still work on earlier tiles.
 constexpr int BQ = 128, CH = 64, D = 64;
-constexpr int NK = BSA_TC_NK, NV = BSA_TC_NV, VLAG = BSA_TC_VLAG, PVLAG = BSA_TC_PVLAG;
+constexpr int NK = BSA_TC_NK, NV = BSA_TC_NV, VLAG = BSA_TC_VLAG;
+// when P aliases S, S(j) needs the buffer that PV(j - NSB) read
+constexpr int PV_LAG = LAYOUT == 1 ? BSA_TC_PVLAG : NSB - 1;
 constexpr int Q_BYTES = BQ * D * 2;          // 16 KB
 constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB (one K or V tile)
 constexpr int NUM_THREADS = 192;
-constexpr int CTAS_PER_SM = 2;
+// registers per thread: CTAS_PER_SM CTAs x 192 threads share 64K (8-register granularity)
+constexpr int MAX_REGS = (65536 / (CTAS_PER_SM * NUM_THREADS)) / 8 * 8;
 constexpr int OFF_Q = 0;                     // one Q tile (refilled between work items)
 constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
 constexpr int OFF_BAR = OFF_V + NV * CHUNK_BYTES;
 constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;  // barriers/ring + alignment slack
-static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
-static_assert(PVLAG >= 1 && PVLAG <= 2, "S is double buffered in TMEM");
-constexpr uint32_t TMEM_COLS = 256;
+static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
+static_assert(PV_LAG >= 0 && PV_LAG <= 2 && (LAYOUT != 1 || PV_LAG >= 1), "PV lag");
 
-#ifndef BSA_TC_QTMEM
-#define BSA_TC_QTMEM 1
-#endif
-// QT: the Q tile lives in TMEM and S = Q K^T reads it as the A operand
-// (tcgen05.mma .ts form), so per key tile the tensor core reads only K and V
-// from shared memory; P is written over its own S buffer.  Otherwise Q is a
-// TMA-loaded shared-memory operand and P has its own TMEM buffers.
-constexpr bool QT = BSA_TC_QTMEM != 0;
-constexpr int PV_LAG = QT ? 1 : PVLAG;  // QT: S(j) reuses the buffer PV(j-2) read
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = QT ? 128 : 192, TM_Q = 192;
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = LAYOUT == 1 ? 192 : 64 * NSB, TM_Q = 192;
 __host__ __device__ constexpr uint32_t p_col(uint32_t sb) {
-  return QT ? TM_S + sb * 64 : TM_P + sb * 32;
+  return ALIAS_P ? TM_S + sb * 64 : TM_P + sb * 32;
 }
 
 // barrier slots (8 bytes each) inside the barrier region
@@ -300,6 +313,19 @@ __device__ __forceinline__ float exp_tile(const float (&s)[64], float sl2, float
   return t.x + t.y;
 }
 
+// row max of a 64-column S tile (3-input max tree)
+__device__ __forceinline__ float tile_max(const float (&s)[64]) {
+  float mx8[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[8 + i]);
+#pragma unroll
+  for (int e = 16; e < 64; e += 8)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[e + i]);
+  return fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+}
+
 // UMMA shared-memory descriptor: SWIZZLE_128B, version 1 (sm_100).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -320,44 +346,46 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, i
 // work item decoding
 // ---------------------------------------------------------------------------
 struct Item {
-  int64_t h;
-  int64_t qb;      // -1 for a special-row tile
-  int64_t row0;    // first partitioned query row
-  int rows;        // valid query rows
-  int nchunks;     // 64-key tiles in the key stream
-  int last_len;    // length of the final tile (ragged tails)
-  int nsc;         // leading contiguous tiles (special strip / all keys)
-  int spec_last;   // length of the last contiguous tile
+  int32_t h;
+  int32_t qb;       // -1 for a special-row tile
+  int32_t row0;     // first partitioned query row
+  int32_t rows;     // valid query rows
+  int32_t nchunks;  // 64-key tiles in the key stream
+  int32_t last_len; // length of the final tile (ragged tails)
+  int32_t nsc;      // leading contiguous tiles (special strip / all keys)
+  int32_t spec_last;  // length of the last contiguous tile
 };
 
+// 32-bit fields: the tensor-core path requires T < 2^31 and H < 65536.
 __device__ __forceinline__ Item decode(const AttnGeom& G, int32_t code, const int32_t* counts,
                                        const uint8_t* bits) {
   Item it;
-  const int64_t nst = ceil_div(G.Ts, BQ);
-  const int64_t M = nst + G.nq;
+  const int32_t nst = (int32_t)ceil_div(G.Ts, BQ);
+  const int32_t M = nst + (int32_t)G.nq;
+  const int32_t T = (int32_t)G.T, Ts = (int32_t)G.Ts, Tp = (int32_t)G.Tp;
   it.h = code / M;
-  const int64_t li = code % M;
+  const int32_t li = code - it.h * M;
   if (li < nst) {
     it.qb = -1;
     it.row0 = li * BQ;
-    it.rows = (int)min((int64_t)BQ, G.Ts - it.row0);
-    it.nsc = (int)ceil_div(G.T, CH);
-    it.spec_last = (int)(G.T - (int64_t)(it.nsc - 1) * CH);
+    it.rows = min(BQ, Ts - it.row0);
+    it.nsc = (T + CH - 1) / CH;
+    it.spec_last = T - (it.nsc - 1) * CH;
     it.nchunks = it.nsc;
     it.last_len = it.spec_last;
   } else {
     it.qb = li - nst;
-    it.row0 = G.Ts + it.qb * BQ;
-    it.rows = (int)min((int64_t)BQ, G.Tp - it.qb * BQ);
-    it.nsc = (int)ceil_div(G.Ts, CH);
-    it.spec_last = it.nsc ? (int)(G.Ts - (int64_t)(it.nsc - 1) * CH) : CH;
-    const int cnt = counts[it.h * G.nq + it.qb];
+    it.row0 = Ts + it.qb * BQ;
+    it.rows = min(BQ, Tp - it.qb * BQ);
+    it.nsc = (Ts + CH - 1) / CH;
+    it.spec_last = it.nsc ? Ts - (it.nsc - 1) * CH : CH;
+    const int32_t cnt = counts[(int64_t)it.h * G.nq + it.qb];
     it.nchunks = it.nsc + cnt;
     // the ragged last patch block, if selected, is always the final tile
-    const int64_t lastb = G.nk - 1;
-    const uint8_t lb = bits[(it.h * G.nq + it.qb) * G.mask_row_bytes + (lastb >> 3)];
+    const int32_t lastb = (int32_t)G.nk - 1;
+    const uint8_t lb = bits[((int64_t)it.h * G.nq + it.qb) * G.mask_row_bytes + (lastb >> 3)];
     const bool last_sel = (lb >> (lastb & 7)) & 1;
-    it.last_len = last_sel ? (int)(G.Tp - lastb * CH) : CH;
+    it.last_len = last_sel ? Tp - lastb * CH : CH;
     if (cnt == 0) it.last_len = it.spec_last;
   }
   return it;
@@ -390,7 +418,7 @@ constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
 // the kernel
 // ---------------------------------------------------------------------------
 template <int POLY, bool F16P>
-__global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
+__global__ void __maxnreg__(MAX_REGS)
     bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -538,8 +566,8 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       mbar_wait(BAR(B_QFULL), it & 1);
       tc_fence_after();
       auto issue_pv = [&](int jj) {
-        const uint32_t sv = gp % NV, pb = gp & 1;
-        mbar_wait(BAR(B_PFULL + pb), (gp >> 1) & 1);
+        const uint32_t sv = gp % NV, pb = gp % NSB;
+        mbar_wait(BAR(B_PFULL + pb), (gp / NSB) & 1);
         mbar_wait(BAR(B_VFULL + sv), (gp / NV) & 1);
         if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
@@ -557,12 +585,12 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
         ++gp;
       };
       for (int j = 0; j < ntiles; ++j) {
-        const uint32_t sk = gs % NK, sb = gs & 1;
+        const uint32_t sk = gs % NK, sb = gs % NSB;
         mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
         if (lane == 0) BSA_TR(3, gs);
-        // S buffer free: QT -> the PV that read P from it (tile gs-2) is done;
-        // else the softmax warps have copied S(gs-2) to registers
-        mbar_wait(BAR((QT ? B_PFREE : B_SEMPTY) + sb), ((gs >> 1) & 1) ^ 1);
+        // S buffer free: P aliases S -> the PV that read P from it (tile
+        // gs-NSB) is done; else the softmax warps copied S(gs-2) to registers
+        mbar_wait(BAR((ALIAS_P ? B_PFREE : B_SEMPTY) + sb), ((gs / NSB) & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
@@ -595,6 +623,9 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     const int row = threadIdx.x;  // TMEM lane == query row in the tile
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const float sl2 = A.scale_log2;
+    // largest tile sum (hence P value) accepted before rescaling: keeps P and
+    // the fp32 accumulators far from overflow (fp16 P: its 65504 range)
+    const float P_LIMIT = F16P ? 32768.0f : 18446744073709551616.0f;
     const float NEG_INF = -__int_as_float(0x7f800000);
     uint32_t it = 0, g = 0;
     while (true) {
@@ -632,10 +663,10 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       }
       float m = NEG_INF, l = 0.0f;
       for (int j = 0; j < ntiles; ++j) {
-        const uint32_t gg = g + j, sb = gg & 1;
+        const uint32_t gg = g + j, sb = gg % NSB;
         const int len = chunk_len(I, j);
         if (lane == 0) BSA_TR(4 + warp, gg);
-        mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
+        mbar_wait(BAR(B_SFULL + sb), (gg / NSB) & 1);
         tc_fence_after();
         uint32_t sr[64];
 #pragma unroll
@@ -646,7 +677,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (!QT) mbar_arrive(BAR(B_SEMPTY + sb));
+          if (!ALIAS_P) mbar_arrive(BAR(B_SEMPTY + sb));
           BSA_TR(8 + warp, gg);
         }
         float s[64];
@@ -657,44 +688,19 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
           for (int e = 0; e < 64; ++e)
             if (e >= len) s[e] = NEG_INF;
         }
-        float mx8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[8 + i]);
-#pragma unroll
-        for (int e = 16; e < 64; e += 8)
-#pragma unroll
-          for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[e + i]);
-        const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float mnew = fmaxf(m, mt * sl2);
-        const bool need = mnew > m + 8.0f;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = need ? ex2(m - mnew) : 1.0f;
-          if (j > 0) {
-            // O must be stable: wait for PV of the previous tile
-            mbar_wait(BAR(B_PFREE + ((gg - 1) & 1)), ((gg - 1) >> 1) & 1);
-            tc_fence_after();
-            uint32_t orr[64];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
-#pragma unroll
-            for (int e = 0; e < 64; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_st16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
-          }
-          if (need) {
-            l *= alpha;
-            m = mnew;
-          }
-        }
+        // Exponent offset m: the row max of the item's first tile, then kept
+        // ("stale max") while no P value exceeds P_LIMIT -- the online-softmax
+        // result does not depend on the offset, only overflow does.  The sum
+        // of the tile bounds every P in it; when it exceeds the limit (rare:
+        // scores grew by > log2(P_LIMIT)), fall back to the exact max,
+        // rescale O and l, and recompute the tile.
         // P buffer sb is free once the PV that read it (two tiles ago) is done
-        // (QT: P(gg) overwrites S(gg), whose issue already waited for PV(gg-2))
-        if (!QT && gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
+        // (P aliasing S: S(gg) was issued only after PV(gg-NSB) completed)
+        if (!ALIAS_P && gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
         tc_fence_after();
+        if (m == NEG_INF) m = tile_max(s) * sl2;
 #if BSA_TC_EXPERIMENT == 1
+        float lt;
         {  // timing experiment: no exponentials (results are wrong)
           uint32_t r[16];
 #pragma unroll
@@ -703,11 +709,36 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
             for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]);
             tmem_st16(tmem + lane_off + p_col(sb) + c * 16, r);
           }
-          l += 1.0f;
+          lt = 1.0f;
         }
 #else
-        l += exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
+        float lt = exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
 #endif
+        if (__any_sync(0xffffffffu, !(lt <= P_LIMIT))) {
+          const float mnew = fmaxf(m, tile_max(s) * sl2);
+          const float alpha = ex2(m - mnew);
+          if (j > 0) {
+            // O must be stable: wait for PV of the previous tile
+            mbar_wait(BAR(B_PFREE + ((gg - 1) % NSB)), ((gg - 1) / NSB) & 1);
+            tc_fence_after();
+            // 16 columns at a time: keeps the register footprint small
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t orr[16];
+              tmem_ld16(tmem + lane_off + TM_O + c * 16, orr);
+              tmem_wait_ld();
+              reg_fence16(orr);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+              tmem_st16(tmem + lane_off + TM_O + c * 16, orr);
+            }
+          }
+          l *= alpha;
+          m = mnew;
+          tmem_wait_st();
+          lt = exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
+        }
+        l += lt;
         if (lane == 0) BSA_TR(12 + warp, gg);
         tmem_wait_st();
         tc_fence_before();
@@ -717,41 +748,43 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
           BSA_TR(16 + warp, gg);
         }
       }
-      // epilogue: O / l
+      // epilogue: O / l, 16 columns at a time (small register footprint)
       mbar_wait(BAR(B_OFULL), it & 1);
       tc_fence_after();
-      uint32_t orr[64];
+      const bool store = row < I.rows;
+      const int64_t pr = I.row0 + row;
+      const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
+      const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / l;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_O + c * 16, &orr[c * 16]);
-      tmem_wait_ld();
+      for (int c = 0; c < 4; ++c) {
+        uint32_t orr[16];
+        tmem_ld16(tmem + lane_off + TM_O + c * 16, orr);
+        tmem_wait_ld();
+        reg_fence16(orr);
+        if (store) {
+          if (A.out_bf16) {
+            uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + (I.h * G.T + dst) * D) + 2 * c;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) reg_fence16(&orr[c * 16]);
+            for (int q = 0; q < 2; ++q) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(orr[8 * q + 0]) * inv, __uint_as_float(orr[8 * q + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(orr[8 * q + 2]) * inv, __uint_as_float(orr[8 * q + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(orr[8 * q + 4]) * inv, __uint_as_float(orr[8 * q + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(orr[8 * q + 6]) * inv, __uint_as_float(orr[8 * q + 7]) * inv);
+              op[q] = v;
+            }
+          } else {
+            float4* op = reinterpret_cast<float4*>((float*)A.out + (I.h * G.T + dst) * D) + 4 * c;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              op[q] = make_float4(__uint_as_float(orr[4 * q]) * inv, __uint_as_float(orr[4 * q + 1]) * inv,
+                                  __uint_as_float(orr[4 * q + 2]) * inv, __uint_as_float(orr[4 * q + 3]) * inv);
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(B_OEMPTY));
-      if (row < I.rows) {
-        const int64_t pr = I.row0 + row;
-        const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
-        const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / l;
-        if (A.out_bf16) {
-          uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + (I.h * G.T + dst) * D);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(orr[8 * c + 0]) * inv, __uint_as_float(orr[8 * c + 1]) * inv);
-            v.y = pack_bf16(__uint_as_float(orr[8 * c + 2]) * inv, __uint_as_float(orr[8 * c + 3]) * inv);
-            v.z = pack_bf16(__uint_as_float(orr[8 * c + 4]) * inv, __uint_as_float(orr[8 * c + 5]) * inv);
-            v.w = pack_bf16(__uint_as_float(orr[8 * c + 6]) * inv, __uint_as_float(orr[8 * c + 7]) * inv);
-            op[c] = v;
-          }
-        } else {
-          float4* op = reinterpret_cast<float4*>((float*)A.out + (I.h * G.T + dst) * D);
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            op[c] = make_float4(__uint_as_float(orr[4 * c]) * inv, __uint_as_float(orr[4 * c + 1]) * inv,
-                                __uint_as_float(orr[4 * c + 2]) * inv, __uint_as_float(orr[4 * c + 3]) * inv);
-        }
-      }
       g += ntiles;
       ++it;
     }
