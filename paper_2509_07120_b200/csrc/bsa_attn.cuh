@@ -111,6 +111,12 @@ struct TcArgs {
   int shard, num_shards;
   int timing;                // record events around the launch (bsa_last_kernel_ms)
   unsigned long long* trace; // debug: clock64 per pipeline event of CTA 0 (BSA_TC_TRACE), or null
+  // stale-max overflow repair: items whose P exceeded the limit are listed
+  // (ovf_flags dedups) and recomputed by the exact-max launch
+  int32_t* ovf_flags;         // [n_items] zeroed per call
+  int32_t* ovf_list;          // [n_items]
+  int32_t* ovf_count;         // [1]
+  const int32_t* n_items_dev; // exact-max launch: item count on the device (else null)
 };
 
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);

@@ -246,6 +246,7 @@ struct TcWorkspace {
   __nv_bfloat16 *qp, *kp;
   void* vp;
   int32_t *items, *counter, *counts, *vshift;
+  int32_t *ovf_flags, *ovf_list, *ovf_count;
   unsigned int* vamax;
   size_t bytes;
 };
@@ -264,6 +265,9 @@ static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G) {
   w.counts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq) * 4, 256);
   w.vshift = (int32_t*)p; p += align_up((size_t)G.H * 4, 256);
   w.vamax = (unsigned int*)p; p += align_up((size_t)G.H * 4, 256);
+  w.ovf_flags = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
+  w.ovf_list = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
+  w.ovf_count = (int32_t*)p; p += 256;
   w.bytes = (size_t)(p - (char*)base);
   return w;
 }
@@ -411,7 +415,7 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   schedule_kernel<<<(unsigned)G.H, 1024, hsmem, st>>>(counts, G.nq, nst, nsc, spec_cost, max_cost,
                                                       W.items);
   BSA_LAUNCH_CHECK();
-  BSA_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 4, st));
+  BSA_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 8, st));  // main + repair launch counters
   TcArgs a;
   a.qp = W.qp;
   a.kp = W.kp;
@@ -431,6 +435,10 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   a.shard = shard;
   a.num_shards = num_shards;
   a.timing = (flags & BSA_FLAG_TIMING) != 0;
+  a.ovf_flags = W.ovf_flags;
+  a.ovf_list = W.ovf_list;
+  a.ovf_count = W.ovf_count;
+  a.n_items_dev = nullptr;
   a.trace = nullptr;
   if (getenv("BSA_TC_TRACE")) {  // debug pipeline trace of CTA 0 (scripts/trace_analyze.py)
     static unsigned long long* tbuf = nullptr;

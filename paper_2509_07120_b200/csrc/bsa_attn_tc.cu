@@ -2,27 +2,34 @@
 //
 // Replaces the reference kernel /root/reference/pkg/src/bsattn/sparse.py:101-205
 // (special strip + selected 64-token key blocks per 128-row query block,
-// online softmax) for bf16 inputs, head_dim 64, block_q 128, block_k 64.
+// online softmax, sparse.py:89-131) for bf16 inputs, head_dim 64, block_q
+// 128, block_k 64.
 //
-// Persistent, warp-specialised CTAs, TWO per SM (so two softmax warpgroups
-// share each SM's issue slots and tensor core), 192 threads each:
-//   warp 4      producer: fetches LPT-ordered work items (atomic counter),
-//               TMA-loads the 128x64 Q tile and, per key tile, the 64-token
-//               K and V chunk of the next selected block (gathered by TMA
-//               coordinates) into a 4-stage SW128 smem ring.
-//   warp 5      MMA issuer (one thread): S = Q K^T (tcgen05.mma kind::f16,
-//               M=128, N=64, fp32 in TMEM, double buffered) and O += P V with
-//               P read from TMEM (A operand) and V from smem (MN-major B);
-//               tcgen05.commit -> mbarriers.
-//   warps 0-3   softmax / correction / epilogue: thread t owns query row t
-//               (TMEM lane t): tcgen05.ld the S row, mask ragged chunks, packed
-//               ex2.approx.f16x2 (two exps per MUFU op; the argument is formed
-//               in fp32 with f32x2 FMAs), lazy (2^8) rescaling of O in TMEM,
-//               fp16 P back to TMEM with tcgen05.st, final O / l to global
-//               memory in the caller's (interleaved) token order.
-// P x V runs as fp16 x fp16 -> fp32: V is stored as fp16 scaled by a per-head
-// power of two (exact, undone in the epilogue) so its range is safe.
-// TMEM (256 of 512 columns per CTA): S0|S1 (2x64) P0|P1 (2x32) O (64).
+// Persistent, warp-specialised, TWO CTAs per SM, 320 threads (10 warps) each:
+//   warp 8      producer: pops LPT-ordered work items (atomic counter) and
+//               TMA-loads, per 64-key tile, the K and V chunk of the next
+//               selected block (the gather is done by TMA coordinates) into
+//               separate SW128 shared-memory rings (K runs VLAG tiles ahead).
+//   warp 9      MMA issuer: S = Q K^T with Q read from TMEM (tcgen05.mma .ts,
+//               kind::f16, M=128 N=64, fp32 in TMEM, two S buffers) and
+//               O += P V with P read from TMEM and V from shared memory;
+//               tcgen05.commit -> mbarriers.  S(j+1) is in flight while the
+//               softmax warps work on tile j.
+//   warps 0-7   softmax + epilogue, TWO threads per query row: warp w (w<4)
+//               and warp w+4 own TMEM lanes 32w..32w+31 and split each S row
+//               into key halves 0-31 / 32-63 (columns 0-31 / 32-63 of the S
+//               tile); each half writes its P over its own S columns.  Four
+//               softmax warps per SM sub-partition hide each other's MUFU,
+//               TMEM-load and barrier latencies.
+// Softmax offset ("stale max"): the row max of the item's first tile (the two
+// halves exchange it once through shared memory) is kept for the whole item;
+// online softmax does not depend on the offset, only overflow does.  Every
+// tile's P sum bounds its values; an item whose sum ever exceeds P_LIMIT
+// (scores grew by > 64 in log2 units -- never for attention logits of sane
+// scale) is listed and recomputed by a second, exact-max launch of the same
+// kernel (per-tile max exchanged between the halves, lazy 2^8 rescaling of O).
+// The row sum l is kept per half and combined in the epilogue.
+// TMEM (256 of 512 columns per CTA): S0|S1 (2x64, P over S) O (64) Q (32).
 #include <cuda.h>
 
 #include <cstdio>
@@ -36,80 +43,47 @@ namespace tc {
 #ifndef BSA_TC_EXPERIMENT
 #define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
 #endif
-#ifndef BSA_TC_LAYOUT
-#define BSA_TC_LAYOUT 2
-#endif
-// Pipeline layouts (TMEM columns per CTA, CTAs per SM):
-//  1: 2 CTAs/SM, TMEM 256 = S0|S1 (2x64) P0|P1 (2x32) O (64); Q in smem.
-//  2: 2 CTAs/SM, TMEM 256 = S0|S1 (2x64, P written over S) O (64) Q (32);
-//     S = Q K^T reads Q from TMEM (.ts form).
-//  3: 3 CTAs/SM, TMEM 128 = S (64, P written over S) O (64); Q in smem.
-//     One S buffer, so each CTA runs S(j) -> softmax(j) -> PV(j) -> S(j+1)
-//     strictly in turn; three CTAs per SM (three softmax warps per SM
-//     sub-partition) hide each other's MMA and barrier latencies and keep
-//     the MUFU pipes busy.
-constexpr int LAYOUT = BSA_TC_LAYOUT;
-static_assert(LAYOUT >= 1 && LAYOUT <= 3, "layout");
-constexpr bool QT = LAYOUT == 2;          // Q tile in TMEM
-constexpr bool ALIAS_P = LAYOUT != 1;     // P overwrites its own S tile
-constexpr int NSB = LAYOUT == 3 ? 1 : 2;  // S buffers in TMEM
-constexpr int CTAS_PER_SM = LAYOUT == 3 ? 3 : 2;
-constexpr uint32_t TMEM_COLS = LAYOUT == 3 ? 128 : 256;
-
 #ifndef BSA_TC_NK
-#define BSA_TC_NK (BSA_TC_LAYOUT == 3 ? 3 : 6)
+#define BSA_TC_NK 7
 #endif
 #ifndef BSA_TC_NV
-#define BSA_TC_NV (BSA_TC_LAYOUT == 3 ? 3 : 5)
+#define BSA_TC_NV 6
 #endif
 #ifndef BSA_TC_VLAG
-#define BSA_TC_VLAG (BSA_TC_LAYOUT == 3 ? 1 : 2)
+#define BSA_TC_VLAG 2
 #endif
-#ifndef BSA_TC_PVLAG
-#define BSA_TC_PVLAG 2
-#endif
-// K and V rings are separate: a K tile is released as soon as its S = QK^T
-// MMA completes, a V tile only after its PV MMA, so the producer issues K
-// VLAG tiles ahead of V.  With two S buffers the MMA issuer runs S(j) ahead
-// of PV(j - PV_LAG) while the softmax warps still work on earlier tiles.
 constexpr int BQ = 128, CH = 64, D = 64;
 constexpr int NK = BSA_TC_NK, NV = BSA_TC_NV, VLAG = BSA_TC_VLAG;
-// when P aliases S, S(j) needs the buffer that PV(j - NSB) read
-constexpr int PV_LAG = LAYOUT == 1 ? BSA_TC_PVLAG : NSB - 1;
-constexpr int Q_BYTES = BQ * D * 2;          // 16 KB
-constexpr int CHUNK_BYTES = CH * D * 2;      // 8 KB (one K or V tile)
-constexpr int NUM_THREADS = 192;
-// registers per thread: CTAS_PER_SM CTAs x 192 threads share 64K (8-register granularity)
+constexpr int CHUNK_BYTES = CH * D * 2;  // 8 KB (one K or V tile)
+constexpr int SM_WARPS = 8;              // softmax warps (two per TMEM lane quarter)
+constexpr int PRODUCER_WARP = 8, MMA_WARP = 9;
+constexpr int NUM_THREADS = 320;
+constexpr int CTAS_PER_SM = 2;
+// registers per thread: two CTAs x 320 threads share 64K (8-register granules)
 constexpr int MAX_REGS = (65536 / (CTAS_PER_SM * NUM_THREADS)) / 8 * 8;
-constexpr int OFF_Q = 0;                     // one Q tile (refilled between work items)
-constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int OFF_K = 0;
 constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
-constexpr int OFF_BAR = OFF_V + NV * CHUNK_BYTES;
-constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;  // barriers/ring + alignment slack
+constexpr int OFF_XCH = OFF_V + NV * CHUNK_BYTES;  // half-row exchange: 3 x 2 x 128 floats
+constexpr int OFF_BAR = OFF_XCH + 3 * 2 * BQ * 4;
+constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;    // barriers/ring + alignment slack
 static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
-static_assert(PV_LAG >= 0 && PV_LAG <= 2 && (LAYOUT != 1 || PV_LAG >= 1), "PV lag");
-
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = LAYOUT == 1 ? 192 : 64 * NSB, TM_Q = 192;
-__host__ __device__ constexpr uint32_t p_col(uint32_t sb) {
-  return ALIAS_P ? TM_S + sb * 64 : TM_P + sb * 32;
-}
+constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TM_S = 0, TM_O = 128, TM_Q = 192;
 
 // barrier slots (8 bytes each) inside the barrier region
 enum {
-  B_QFULL = 0,              // [1]
-  B_QEMPTY = 1,             // [1]
-  B_KFULL = 2,              // [NK]
+  B_QFULL = 0,              // [1]  Q row halves in TMEM (8 softmax warps)
+  B_KFULL = 1,              // [NK]
   B_KEMPTY = B_KFULL + NK,  // [NK]
   B_VFULL = B_KEMPTY + NK,  // [NV]
   B_VEMPTY = B_VFULL + NV,  // [NV]
   B_SFULL = B_VEMPTY + NV,  // [2]
-  B_SEMPTY = B_SFULL + 2,   // [2]
-  B_PFULL = B_SEMPTY + 2,   // [2]
-  B_PFREE = B_PFULL + 2,    // [2]
+  B_PFULL = B_SFULL + 2,    // [2]  8 softmax warps
+  B_PFREE = B_PFULL + 2,    // [2]  PV done: P/S buffer reusable
   B_OFULL = B_PFREE + 2,    // [1]
   B_OEMPTY = B_OFULL + 1,   // [1]
   B_IFULL = B_OEMPTY + 1,   // [2]
-  B_IEMPTY = B_IFULL + 2,   // [2]
+  B_IEMPTY = B_IFULL + 2,   // [2]  8 softmax warps + MMA warp
   B_COUNT = B_IEMPTY + 2
 };
 static_assert(B_COUNT * 8 + 32 <= 512, "barrier region");
@@ -282,50 +256,6 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// P = exp2(s * scale_log2 - m) for one 64-column S row, streamed to TMEM as
-// packed 16-bit pairs (2 x tcgen05.st.32x32b.x16); returns the fp32 row sum.
-// The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
-// the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
-// V) instead of bf16 P.
-template <int POLY, bool F16P>
-__device__ __forceinline__ float exp_tile(const float (&s)[64], float sl2, float m,
-                                          uint32_t p_taddr) {
-  const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
-  float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                  make_float2(0.f, 0.f)};
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t r[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sl2v,
-                                  nmv);
-      float2 p;
-      if ((e & 7) < POLY) p = exp2_poly2(x);
-      else p = make_float2(ex2(x.x), ex2(x.y));
-      rs[e & 3] = __fadd2_rn(rs[e & 3], p);
-      if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
-      else r[e] = pack_bf16(p.x, p.y);
-    }
-    tmem_st16(p_taddr + c * 16, r);
-  }
-  const float2 t = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
-  return t.x + t.y;
-}
-
-// row max of a 64-column S tile (3-input max tree)
-__device__ __forceinline__ float tile_max(const float (&s)[64]) {
-  float mx8[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(s[i], s[8 + i]);
-#pragma unroll
-  for (int e = 16; e < 64; e += 8)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) mx8[i] = fmaxf(mx8[i], s[e + i]);
-  return fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-}
-
 // UMMA shared-memory descriptor: SWIZZLE_128B, version 1 (sm_100).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -340,6 +270,50 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, int fmt) {
   return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)b_mn_major << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// P = exp2(s * scale_log2 - m) for one 32-key half row, written to TMEM as
+// packed 16-bit pairs (one tcgen05.st.32x32b.x16); returns the fp32 sum.
+// The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
+// the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
+// V) instead of bf16 P.
+template <int POLY, bool F16P>
+__device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float m,
+                                          uint32_t p_taddr) {
+  const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
+  float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                  make_float2(0.f, 0.f)};
+  uint32_t r[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
+    float2 p;
+    if ((e & 7) < POLY) p = exp2_poly2(x);
+    else p = make_float2(ex2(x.x), ex2(x.y));
+    rs[e & 3] = __fadd2_rn(rs[e & 3], p);
+    if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
+    else r[e] = pack_bf16(p.x, p.y);
+  }
+  tmem_st16(p_taddr, r);
+  const float2 t = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
+  return t.x + t.y;
+}
+
+// max of 32 values (3-input max tree)
+__device__ __forceinline__ float max32(const float (&s)[32]) {
+  float mx4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mx4[i] = fmaxf(s[i], s[4 + i]);
+#pragma unroll
+  for (int e = 8; e < 32; e += 4)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mx4[i] = fmaxf(mx4[i], s[e + i]);
+  return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+}
+
+// named barrier between the two warps that share a TMEM lane quarter
+__device__ __forceinline__ void pair_sync(int quarter) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -398,10 +372,9 @@ __device__ __forceinline__ int chunk_len(const Item& it, int c) {
 }
 
 // debug pipeline trace (BSA_TC_TRACE): clock64 of event `ev` for key tile `idx`
-// of CTA 0; TRACE_TILES tiles per event
+// of CTA 0; TRACE_TILES tiles per event.  Compiled in only with
+// -DBSA_TC_TRACE_BUILD: the clock reads split the scheduler's basic blocks.
 constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
-// Compiled in only with -DBSA_TC_TRACE_BUILD: the clock reads split the
-// scheduler's basic blocks and cost ~20% in the production kernel.
 #ifdef BSA_TC_TRACE_BUILD
 #define BSA_TR(ev, idx)                                                              \
   do {                                                                               \
@@ -415,12 +388,13 @@ constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
 #endif
 
 // ---------------------------------------------------------------------------
-// the kernel
+// the kernel.  EXACT: the repair launch (per-tile max, lazy O rescaling) over
+// the items the stale-max launch listed.
 // ---------------------------------------------------------------------------
-template <int POLY, bool F16P>
+template <int POLY, bool F16P, bool EXACT>
 __global__ void __maxnreg__(MAX_REGS)
-    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
+    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                  AttnGeom G, TcArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -428,19 +402,18 @@ __global__ void __maxnreg__(MAX_REGS)
   auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
   volatile int32_t* item_ring = (volatile int32_t*)(smem + OFF_BAR + 8 * B_COUNT);
   uint32_t* tmem_holder = (uint32_t*)(smem + OFF_BAR + 8 * B_COUNT + 16);
+  float* xch = (float*)(smem + OFF_XCH);  // [3][2][128]: first-tile max, tile max, l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(BAR(B_QFULL), QT ? 4 : 1);
-    mbar_init(BAR(B_QEMPTY), 1);
+    mbar_init(BAR(B_QFULL), SM_WARPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(BAR(B_SFULL + i), 1);
-      mbar_init(BAR(B_SEMPTY + i), 4);
-      mbar_init(BAR(B_PFULL + i), 4);
+      mbar_init(BAR(B_PFULL + i), SM_WARPS);
       mbar_init(BAR(B_PFREE + i), 1);
       mbar_init(BAR(B_IFULL + i), 1);
-      mbar_init(BAR(B_IEMPTY + i), 5);
+      mbar_init(BAR(B_IEMPTY + i), SM_WARPS + 1);
     }
     for (int s = 0; s < NK; ++s) {
       mbar_init(BAR(B_KFULL + s), 1);
@@ -451,17 +424,16 @@ __global__ void __maxnreg__(MAX_REGS)
       mbar_init(BAR(B_VEMPTY + s), 1);
     }
     mbar_init(BAR(B_OFULL), 1);
-    mbar_init(BAR(B_OEMPTY), 4);
+    mbar_init(BAR(B_OEMPTY), SM_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_holder)), "n"(TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (warp == 4 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_q) : "memory");
+  if (warp == PRODUCER_WARP && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
   }
@@ -470,22 +442,24 @@ __global__ void __maxnreg__(MAX_REGS)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  const int64_t n_work =
-      A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards : A.n_items;
+  int64_t n_work;
+  if (EXACT) n_work = *A.n_items_dev;
+  else n_work = A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards
+                                 : A.n_items;
 
-  if (warp == 4) {
+  if (warp == PRODUCER_WARP) {
     // ======================= producer (whole warp; one elected lane issues) =====
-    // Control flow and operands are warp-uniform, so they live in uniform
-    // registers and the TMA issue needs no per-instruction broadcast loop.
-    // Key tile j of the running stream: K(j) is issued VLAG tiles before V(j).
+    // K(j) is issued VLAG tiles before V(j): a K tile is released as soon as
+    // its S MMA completes, a V tile only after its PV MMA.
     uint32_t it = 0, gk = 0, gv = 0;
-    int64_t vq[VLAG + 1];  // key-chunk starts of the K tiles whose V is pending
+    int32_t vq[VLAG + 1];  // key-chunk starts of the K tiles whose V is pending
     while (true) {
       int64_t w = 0;
       if (lane == 0) w = atomicAdd(A.work_counter, 1);
       w = __shfl_sync(0xffffffffu, w, 0);
       int32_t code = -1;
-      if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
+      if (w < n_work)
+        code = A.items[(!EXACT && A.num_shards > 1) ? w * A.num_shards + A.shard : w];
       const uint32_t slot = it & 1;
       mbar_wait(BAR(B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
       if (elect_one()) {
@@ -495,24 +469,15 @@ __global__ void __maxnreg__(MAX_REGS)
       __syncwarp();
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
-      if constexpr (!QT) {
-        mbar_wait(BAR(B_QEMPTY), (it & 1) ^ 1);
-        if (elect_one()) {
-          mbar_expect_tx(BAR(B_QFULL), Q_BYTES);
-          tma_load_3d(sbase + OFF_Q, &tm_q, BAR(B_QFULL), 0, (int)I.row0, (int)I.h);
-        }
-        __syncwarp();
-      }
       const uint8_t* mrow =
-          I.qb >= 0 ? A.bits + (I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
+          I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
       KeyChunker ck(G, I.qb, mrow, CH);
-      auto load_v = [&](int64_t s0) {
+      auto load_v = [&](int32_t s0) {
         const uint32_t st = gv % NV;
         mbar_wait(BAR(B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
         if (elect_one()) {
           mbar_expect_tx(BAR(B_VFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_V + st * CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, (int)s0,
-                      (int)I.h);
+          tma_load_3d(sbase + OFF_V + st * CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, s0, I.h);
         }
         __syncwarp();
         ++gv;
@@ -525,33 +490,30 @@ __global__ void __maxnreg__(MAX_REGS)
         mbar_wait(BAR(B_KEMPTY + st), ((gk / NK) & 1) ^ 1);
         if (elect_one()) {
           mbar_expect_tx(BAR(B_KFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0,
-                      (int)I.h);
+          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0, I.h);
           BSA_TR(0, gk);
         }
         __syncwarp();
         ++gk;
 #pragma unroll
         for (int q = VLAG; q > 0; --q) vq[q] = vq[q - 1];
-        vq[0] = s0;
+        vq[0] = (int32_t)s0;
         if (j >= VLAG) load_v(vq[VLAG]);
       }
-      // drain the V tiles still pending for this item
 #pragma unroll
       for (int q = VLAG - 1; q >= 0; --q)
         if (q < I.nchunks) load_v(vq[q]);
       ++it;
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_WARP) {
     // ======================= MMA issuer (whole warp; one elected lane issues) ===
-    // Shared-memory descriptors are built once; per tile only the stage offset
-    // (address >> 4, no carry out of the 14-bit field: smem < 256 KB) is added.
-    // S(j) is issued as soon as K(j) and the S buffer are ready; PV(j) trails
-    // it by PVLAG tiles.
+    // Descriptors are built once; per tile only the stage offset (address >> 4,
+    // no carry out of the 14-bit field: smem < 256 KB) is added.  S(j) goes
+    // into buffer j&1 once PV(j-2), which read P from it, has completed; PV(j)
+    // trails S(j+1).
     uint32_t it = 0, gs = 0, gp = 0;
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
     const uint32_t id_pv = idesc_f16(128, 64, 1, F16P ? 0 : 1);       // P x V (fp16 | bf16)
-    const uint64_t dq = sdesc(sbase + OFF_Q, 16, 1024);
     const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + OFF_V, 8192, 1024);
     while (true) {
@@ -566,17 +528,19 @@ __global__ void __maxnreg__(MAX_REGS)
       mbar_wait(BAR(B_QFULL), it & 1);
       tc_fence_after();
       auto issue_pv = [&](int jj) {
-        const uint32_t sv = gp % NV, pb = gp % NSB;
-        mbar_wait(BAR(B_PFULL + pb), (gp / NSB) & 1);
+        const uint32_t sv = gp % NV, pb = gp & 1;
+        mbar_wait(BAR(B_PFULL + pb), (gp >> 1) & 1);
         mbar_wait(BAR(B_VFULL + sv), (gp / NV) & 1);
         if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)((sv * CHUNK_BYTES) >> 4);
+          // keys 16k..16k+15: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k)
-            if (BSA_TC_EXPERIMENT != 2) mma_ts(tmem + TM_O, tmem + p_col(pb) + k * 8, dv + (uint64_t)(k * (2048 >> 4)),
-                   id_pv, (jj > 0 || k > 0) ? 1u : 0u);
+            if (BSA_TC_EXPERIMENT != 2)
+              mma_ts(tmem + TM_O, tmem + TM_S + pb * 64 + (k >> 1) * 32 + (k & 1) * 8,
+                     dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(B_PFREE + pb));
           tc_commit(BAR(B_VEMPTY + sv));
           BSA_TR(2, gp);
@@ -585,48 +549,44 @@ __global__ void __maxnreg__(MAX_REGS)
         ++gp;
       };
       for (int j = 0; j < ntiles; ++j) {
-        const uint32_t sk = gs % NK, sb = gs % NSB;
+        const uint32_t sk = gs % NK, sb = gs & 1;
         mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
         if (lane == 0) BSA_TR(3, gs);
-        // S buffer free: P aliases S -> the PV that read P from it (tile
-        // gs-NSB) is done; else the softmax warps copied S(gs-2) to registers
-        mbar_wait(BAR((ALIAS_P ? B_PFREE : B_SEMPTY) + sb), ((gs / NSB) & 1) ^ 1);
+        mbar_wait(BAR(B_PFREE + sb), ((gs >> 1) & 1) ^ 1);  // PV(gs-2) done
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            if (BSA_TC_EXPERIMENT == 2) continue;
-            if constexpr (QT)
+          for (int k = 0; k < D / 16; ++k)
+            if (BSA_TC_EXPERIMENT != 2)
               mma_ts(tmem + TM_S + sb * 64, tmem + TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
                      k > 0 ? 1u : 0u);
-            else
-              mma_ss(tmem + TM_S + sb * 64, dq + (uint64_t)(2 * k), dk + (uint64_t)(2 * k), id_s,
-                     k > 0 ? 1u : 0u);
-          }
           tc_commit(BAR(B_SFULL + sb));
           tc_commit(BAR(B_KEMPTY + sk));
           BSA_TR(1, gs);
-          if (!QT && j == ntiles - 1) tc_commit(BAR(B_QEMPTY));
         }
         __syncwarp();
         ++gs;
-        if (j >= PV_LAG) issue_pv(j - PV_LAG);
+        if (j >= 1) issue_pv(j - 1);
       }
-      for (int jj = ntiles > PV_LAG ? ntiles - PV_LAG : 0; jj < ntiles; ++jj) issue_pv(jj);
+      issue_pv(ntiles - 1);
       if (elect_one()) tc_commit(BAR(B_OFULL));
       __syncwarp();
       ++it;
     }
   } else {
-    // ======================= softmax warps 0..3 =======================
-    const int row = threadIdx.x;  // TMEM lane == query row in the tile
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    // ======================= softmax warps 0..7 =======================
+    const int half = warp >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;  // TMEM lane == query row in the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = A.scale_log2;
-    // largest tile sum (hence P value) accepted before rescaling: keeps P and
-    // the fp32 accumulators far from overflow (fp16 P: its 65504 range)
-    const float P_LIMIT = F16P ? 32768.0f : 18446744073709551616.0f;
     const float NEG_INF = -__int_as_float(0x7f800000);
+    // largest tile sum (hence P value) accepted with the stale offset: keeps P
+    // and the fp32 accumulators far from overflow (fp16 P: its 65504 range)
+    const float P_LIMIT = F16P ? 32768.0f : 18446744073709551616.0f;
+    float* x_first = xch;            // [2][128]
+    float* x_tile = xch + 2 * BQ;    // [2][128] (EXACT)
+    float* x_l = xch + 4 * BQ;       // [2][128]
     uint32_t it = 0, g = 0;
     while (true) {
       const uint32_t slot = it & 1;
@@ -637,133 +597,139 @@ __global__ void __maxnreg__(MAX_REGS)
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
-      if constexpr (QT) {
-        // this thread's query row of the packed partitioned Q -> TMEM lane `row`
-        // (32 columns of bf16 pairs: the A operand layout of S = Q K^T).  The
-        // previous item's S MMAs are complete: their S tiles were all consumed.
-        const int64_t pr = I.row0 + row;
-        uint32_t qr[32];
-        if (pr < G.T) {
-          const uint4* src = reinterpret_cast<const uint4*>(A.qp + (I.h * G.T + pr) * D);
+      {
+        // this thread's half of its query row of the packed partitioned Q ->
+        // TMEM (16 columns of bf16 pairs: the A operand of S = Q K^T).  The
+        // previous item's S MMAs are complete: their S tiles were consumed.
+        const int32_t pr = I.row0 + row;
+        uint32_t qr[16];
+        if (pr < (int32_t)G.T) {
+          const uint4* src =
+              reinterpret_cast<const uint4*>(A.qp + ((int64_t)I.h * G.T + pr) * D + half * 32);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 4; ++c) {
             const uint4 v = __ldg(src + c);
             qr[4 * c] = v.x; qr[4 * c + 1] = v.y; qr[4 * c + 2] = v.z; qr[4 * c + 3] = v.w;
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) qr[c] = 0u;
+          for (int c = 0; c < 16; ++c) qr[c] = 0u;
         }
-        tmem_st16(tmem + lane_off + TM_Q, qr);
-        tmem_st16(tmem + lane_off + TM_Q + 16, qr + 16);
+        tmem_st16(tmem + lane_off + TM_Q + half * 16, qr);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(B_QFULL));
       }
       float m = NEG_INF, l = 0.0f;
+      bool ovf = false;
       for (int j = 0; j < ntiles; ++j) {
-        const uint32_t gg = g + j, sb = gg % NSB;
-        const int len = chunk_len(I, j);
-        if (lane == 0) BSA_TR(4 + warp, gg);
-        mbar_wait(BAR(B_SFULL + sb), (gg / NSB) & 1);
+        const uint32_t gg = g + j, sb = gg & 1;
+        const int len = chunk_len(I, j) - half * 32;  // valid keys of this half
+        if (lane == 0 && warp < 4) BSA_TR(4 + warp, gg);
+        mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
         tc_fence_after();
-        uint32_t sr[64];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld16(tmem + lane_off + TM_S + sb * 64 + c * 16, &sr[c * 16]);
+        uint32_t sr[32];
+        const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + half * 32;
+        tmem_ld16(s_col, &sr[0]);
+        tmem_ld16(s_col + 16, &sr[16]);
         tmem_wait_ld();
+        reg_fence16(&sr[0]);
+        reg_fence16(&sr[16]);
+        if (lane == 0 && warp < 4) BSA_TR(8 + warp, gg);
+        float s[32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) reg_fence16(&sr[c * 16]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (!ALIAS_P) mbar_arrive(BAR(B_SEMPTY + sb));
-          BSA_TR(8 + warp, gg);
-        }
-        float s[64];
+        for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
+        if (len < 32) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(sr[e]);
-        if (len < CH) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
+          for (int e = 0; e < 32; ++e)
             if (e >= len) s[e] = NEG_INF;
         }
-        // Exponent offset m: the row max of the item's first tile, then kept
-        // ("stale max") while no P value exceeds P_LIMIT -- the online-softmax
-        // result does not depend on the offset, only overflow does.  The sum
-        // of the tile bounds every P in it; when it exceeds the limit (rare:
-        // scores grew by > log2(P_LIMIT)), fall back to the exact max,
-        // rescale O and l, and recompute the tile.
-        // P buffer sb is free once the PV that read it (two tiles ago) is done
-        // (P aliasing S: S(gg) was issued only after PV(gg-NSB) completed)
-        if (!ALIAS_P && gg >= 2) mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
-        tc_fence_after();
-        if (m == NEG_INF) m = tile_max(s) * sl2;
+        if constexpr (!EXACT) {
+          if (j == 0) {
+            // first tile: the row max over both halves becomes the offset
+            x_first[half * BQ + row] = max32(s);
+            pair_sync(quarter);
+            m = fmaxf(x_first[row], x_first[BQ + row]) * sl2;
+          }
+        } else {
+          // exact offset: tile max over both halves, lazy (2^8) rescaling
+          float* xt = x_tile;
+          xt[half * BQ + row] = max32(s);
+          pair_sync(quarter);
+          const float mnew = fmaxf(m, fmaxf(xt[row], xt[BQ + row]) * sl2);
+          pair_sync(quarter);  // both halves read before the next tile's write
+          const bool need = mnew > m + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? ex2(m - mnew) : 1.0f;
+            if (j > 0) {
+              // O must be stable: wait for PV of the previous tile; each half
+              // rescales its 32 columns of O
+              mbar_wait(BAR(B_PFREE + ((gg - 1) & 1)), ((gg - 1) >> 1) & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                uint32_t orr[16];
+                const uint32_t oc = tmem + lane_off + TM_O + half * 32 + c * 16;
+                tmem_ld16(oc, orr);
+                tmem_wait_ld();
+                reg_fence16(orr);
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
+                tmem_st16(oc, orr);
+              }
+            }
+            if (need) {
+              l *= alpha;
+              m = mnew;
+            }
+          }
+        }
+        const uint32_t p_col = tmem + lane_off + TM_S + sb * 64 + half * 32;
 #if BSA_TC_EXPERIMENT == 1
         float lt;
         {  // timing experiment: no exponentials (results are wrong)
           uint32_t r[16];
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]);
-            tmem_st16(tmem + lane_off + p_col(sb) + c * 16, r);
-          }
+          for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+          tmem_st16(p_col, r);
           lt = 1.0f;
         }
 #else
-        float lt = exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
+        const float lt = exp_half<POLY, F16P>(s, sl2, m, p_col);
 #endif
-        if (__any_sync(0xffffffffu, !(lt <= P_LIMIT))) {
-          const float mnew = fmaxf(m, tile_max(s) * sl2);
-          const float alpha = ex2(m - mnew);
-          if (j > 0) {
-            // O must be stable: wait for PV of the previous tile
-            mbar_wait(BAR(B_PFREE + ((gg - 1) % NSB)), ((gg - 1) / NSB) & 1);
-            tc_fence_after();
-            // 16 columns at a time: keeps the register footprint small
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t orr[16];
-              tmem_ld16(tmem + lane_off + TM_O + c * 16, orr);
-              tmem_wait_ld();
-              reg_fence16(orr);
-#pragma unroll
-              for (int e = 0; e < 16; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * alpha);
-              tmem_st16(tmem + lane_off + TM_O + c * 16, orr);
-            }
-          }
-          l *= alpha;
-          m = mnew;
-          tmem_wait_st();
-          lt = exp_tile<POLY, F16P>(s, sl2, m, tmem + lane_off + p_col(sb));
-        }
+        if (!EXACT) ovf |= !(lt <= P_LIMIT);
         l += lt;
-        if (lane == 0) BSA_TR(12 + warp, gg);
+        if (lane == 0 && warp < 4) BSA_TR(12 + warp, gg);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(BAR(B_PFULL + sb));
-          BSA_TR(16 + warp, gg);
+          if (warp < 4) BSA_TR(16 + warp, gg);
         }
       }
-      // epilogue: O / l, 16 columns at a time (small register footprint)
+      // epilogue: O / l.  The halves combine l; each writes its 32 columns.
+      x_l[half * BQ + row] = l;
+      pair_sync(quarter);
+      const float ltot = x_l[row] + x_l[BQ + row];
       mbar_wait(BAR(B_OFULL), it & 1);
       tc_fence_after();
       const bool store = row < I.rows;
-      const int64_t pr = I.row0 + row;
+      const int32_t pr = I.row0 + row;
       const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
-      const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / l;
+      const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / ltot;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t orr[16];
-        tmem_ld16(tmem + lane_off + TM_O + c * 16, orr);
+        tmem_ld16(tmem + lane_off + TM_O + half * 32 + c * 16, orr);
         tmem_wait_ld();
         reg_fence16(orr);
         if (store) {
+          const int64_t base = ((int64_t)I.h * G.T + dst) * D + half * 32 + c * 16;
           if (A.out_bf16) {
-            uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + (I.h * G.T + dst) * D) + 2 * c;
+            uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + base);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               uint4 v;
@@ -774,7 +740,7 @@ __global__ void __maxnreg__(MAX_REGS)
               op[q] = v;
             }
           } else {
-            float4* op = reinterpret_cast<float4*>((float*)A.out + (I.h * G.T + dst) * D) + 4 * c;
+            float4* op = reinterpret_cast<float4*>((float*)A.out + base);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               op[q] = make_float4(__uint_as_float(orr[4 * q]) * inv, __uint_as_float(orr[4 * q + 1]) * inv,
@@ -785,6 +751,13 @@ __global__ void __maxnreg__(MAX_REGS)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(B_OEMPTY));
+      if constexpr (!EXACT) {
+        // stale offset overflowed somewhere in this item: list it once for
+        // the exact-max launch (which rewrites all of its rows)
+        if (__any_sync(0xffffffffu, ovf) && lane == 0) {
+          if (atomicCAS(&A.ovf_flags[code], 0, 1) == 0) A.ovf_list[atomicAdd(A.ovf_count, 1)] = code;
+        }
+      }
       g += ntiles;
       ++it;
     }
@@ -792,7 +765,7 @@ __global__ void __maxnreg__(MAX_REGS)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
                  : "memory");
@@ -849,10 +822,37 @@ cudaEvent_t timing_events(int which) {
   return ev[which];
 }
 
+template <int POLY, bool F16P, bool EXACT>
+static int launch_variant(const CUtensorMap& mk, const CUtensorMap& mv, const AttnGeom& G,
+                          const TcArgs& a, int grid, cudaStream_t st) {
+  auto kern = tc::bsa_tc_kernel<POLY, F16P, EXACT>;
+  BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::SMEM_BYTES));
+  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mk, mv, G, a);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+template <bool EXACT>
+static int launch_pick(const CUtensorMap& mk, const CUtensorMap& mv, const AttnGeom& G,
+                       const TcArgs& a, int grid, cudaStream_t st) {
+  switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {
+    case 0: return launch_variant<0, false, EXACT>(mk, mv, G, a, grid, st);
+    case 1: return launch_variant<1, false, EXACT>(mk, mv, G, a, grid, st);
+    case 2: return launch_variant<2, false, EXACT>(mk, mv, G, a, grid, st);
+    case 3: return launch_variant<3, false, EXACT>(mk, mv, G, a, grid, st);
+    case 16: return launch_variant<0, true, EXACT>(mk, mv, G, a, grid, st);
+    case 18: return launch_variant<2, true, EXACT>(mk, mv, G, a, grid, st);
+    default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
+  }
+}
+
+// Two launches: the stale-max kernel over the (sharded) LPT list, then the
+// exact-max kernel over the items it listed as overflowed (normally none: the
+// second launch reads a zero count and its CTAs exit at once).
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
-  CUtensorMap mq, mk, mv;
-  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);
-  if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
+  CUtensorMap mk, mv;
+  int rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
   if (!rc)
     rc = make_map(&mv, a.vp, G.H, G.T, tc::CH,
                   a.v_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
@@ -865,22 +865,19 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
                              : a.n_items;
   const int grid =
       (int)std::min<int64_t>((int64_t)sms * tc::CTAS_PER_SM, std::max<int64_t>(1, n_work));
-  auto kern = tc::bsa_tc_kernel<0, false>;
-  switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {
-    case 0: kern = tc::bsa_tc_kernel<0, false>; break;
-    case 1: kern = tc::bsa_tc_kernel<1, false>; break;
-    case 2: kern = tc::bsa_tc_kernel<2, false>; break;
-    case 3: kern = tc::bsa_tc_kernel<3, false>; break;
-    case 4: kern = tc::bsa_tc_kernel<4, false>; break;
-    case 16: kern = tc::bsa_tc_kernel<0, true>; break;
-    case 18: kern = tc::bsa_tc_kernel<2, true>; break;
-    default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
-  }
-  BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::SMEM_BYTES));
+  BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_flags, 0, (size_t)a.n_items * 4, st));
+  BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_count, 0, 4, st));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
-  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
-  BSA_LAUNCH_CHECK();
+  rc = launch_pick<false>(mk, mv, G, a, grid, st);
+  if (rc) return rc;
+  TcArgs r = a;  // repair launch
+  r.items = a.ovf_list;
+  r.n_items_dev = a.ovf_count;
+  r.work_counter = a.work_counter + 1;
+  r.num_shards = 1;
+  r.shard = 0;
+  rc = launch_pick<true>(mk, mv, G, r, sms, st);
+  if (rc) return rc;
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
   if (a.trace) {
     // debug only: dump the CTA-0 pipeline trace (BSA_TC_TRACE=<file>)

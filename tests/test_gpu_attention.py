@@ -107,6 +107,33 @@ def test_tc_random_masks(bsa, oracle, keep):
     assert _rel(out, ref) <= BF16_REL_TOL
 
 
+@pytest.mark.parametrize("growth", ["late_keys", "uniform"])
+def test_tc_large_logits_exact_repair(bsa, oracle, growth):
+    """Logits spanning hundreds of log2 units: the stale-max offset overflows
+    on later tiles, so those items go through the exact-max repair launch.
+    Results must still match the float64 oracle."""
+    rng = np.random.default_rng(13)
+    lay = bsa.TokenLayout(2, 900, 5)
+    T = lay.total_tokens
+    q, k, v = make_qkv(2, T, 64, 19)
+    q *= 6.0
+    if growth == "late_keys":
+        # small keys first (special strip, early blocks), large ones later
+        ramp = np.linspace(0.2, 8.0, T, dtype=np.float32)[None, :, None]
+        k *= ramp
+    else:
+        k *= 6.0
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    blocks = _random_mask(rng, g, 2, 0.4)
+    qd, kd, vd = _to_bf16(q, k, v)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, bsa.BlockMask(blocks, g))
+    out = bsa.sparse_attention(job).float().cpu().numpy()
+    assert np.isfinite(out).all()
+    qb, kb, vb = (t.float().cpu().numpy() for t in (qd, kd, vd))
+    ref = oracle.masked_attention_f64(qb, kb, vb, 2, 900, 5, blocks, 128, 64)
+    assert _rel(out, ref) <= BF16_REL_TOL
+
+
 def test_tc_full_mask_equals_dense(bsa):
     """Zero sparsity == dense attention (acceptance C1) on the tensor-core path."""
     import torch
