@@ -39,14 +39,43 @@ struct PoolRows {
   int64_t sT;
   uint32_t P, S, spec_off;  // patch->source remap (32-bit: tokens < 2^31)
   bool gather;
+  // Rows are visited in increasing patch order (every caller walks them
+  // left to right), so the frame of row p is tracked incrementally:
+  // [frame_end - P, frame_end) are the patches of frame `frame`.
+  mutable uint32_t frame, frame_end;
+  __device__ __forceinline__ void seek(int64_t p) const {
+    if (gather) {
+      frame = (uint32_t)p / P;
+      frame_end = (frame + 1) * P;
+    }
+  }
   __device__ __forceinline__ void load(int64_t p, float (&v)[VEC]) const {
     int64_t src = p;
     if (gather) {
-      const uint32_t f = (uint32_t)p / P;
-      src = (int64_t)f * (P + S) + spec_off + ((uint32_t)p - f * P);
+      while ((uint32_t)p >= frame_end) {
+        ++frame;
+        frame_end += P;
+      }
+      src = p + (int64_t)frame * S + spec_off;
     }
     const T* ptr = base + src * sT;
-    if constexpr (VEC == 4) {
+    if constexpr (VEC == 8) {
+      if constexpr (sizeof(T) == 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(ptr));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(ptr) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      } else {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(ptr));
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+          v[2 * q] = f2.x;
+          v[2 * q + 1] = f2.y;
+        }
+      }
+    } else if constexpr (VEC == 4) {
       Vec4<T>::load(ptr, v);
     } else if constexpr (VEC == 2) {
       if constexpr (sizeof(T) == 4) {
@@ -165,7 +194,8 @@ __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int6
   const float fl = (float)len;
   for (int col = lig * VEC; col < d; col += lanes_per_row * VEC) {
     PoolRows<T, VEC> R{x + h * sH + col, sT, (uint32_t)L.P, (uint32_t)L.S,
-                       (uint32_t)(L.specials_first ? L.S : 0), gather != 0};
+                       (uint32_t)(L.specials_first ? L.S : 0), gather != 0, 0u, 0u};
+    R.seek(r0);
     float x0[VEC];
     R.load(r0, x0);
     float s[VEC];
@@ -181,6 +211,123 @@ __global__ void __launch_bounds__(256) pool_kernel(const T* __restrict__ x, int6
     float* o = out + pr * d + col;
 #pragma unroll
     for (int c = 0; c < VEC; ++c) o[c] = __fdiv_rn(s[c], fl);
+  }
+}
+
+// Leaf-sized blocks (block <= 129), d % 8 == 0, 16-byte aligned rows: eight
+// threads per (pooled row, 8-column group), one per accumulator of numpy's
+// 8-way unrolled pairwise sum.  Thread j sums rows j, j+8, j+16, ... of the
+// block in order (its accumulator chain, independent loads in flight), the
+// eight partials combine with shuffles in numpy's tree order
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) -- IEEE addition is commutative, so each
+// xor-partner pair produces the same value on both lanes -- and the tail and
+// short blocks are added sequentially.  Bit-identical to pw_leaf.
+template <typename T>
+__device__ __forceinline__ void load8(const T* ptr, float (&v)[8]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(ptr));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(ptr) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(ptr));
+    const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+      v[2 * q] = f2.x;
+      v[2 * q + 1] = f2.y;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) pool8_kernel(const T* __restrict__ x, int64_t sH,
+                                                    int64_t sT, int64_t H, int64_t n, int d,
+                                                    int block, Layout L, int gather,
+                                                    float* __restrict__ out, int64_t nb) {
+  const int cgs = d / 8;                               // 8-column groups per row
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (int)(t & 7);                          // accumulator index
+  const int glane = (int)(threadIdx.x & 31) & ~7;       // first lane of the 8-lane group
+  const unsigned gmask = 0xFFu << glane;                // groups diverge on ragged blocks
+  const int64_t cgi = t >> 3;                          // (pooled row, column group)
+  const bool live = cgi < H * nb * cgs;
+  const int64_t pr = live ? cgi / cgs : 0;
+  const int cg = live ? (int)(cgi % cgs) : 0;
+  const int64_t h = pr / nb, b = pr % nb;
+  const int64_t r0 = b * block;
+  const int64_t len = live ? min((int64_t)block, n - r0) : 1;
+  const T* base = x + h * sH + cg * 8;
+  const uint32_t P = (uint32_t)L.P, S = (uint32_t)L.S, so = L.specials_first ? S : 0u;
+  auto row_ptr = [&](int64_t p) {
+    int64_t src = p;
+    if (gather) src = p + (int64_t)((uint32_t)p / P) * S + so;
+    return base + src * sT;
+  };
+  const int64_t first = r0 + 1, m = len - 1;
+  const int64_t stop = m >= 8 ? m - (m % 8) : 0;
+  float acc[8];
+  if (m >= 8) {
+    // this accumulator's rows p = first + j + 8i, frame tracked incrementally
+    uint32_t p = (uint32_t)(first + j);
+    uint32_t f = gather ? p / P : 0u, fend = gather ? (f + 1) * P : 0xFFFFFFFFu;
+    const T* rp = base + ((int64_t)p + (int64_t)f * S + (gather ? so : 0u)) * sT;
+    load8<T>(rp, acc);
+    auto advance = [&]() {
+      p += 8;
+      rp += 8 * sT;
+      while (p >= fend) {  // crossed into the next frame: skip its specials
+        fend += P;
+        rp += (int64_t)S * sT;
+      }
+    };
+    // four rows in flight per step, added strictly in row order
+    int64_t i = 8;
+    for (; i + 24 < stop; i += 32) {
+      float v[4][8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        advance();
+        load8<T>(rp, v[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], v[q][c]);
+    }
+    for (; i < stop; i += 8) {
+      advance();
+      float v[8];
+      load8<T>(rp, v);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], v[c]);
+    }
+#pragma unroll
+    for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __shfl_xor_sync(gmask, acc[c], sh));
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
+  }
+  // tail (m % 8 rows, or all m < 8 rows), added sequentially
+  const int ntail = (int)(m - stop);
+  float tv[8];
+  if (j < ntail) load8<T>(row_ptr(first + stop + j), tv);
+  for (int k = 0; k < ntail; ++k)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __shfl_sync(gmask, tv[c], glane + k));
+  if (j == 0 && live) {
+    float x0[8];
+    load8<T>(row_ptr(r0), x0);
+    const float fl = (float)len;
+    float o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = __fdiv_rn(len > 1 ? __fadd_rn(x0[c], acc[c]) : x0[c], fl);
+    float4* op = reinterpret_cast<float4*>(out + pr * d + cg * 8);
+    op[0] = make_float4(o[0], o[1], o[2], o[3]);
+    op[1] = make_float4(o[4], o[5], o[6], o[7]);
   }
 }
 
@@ -906,7 +1053,13 @@ static int launch_pool_t(const bsa_tensor* x, const Layout& L, bool gather, int6
   };
   // one warp-row per pooled row: lanes cover the head dim with 2 (d <= 64)
   // or 4 (d <= 128) columns each, i.e. fully coalesced 128/256-byte rows
-  if (d <= 64 && aligned(2)) launch_pool_v<T, 2>(x, L, gather, n, block, out, st);
+  if (d % 8 == 0 && block <= 129 && aligned(8) && (8 * sizeof(T)) % 16 == 0) {
+    const int64_t nb = ceil_div(n, block);
+    const int64_t threads = x->heads * nb * (d / 8) * 8;
+    pool8_kernel<T><<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(
+        (const T*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
+        gather ? 1 : 0, out, nb);
+  } else if (d <= 64 && aligned(2)) launch_pool_v<T, 2>(x, L, gather, n, block, out, st);
   else if (aligned(4)) launch_pool_v<T, 4>(x, L, gather, n, block, out, st);
   else launch_pool_v<T, 1>(x, L, gather, n, block, out, st);
   BSA_LAUNCH_CHECK();
