@@ -616,6 +616,102 @@ __device__ unsigned int search_keys(const unsigned int* keys, int64_t nk, unsign
   return lo;
 }
 
+// Radix form of search_keys: the same predicate, evaluated digit by digit
+// (8 bits at a time from the top, starting below the common prefix of mn and
+// mx).  Each pass histograms the keys that share the prefix chosen so far --
+// counts, and for MASS the exact fixed-point mass -- and one block-wide suffix
+// scan over the 256 bins picks the largest digit whose "at or above" statistic
+// (mass/count of keys above the prefix range + bins >= digit) still meets the
+// target.  The integers compared are exactly those search_keys compares, so
+// the threshold is identical; it takes at most 4 passes instead of ~10.
+static_assert(SS_THREADS == 256, "one thread per radix bin");
+template <bool MASS>
+__device__ unsigned int radix_search(const unsigned int* keys, int64_t nk, unsigned int mn,
+                                     unsigned int mx, double tau, int64_t take) {
+  __shared__ unsigned int hc[256];
+  __shared__ unsigned long long hm[256];
+  __shared__ unsigned int wc[SS_WARPS];
+  __shared__ unsigned long long wm[SS_WARPS];
+  __shared__ unsigned int s_digit, s_above_c;
+  __shared__ unsigned long long s_above_m;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // bits above the highest one where mn and mx differ are common to all keys
+  int hi = (mn == mx) ? 0 : 32 - __clz(mn ^ mx);  // undecided bits: [0, hi)
+  unsigned int prefix = hi >= 32 ? 0u : (mn & (0xFFFFFFFFu << hi));
+  unsigned int above_c = 0;
+  unsigned long long above_m = 0;
+  while (hi > 0) {
+    const int width = hi < 8 ? hi : 8;
+    const int shift = hi - width;
+    const unsigned int hi_mask = hi >= 32 ? 0u : (0xFFFFFFFFu << hi);
+    const unsigned int dmask = (1u << width) - 1u;
+    hc[tid] = 0;
+    if (MASS) hm[tid] = 0;
+    if (tid == 0) {
+      s_digit = 0;
+      s_above_c = above_c;
+      s_above_m = above_m;
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < nk; j += SS_THREADS) {
+      const unsigned int k = keys[j];
+      if ((k & hi_mask) == prefix) {
+        const unsigned int d = (k >> shift) & dmask;
+        atomicAdd(&hc[d], 1u);
+        if (MASS) atomicAdd(&hm[d], fx52(k));
+      }
+    }
+    __syncthreads();
+    // suffix sums over bins 255..0: thread t holds bin 255 - t (inclusive scan)
+    const int bin = 255 - tid;
+    unsigned int c = hc[bin];
+    unsigned long long m = MASS ? hm[bin] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int tc = __shfl_up_sync(0xffffffffu, c, o);
+      const unsigned long long tm = MASS ? __shfl_up_sync(0xffffffffu, m, o) : 0ull;
+      if (lane >= o) {
+        c += tc;
+        if (MASS) m += tm;
+      }
+    }
+    if (lane == 31) {
+      wc[w] = c;
+      if (MASS) wm[w] = m;
+    }
+    __syncthreads();
+    for (int i = 0; i < w; ++i) {
+      c += wc[i];
+      if (MASS) m += wm[i];
+    }
+    // statistic of "keys >= prefix | bin << shift" (bins beyond 2^width are
+    // empty: they repeat the statistic of the top real bin and fail with it)
+    const unsigned int tot_c = above_c + c;
+    const unsigned long long tot_m = above_m + m;
+    const bool ok = (unsigned int)bin <= dmask &&
+                    (MASS ? ((double)tot_m * 0x1p-52 >= tau) : ((int64_t)tot_c >= take));
+    // the largest ok bin: ok is monotone (true for low bins); the next higher
+    // bin belongs to thread tid - 1
+    unsigned int ok_up = __shfl_up_sync(0xffffffffu, ok ? 1u : 0u, 1);
+    __syncthreads();
+    if (lane == 31) wc[w] = ok ? 1u : 0u;
+    __syncthreads();
+    if (lane == 0) ok_up = w > 0 ? wc[w - 1] : 0u;
+    if (ok && !ok_up) {
+      s_digit = (unsigned int)bin;
+      s_above_c = tot_c - hc[bin];
+      s_above_m = MASS ? tot_m - hm[bin] : 0ull;
+    }
+    __syncthreads();
+    prefix |= s_digit << shift;
+    above_c = s_above_c;
+    above_m = s_above_m;
+    __syncthreads();
+    hi = shift;
+  }
+  return prefix;
+}
+
 // keys[] aliases the probability row (bits of non-negative floats).
 // Returns false (row -> fallback) when the fast path cannot be exact.
 __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau,
@@ -646,7 +742,7 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
       cdf_len = nk;
     } else {
       // largest key t with mass(keys >= t) >= tau (8-ary search)
-      vstar = search_keys<true>(keys, nk, mn, (unsigned long long)mx + 1, tau, 0, sh);
+      vstar = radix_search<true>(keys, nk, mn, mx, tau, 0);
       if (vstar < KEY_TINY) return false;
       unsigned long long m_ge, m_gt;
       unsigned int c_ge, c_gt, ties, e2;
@@ -688,7 +784,7 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
     count_at_or_above(keys, nk, vstar + 1, sh, c_gt, e2);
     need = take - (int64_t)c_gt;
   } else {
-    vt = search_keys<false>(keys, nk, mn, (unsigned long long)mx + 1, 0.0, take, sh);
+    vt = radix_search<false>(keys, nk, mn, mx, 0.0, take);
     unsigned int c_gt, e2;
     if (vt == 0xffffffffu) c_gt = 0;
     else count_at_or_above(keys, nk, vt + 1, sh, c_gt, e2);
