@@ -348,11 +348,14 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
   const float* qh = qp + h * nq * d;
   const float* kh = kp + h * nk * d;
   const int tr = tid / 16, tc = tid % 16;  // 8 rows x 8 cols per thread
-  float acc[8][8];
+  // column pairs (b, b+1) share one f32x2 FMA: each lane is still one exact
+  // fmaf, so every output keeps its sequential k = 0..d-1 chain
+  float2 acc[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0f;
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_float2(0.0f, 0.0f);
+  const bool vec = (d % 4) == 0;
 
   for (int c0 = 0; c0 < d; c0 += SC_KC) {
     const int kc = min(SC_KC, d - c0);
@@ -362,11 +365,22 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
       const bool qok = i0 + i < nq, kok = j0 + i < nk;
       const float* qrow = qh + (i0 + i) * d + c0;
       const float* krow = kh + (j0 + i) * d + c0;
+      if (vec && cg * 16 + 16 <= kc) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int c = cg * 16 + u;
-        qs[c][i] = (qok && c < kc) ? qrow[c] : 0.0f;
-        ks[c][i] = (kok && c < kc) ? krow[c] : 0.0f;
+        for (int u = 0; u < 16; u += 4) {
+          const int c = cg * 16 + u;
+          const float4 qv = qok ? __ldg(reinterpret_cast<const float4*>(qrow + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 kv = kok ? __ldg(reinterpret_cast<const float4*>(krow + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          qs[c][i] = qv.x; qs[c + 1][i] = qv.y; qs[c + 2][i] = qv.z; qs[c + 3][i] = qv.w;
+          ks[c][i] = kv.x; ks[c + 1][i] = kv.y; ks[c + 2][i] = kv.z; ks[c + 3][i] = kv.w;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int c = cg * 16 + u;
+          qs[c][i] = (qok && c < kc) ? qrow[c] : 0.0f;
+          ks[c][i] = (kok && c < kc) ? krow[c] : 0.0f;
+        }
       }
     }
     __syncthreads();
@@ -376,22 +390,35 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
       const float4 ka = *reinterpret_cast<const float4*>(&ks[c][tc * 8]);
       const float4 kb = *reinterpret_cast<const float4*>(&ks[c][tc * 8 + 4]);
       const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-      const float kv[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+      const float2 kv[4] = {make_float2(ka.x, ka.y), make_float2(ka.z, ka.w),
+                            make_float2(kb.x, kb.y), make_float2(kb.z, kb.w)};
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = __fmaf_rn(qv[a], kv[b], acc[a][b]);
+        for (int b = 0; b < 4; ++b)
+          acc[a][b] = __ffma2_rn(make_float2(qv[a], qv[a]), kv[b], acc[a][b]);
     }
   }
+  const bool vst = (ldz % 4) == 0 && ((uintptr_t)z % 16) == 0;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int64_t i = i0 + tr * 8 + a;
     if (i >= nq) continue;
     float* zr = z + (h * nq + i) * ldz;
+    const int64_t jb = j0 + tc * 8;
+    float o[8];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int64_t j = j0 + tc * 8 + b;
-      if (j < nk) zr[j] = __fmul_rn(acc[a][b], scale);
+    for (int b = 0; b < 4; ++b) {
+      o[2 * b] = __fmul_rn(acc[a][b].x, scale);
+      o[2 * b + 1] = __fmul_rn(acc[a][b].y, scale);
+    }
+    if (vst && jb + 8 <= nk) {
+      reinterpret_cast<float4*>(zr + jb)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(zr + jb)[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (jb + b < nk) zr[jb + b] = o[b];
     }
   }
 }
