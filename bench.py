@@ -43,7 +43,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-P_PER_FRAME, S_PER_FRAME = 1369, 5
+P_PER_FRAME, S_PER_FRAME = 1369, 5  # VGGT at 518^2: 37x37 patches + camera + 4 register tokens
 
 
 def parse():
@@ -63,15 +63,19 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
+    ap.add_argument("--specials", type=int, default=S_PER_FRAME,
+                    help="special tokens per frame (VGGT 5; pi3: 4 register tokens, no camera)")
     return ap.parse_args()
 
 
 def workload_config(a, extra=None):
-    T = a.frames * (P_PER_FRAME + S_PER_FRAME)
+    T = a.frames * (P_PER_FRAME + a.specials)
     cfg = {
-        "workload": f"VGGT global attention, N={a.frames} frames x 1374 tok (518^2), "
+        "workload": f"{'VGGT' if a.specials == 5 else 'pi3-shaped'} global attention, "
+                    f"N={a.frames} frames x {P_PER_FRAME + a.specials} tok (518^2), "
                     f"{a.heads} heads x d{a.dim}, tau={a.tau} rho={a.rho}",
-        "frames": a.frames, "tokens": T, "heads": a.heads, "head_dim": a.dim,
+        "frames": a.frames, "specials_per_frame": a.specials, "tokens": T, "heads": a.heads,
+        "head_dim": a.dim,
         "block_q": 128, "block_k": 64, "tau": a.tau, "rho": a.rho,
         "l2": "inputs larger than L2 (3 x %.2f GB bf16 Q/K/V vs 126 MB L2)" %
               (a.heads * T * a.dim * 2 / 1e9),
@@ -160,7 +164,7 @@ def run_ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    lay = bsa.TokenLayout(a.frames, P_PER_FRAME, S_PER_FRAME)
+    lay = bsa.TokenLayout(a.frames, P_PER_FRAME, a.specials)
     T, H, d = lay.total_tokens, a.heads, a.dim
     g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
     pol = bsa.MaskPolicy(a.tau, a.rho, g)
@@ -359,16 +363,16 @@ def cpu_reference(a, budget_s=20.0):
     import oracle
 
     threads = oracle.host_threads()
-    lay_T = a.frames * (P_PER_FRAME + S_PER_FRAME)
-    Tp, Ts = a.frames * P_PER_FRAME, a.frames * S_PER_FRAME
+    lay_T = a.frames * (P_PER_FRAME + a.specials)
+    Tp, Ts = a.frames * P_PER_FRAME, a.frames * a.specials
     rng = np.random.default_rng(a.seed)
     q, k, v = (rng.standard_normal((1, lay_T, a.dim), dtype=np.float32) for _ in range(3))
-    pidx = oracle.patch_indices(a.frames, P_PER_FRAME, S_PER_FRAME)
+    pidx = oracle.patch_indices(a.frames, P_PER_FRAME, a.specials)
     t0 = time.perf_counter()
     mask, _ = oracle.predict_mask(q[:, pidx], k[:, pidx], 128, 64, a.tau, a.rho)
     t_score = time.perf_counter() - t0
     nq = mask.shape[1]
-    perm, _ = oracle.partition_perm(a.frames, P_PER_FRAME, S_PER_FRAME)
+    perm, _ = oracle.partition_perm(a.frames, P_PER_FRAME, a.specials)
     qp, kp, vp = q[:, perm], k[:, perm], v[:, perm]
     # attention sample: q-blocks in a seeded random order (spread over the
     # sequence), run until ~60% of the budget is spent
@@ -386,14 +390,14 @@ def cpu_reference(a, budget_s=20.0):
     if ctx:
         ctx.__enter__()
     # untimed warm-up (thread pool, BLAS buffers, page faults)
-    oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, S_PER_FRAME, mask, 128, 64,
+    oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, a.specials, mask, 128, 64,
                                  threads=threads, inputs_permuted=True,
                                  work=[(0, qb) for qb in sample[:threads]])
     t_start = time.perf_counter()
     while done < len(sample) and (time.perf_counter() - t_start) < budget_s * 0.6:
         items = [(0, qb) for qb in sample[done:done + chunk]]
         t1 = time.perf_counter()
-        oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, S_PER_FRAME, mask, 128, 64,
+        oracle.sparse_attention_port(qp, kp, vp, a.frames, P_PER_FRAME, a.specials, mask, 128, 64,
                                      threads=threads, inputs_permuted=True, work=items)
         t_attn += time.perf_counter() - t1
         done += len(items)

@@ -1,0 +1,105 @@
+"""Model harness for BASELINE.json config 3: a stack of VGGT-aggregator
+global-attention blocks with random-init weights, each block's dense global
+attention replaced by the block-sparse operator (arXiv 2509.07120 retrofit).
+
+The reference package has no model code. This harness builds the
+smallest faithful block around the path: pre-LayerNorm, fused QKV
+projection, per-head attention over the whole multi-frame token sequence, an
+output projection and a residual. It also has an optional MLP. The GEMMs are
+plain cuBLAS (torch.nn.functional.linear); the attention is
+``predict_mask`` + ``sparse_attention`` from this package
+(``mode="sparse"``), or cuDNN SDPA (``mode="dense"``) as the baseline.
+
+Tokens are (T, C) in the interleaved VGGT order (per frame: S special tokens,
+then P patches, layout.py:27-66). C = heads x head_dim = 16 x 64 = 1024.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from .dense import AttentionInputs
+from .layout import BlockGeometry, TokenLayout
+from .maskpred import MaskPolicy, predict_mask
+from .sparse import SparseAttentionJob, sparse_attention
+
+
+@dataclass
+class BlockWeights:
+    ln_w: torch.Tensor
+    ln_b: torch.Tensor
+    qkv_w: torch.Tensor  # (3C, C)
+    qkv_b: torch.Tensor
+    proj_w: torch.Tensor  # (C, C)
+    proj_b: torch.Tensor
+    mlp: tuple | None = None  # (ln_w, ln_b, fc1_w, fc1_b, fc2_w, fc2_b)
+
+
+class GlobalAttentionStack:
+    """`layers` global-attention blocks of width heads*head_dim, random init
+    (seeded): weights ~ N(0, 1/C), biases 0, LayerNorm identity."""
+
+    def __init__(self, layers: int = 24, heads: int = 16, head_dim: int = 64, mlp: bool = False,
+                 seed: int = 0, device="cuda", dtype=torch.bfloat16):
+        self.heads, self.head_dim = heads, head_dim
+        C = heads * head_dim
+        self.dim = C
+        g = torch.Generator(device="cpu").manual_seed(seed)
+
+        def w(o, i):
+            return (torch.randn((o, i), generator=g) / math.sqrt(i)).to(device, dtype)
+
+        self.blocks = []
+        for _ in range(layers):
+            mlp_w = None
+            if mlp:
+                mlp_w = (torch.ones(C, device=device, dtype=dtype), torch.zeros(C, device=device, dtype=dtype),
+                         w(4 * C, C), torch.zeros(4 * C, device=device, dtype=dtype),
+                         w(C, 4 * C), torch.zeros(C, device=device, dtype=dtype))
+            self.blocks.append(BlockWeights(
+                torch.ones(C, device=device, dtype=dtype), torch.zeros(C, device=device, dtype=dtype),
+                w(3 * C, C), torch.zeros(3 * C, device=device, dtype=dtype),
+                w(C, C), torch.zeros(C, device=device, dtype=dtype), mlp_w))
+
+    def attention(self, x: torch.Tensor, blk: BlockWeights, layout: TokenLayout,
+                  policy: MaskPolicy | None, mode: str) -> torch.Tensor:
+        T, C = x.shape
+        H, d = self.heads, self.head_dim
+        h = F.layer_norm(x, (C,), blk.ln_w, blk.ln_b)
+        qkv = F.linear(h, blk.qkv_w, blk.qkv_b)                       # (T, 3C)
+        qkv = qkv.view(T, 3, H, d).permute(1, 2, 0, 3)                # (3, H, T, d) view
+        q, k, v = qkv[0], qkv[1], qkv[2]                              # token stride 3C
+        if mode == "sparse":
+            mask = predict_mask(q, k, policy, layout=layout)
+            o = sparse_attention(SparseAttentionJob(AttentionInputs(q, k, v), layout, mask))
+        elif mode == "dense":
+            o = F.scaled_dot_product_attention(q[None], k[None], v[None])[0]
+        else:
+            raise ValueError(f"mode must be 'sparse' or 'dense', got {mode!r}")
+        o = o.permute(1, 0, 2).reshape(T, C)
+        return F.linear(o, blk.proj_w, blk.proj_b)
+
+    def forward(self, x: torch.Tensor, layout: TokenLayout, policy: MaskPolicy | None = None,
+                mode: str = "sparse") -> torch.Tensor:
+        if x.shape != (layout.total_tokens, self.dim):
+            raise ValueError(f"x must be ({layout.total_tokens}, {self.dim}), got {tuple(x.shape)}")
+        if mode == "sparse" and policy is None:
+            raise ValueError("sparse mode needs a MaskPolicy")
+        for blk in self.blocks:
+            x = x + self.attention(x, blk, layout, policy, mode)
+            if blk.mlp is not None:
+                lw, lb, w1, b1, w2, b2 = blk.mlp
+                h = F.layer_norm(x, (self.dim,), lw, lb)
+                x = x + F.linear(F.gelu(F.linear(h, w1, b1)), w2, b2)
+        return x
+
+    __call__ = forward
+
+
+def policy_for(layout: TokenLayout, tau: float, rho: float, block_q: int = 128,
+               block_k: int = 64) -> MaskPolicy:
+    return MaskPolicy(tau, rho, BlockGeometry(layout.patch_tokens, block_q, block_k))
