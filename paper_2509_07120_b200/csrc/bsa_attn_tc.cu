@@ -43,6 +43,14 @@ namespace tc {
 #ifndef BSA_TC_EXPERIMENT
 #define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
 #endif
+#ifndef BSA_TC_TILESPLIT
+#define BSA_TC_TILESPLIT 1
+#endif
+// stale-max launch: the two warp groups (warps 0-3, 4-7) take alternate key
+// tiles (S buffer 0 / 1) of every row, full 64 columns each, instead of the
+// two column halves of every tile -- their phases interleave on the MUFU and
+// the per-tile overhead is paid half as often.
+constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
 #ifndef BSA_TC_NK
 #define BSA_TC_NK 7
 #endif
@@ -410,7 +418,7 @@ __global__ void __maxnreg__(MAX_REGS)
     mbar_init(BAR(B_QFULL), SM_WARPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(BAR(B_SFULL + i), 1);
-      mbar_init(BAR(B_PFULL + i), SM_WARPS);
+      mbar_init(BAR(B_PFULL + i), (TILE_SPLIT && !EXACT) ? SM_WARPS / 2 : SM_WARPS);
       mbar_init(BAR(B_PFREE + i), 1);
       mbar_init(BAR(B_IFULL + i), 1);
       mbar_init(BAR(B_IEMPTY + i), SM_WARPS + 1);
@@ -535,11 +543,14 @@ __global__ void __maxnreg__(MAX_REGS)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)((sv * CHUNK_BYTES) >> 4);
-          // keys 16k..16k+15: half k>>1 wrote its P over S columns 32*(k>>1)
+          // keys 16k..16k+15.  Tile split: P packed contiguously over S columns
+          // 0-31; column split: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k)
             if (BSA_TC_EXPERIMENT != 2)
-              mma_ts(tmem + TM_O, tmem + TM_S + pb * 64 + (k >> 1) * 32 + (k & 1) * 8,
+              mma_ts(tmem + TM_O,
+                     tmem + TM_S + pb * 64 +
+                         ((TILE_SPLIT && !EXACT) ? k * 8 : (k >> 1) * 32 + (k & 1) * 8),
                      dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(B_PFREE + pb));
           tc_commit(BAR(B_VEMPTY + sv));
@@ -623,6 +634,83 @@ __global__ void __maxnreg__(MAX_REGS)
       }
       float m = NEG_INF, l = 0.0f;
       bool ovf = false;
+      if constexpr (TILE_SPLIT && !EXACT) {
+        const int grp = half;                 // serves S buffer `grp`: tiles with (g+j)&1 == grp
+        const int first_grp = (int)(g & 1);   // group that owns the item's tile 0
+        if (grp == first_grp) {
+          // tile 0's row max (both column halves) becomes the item's offset
+          mbar_wait(BAR(B_SFULL + grp), (g >> 1) & 1);
+          tc_fence_after();
+          const int len0 = chunk_len(I, 0);
+          float mx = NEG_INF;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t sr[32];
+            const uint32_t s_col = tmem + lane_off + TM_S + grp * 64 + hh * 32;
+            tmem_ld16(s_col, &sr[0]);
+            tmem_ld16(s_col + 16, &sr[16]);
+            tmem_wait_ld();
+            reg_fence16(&sr[0]);
+            reg_fence16(&sr[16]);
+            float s[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[e] = e + hh * 32 < len0 ? __uint_as_float(sr[e]) : NEG_INF;
+            mx = fmaxf(mx, max32(s));
+          }
+          x_first[row] = mx;
+        }
+        pair_sync(quarter);
+        m = x_first[row] * sl2;
+        for (int j = (grp - first_grp) & 1; j < ntiles; j += 2) {
+          const uint32_t gg = g + j, sb = grp;
+          const int len = chunk_len(I, j);
+          if (lane == 0 && warp < 4) BSA_TR(4 + warp, gg);
+          mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            // 32 keys at a time; P (16 packed columns) overwrites S columns
+            // this thread has already read
+            uint32_t sr[32];
+            const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + hh * 32;
+            tmem_ld16(s_col, &sr[0]);
+            tmem_ld16(s_col + 16, &sr[16]);
+            tmem_wait_ld();
+            reg_fence16(&sr[0]);
+            reg_fence16(&sr[16]);
+            float s[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
+            if (len - hh * 32 < 32) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (e + hh * 32 >= len) s[e] = NEG_INF;
+            }
+#if BSA_TC_EXPERIMENT == 1
+            {
+              uint32_t r[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
+              tmem_st16(tmem + lane_off + TM_S + sb * 64 + hh * 16, r);
+            }
+            const float lt = 1.0f;
+#else
+            const float lt =
+                exp_half<POLY, F16P>(s, sl2, m, tmem + lane_off + TM_S + sb * 64 + hh * 16);
+#endif
+            ovf |= !(lt <= P_LIMIT);
+            l += lt;
+          }
+          if (lane == 0 && warp < 4) BSA_TR(12 + warp, gg);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(BAR(B_PFULL + sb));
+            if (warp < 4) BSA_TR(16 + warp, gg);
+          }
+        }
+      } else
       for (int j = 0; j < ntiles; ++j) {
         const uint32_t gg = g + j, sb = gg & 1;
         const int len = chunk_len(I, j) - half * 32;  // valid keys of this half
