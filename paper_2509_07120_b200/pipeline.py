@@ -1,0 +1,99 @@
+"""One block-sparse global-attention layer from HOST memory, with the PCIe
+copies overlapped with the kernels.
+
+Attention heads are independent all the way through the path: pooling,
+scoring, selection (maskpred.py:104-174 work per head) and the
+block-sparse kernel (sparse.py:134-154 ``_run_head``). The layer therefore
+runs as a pipeline over chunks of heads on three CUDA streams:
+
+    copy-in stream   H2D  Q/K/V of chunk c+1   (pinned host -> HBM)
+    compute stream   predict_mask + sparse_attention of chunk c
+    copy-out stream  D2H  output of chunk c-1  (HBM -> pinned host)
+
+The layer costs about max(compute, copies) plus one chunk of ramp, instead
+of copy-in + compute + copy-out. This is the public entry point a caller
+with host-resident activations uses, and bench.py's ``e2e`` measurement.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .dense import AttentionInputs
+from .layout import TokenLayout
+from .maskpred import BlockMask, MaskPolicy, predict_mask
+from .sparse import SparseAttentionJob, sparse_attention
+
+
+class HostLayerPipeline:
+    """Reusable device buffers and streams for repeated layers of one shape."""
+
+    def __init__(self, heads: int, tokens: int, head_dim: int, dtype=torch.bfloat16,
+                 chunk_heads: int = 2, device=None):
+        if chunk_heads < 1:
+            raise ValueError(f"chunk_heads must be >= 1, got {chunk_heads}")
+        self.device = torch.device(device or "cuda")
+        self.shape = (heads, tokens, head_dim)
+        self.dtype = dtype
+        self.chunk = min(chunk_heads, heads)
+        self.bufs = [torch.empty(self.shape, dtype=dtype, device=self.device) for _ in range(3)]
+        self.obuf = torch.empty(self.shape, dtype=dtype, device=self.device)
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+
+    def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: TokenLayout,
+            policy: MaskPolicy, out: torch.Tensor | None = None, return_masks: bool = False):
+        """q, k, v: host (ideally pinned) (H, T, d) tensors in interleaved
+        token order. Returns the host output (and the per-chunk masks).
+        The call is synchronous: the output is complete on return."""
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if tuple(t.shape) != self.shape or t.dtype != self.dtype:
+                raise ValueError(f"{name} must be {self.shape} {self.dtype}, got "
+                                 f"{tuple(t.shape)} {t.dtype}")
+            if t.device.type != "cpu":
+                raise ValueError(f"{name} must be a host tensor (use sparse_attention for "
+                                 f"device-resident inputs)")
+        if out is None:
+            out = torch.empty(self.shape, dtype=self.dtype, pin_memory=True)
+        H = self.shape[0]
+        dq, dk, dv = self.bufs
+        comp = torch.cuda.current_stream(self.device)
+        masks = []
+        done_in, done_comp = [], []
+        chunks = [(h0, min(H, h0 + self.chunk)) for h0 in range(0, H, self.chunk)]
+        # the copy-in stream must not overwrite buffers a previous call still reads
+        self.s_in.wait_stream(comp)
+        for a, b in chunks:
+            with torch.cuda.stream(self.s_in):
+                dq[a:b].copy_(q[a:b], non_blocking=True)
+                dk[a:b].copy_(k[a:b], non_blocking=True)
+                dv[a:b].copy_(v[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_in)
+                done_in.append(ev)
+        for (a, b), ev_in in zip(chunks, done_in):
+            comp.wait_event(ev_in)
+            mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout)
+            job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b]), layout, mask)
+            sparse_attention(job, out=self.obuf[a:b])
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            done_comp.append(ev)
+            if return_masks:
+                masks.append(mask)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev)
+                out[a:b].copy_(self.obuf[a:b], non_blocking=True)
+        comp.wait_stream(self.s_out)
+        torch.cuda.current_stream(self.device).synchronize()
+        return (out, masks) if return_masks else out
+
+
+def attend_from_host(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, chunk_heads: int = 2,
+                     out=None):
+    """One-shot convenience wrapper around HostLayerPipeline."""
+    p = HostLayerPipeline(q.shape[0], q.shape[1], q.shape[2], q.dtype, chunk_heads)
+    return p.run(q, k, v, layout, policy, out)
+
+
+__all__ = ["HostLayerPipeline", "attend_from_host", "BlockMask"]
