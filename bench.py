@@ -355,9 +355,10 @@ def run_ours(a):
                          "kernel": "bsa_tc_kernel", "algorithmic_flops_per_launch": flops,
                          "dense_flops": dense_flops, "peak_source": peak_src},
             "e2e": e2e,
-            # per step: 2 pool, scores, pw_plan, softsel, fallback, 3 pack,
-            # schedule, bsa_tc_kernel (ncu launch list, profiles/)
-            "gpu_launches": 11 * a.steps,
+            # per step: 2 pool8, scores, pw_plan, softsel, fallback, 3 pack,
+            # schedule, bsa_tc_kernel + its exact-repair launch (ncu launch
+            # list, profiles/r01/launches_v3.csv)
+            "gpu_launches": 12 * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
