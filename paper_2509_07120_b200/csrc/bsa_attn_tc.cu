@@ -51,11 +51,19 @@ namespace tc {
 // two column halves of every tile -- their phases interleave on the MUFU and
 // the per-tile overhead is paid half as often.
 constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
+#ifndef BSA_TC_LSUM
+#define BSA_TC_LSUM 1
+#endif
+// LSUM: the PV MMA runs with N = 80: columns 64-79 of its B operand are an
+// all-ones block kept beside every V stage (at the descriptor's LBO), so
+// O[:, 64] accumulates the row sum of P in fp32 and the softmax threads do
+// no additions.  Costs 25% more PV MMA work and 8 KB of smem per V stage.
+constexpr bool LSUM = BSA_TC_LSUM != 0;
 #ifndef BSA_TC_NK
-#define BSA_TC_NK 7
+#define BSA_TC_NK (BSA_TC_LSUM ? 5 : 7)
 #endif
 #ifndef BSA_TC_NV
-#define BSA_TC_NV 6
+#define BSA_TC_NV (BSA_TC_LSUM ? 4 : 6)
 #endif
 #ifndef BSA_TC_VLAG
 #define BSA_TC_VLAG 2
@@ -71,12 +79,14 @@ constexpr int CTAS_PER_SM = 2;
 constexpr int MAX_REGS = (65536 / (CTAS_PER_SM * NUM_THREADS)) / 8 * 8;
 constexpr int OFF_K = 0;
 constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
-constexpr int OFF_XCH = OFF_V + NV * CHUNK_BYTES;  // half-row exchange: 3 x 2 x 128 floats
+constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ its ones block)
+constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // half-row exchange: 3 x 2 x 128 floats
 constexpr int OFF_BAR = OFF_XCH + 3 * 2 * BQ * 4;
 constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;    // barriers/ring + alignment slack
 static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
 constexpr uint32_t TMEM_COLS = 256;
-constexpr uint32_t TM_S = 0, TM_O = 128, TM_Q = 192;
+// O: 64 columns (+16 row-sum columns with LSUM)
+constexpr uint32_t TM_S = 0, TM_O = 128, TM_Q = LSUM ? 224 : 192, O_COLS = LSUM ? 80 : 64;
 
 // barrier slots (8 bytes each) inside the barrier region
 enum {
@@ -285,7 +295,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, i
 // The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
 // the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
 // V) instead of bf16 P.
-template <int POLY, bool F16P>
+template <int POLY, bool F16P, bool SUM = true>
 __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float m,
                                           uint32_t p_taddr) {
   const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
@@ -298,11 +308,12 @@ __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float
     float2 p;
     if ((e & 7) < POLY) p = exp2_poly2(x);
     else p = make_float2(ex2(x.x), ex2(x.y));
-    rs[e & 3] = __fadd2_rn(rs[e & 3], p);
+    if constexpr (SUM) rs[e & 3] = __fadd2_rn(rs[e & 3], p);
     if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
     else r[e] = pack_bf16(p.x, p.y);
   }
   tmem_st16(p_taddr, r);
+  if constexpr (!SUM) return 0.0f;
   const float2 t = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
   return t.x + t.y;
 }
@@ -435,6 +446,16 @@ __global__ void __maxnreg__(MAX_REGS)
     mbar_init(BAR(B_OEMPTY), SM_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if constexpr (LSUM) {
+    // the all-ones half of every V stage: B columns 64-79 of the PV MMA (any
+    // swizzle permutation of ones is ones)
+    const uint32_t one2 = F16P ? 0x3C003C00u : 0x3F803F80u;
+    for (int i = threadIdx.x; i < NV * CHUNK_BYTES / 4; i += NUM_THREADS) {
+      const int st = i / (CHUNK_BYTES / 4), w = i % (CHUNK_BYTES / 4);
+      reinterpret_cast<uint32_t*>(smem + OFF_V + st * V_STAGE + CHUNK_BYTES)[w] = one2;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_holder)), "n"(TMEM_COLS)
@@ -485,7 +506,7 @@ __global__ void __maxnreg__(MAX_REGS)
         mbar_wait(BAR(B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
         if (elect_one()) {
           mbar_expect_tx(BAR(B_VFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_V + st * CHUNK_BYTES, &tm_v, BAR(B_VFULL + st), 0, s0, I.h);
+          tma_load_3d(sbase + OFF_V + st * V_STAGE, &tm_v, BAR(B_VFULL + st), 0, s0, I.h);
         }
         __syncwarp();
         ++gv;
@@ -521,7 +542,7 @@ __global__ void __maxnreg__(MAX_REGS)
     // trails S(j+1).
     uint32_t it = 0, gs = 0, gp = 0;
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
-    const uint32_t id_pv = idesc_f16(128, 64, 1, F16P ? 0 : 1);       // P x V (fp16 | bf16)
+    const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
     const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + OFF_V, 8192, 1024);
     while (true) {
@@ -542,7 +563,7 @@ __global__ void __maxnreg__(MAX_REGS)
         if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t dv = dv0 + (uint64_t)((sv * CHUNK_BYTES) >> 4);
+          const uint64_t dv = dv0 + (uint64_t)((sv * V_STAGE) >> 4);
           // keys 16k..16k+15.  Tile split: P packed contiguously over S columns
           // 0-31; column split: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
@@ -696,10 +717,12 @@ __global__ void __maxnreg__(MAX_REGS)
             const float lt = 1.0f;
 #else
             const float lt =
-                exp_half<POLY, F16P>(s, sl2, m, tmem + lane_off + TM_S + sb * 64 + hh * 16);
+                exp_half<POLY, F16P, !LSUM>(s, sl2, m, tmem + lane_off + TM_S + sb * 64 + hh * 16);
 #endif
-            ovf |= !(lt <= P_LIMIT);
-            l += lt;
+            if constexpr (!LSUM) {
+              ovf |= !(lt <= P_LIMIT);
+              l += lt;
+            }
           }
           if (lane == 0 && warp < 4) BSA_TR(12 + warp, gg);
           tmem_wait_st();
@@ -801,9 +824,20 @@ __global__ void __maxnreg__(MAX_REGS)
       // epilogue: O / l.  The halves combine l; each writes its 32 columns.
       x_l[half * BQ + row] = l;
       pair_sync(quarter);
-      const float ltot = x_l[row] + x_l[BQ + row];
+      float ltot = x_l[row] + x_l[BQ + row];
       mbar_wait(BAR(B_OFULL), it & 1);
       tc_fence_after();
+      if constexpr (LSUM && TILE_SPLIT && !EXACT) {
+        // row sum of P from the tensor core (O column 64); an overflowed
+        // stale offset shows up as inf / a huge sum -> exact repair launch
+        uint32_t lr;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(lr) : "r"(tmem + lane_off + TM_O + 64));
+        tmem_wait_ld();
+        asm volatile("" : "+r"(lr));
+        ltot = __uint_as_float(lr);
+        ovf = !(ltot <= 1.2676506e30f);  // 2^100: also keeps O = sum p v finite
+      }
       const bool store = row < I.rows;
       const int32_t pr = I.row0 + row;
       const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
