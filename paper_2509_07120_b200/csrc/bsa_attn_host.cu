@@ -390,7 +390,10 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
     env_f16 = f ? atoi(f) : -1;
   }
   const int v_f16 = env_f16 >= 0 ? env_f16 : 0;
-  const int exp_poly = env_poly >= 0 ? env_poly : 0;
+  // 3 of every 8 exp2 pairs on the FMA pipe (degree-2 polynomial), the rest
+  // on MUFU: the kernel is MUFU-bound at d=64 (profiles/r01_summary.md);
+  // measured 0: 90.0 ms, 2: 85.4, 3: 84.5, 4: 90.9
+  const int exp_poly = env_poly >= 0 ? env_poly : 3;
   rc = launch_pack(q, G, inputs_permuted, W.qp, st);
   if (!rc) rc = launch_pack(k, G, inputs_permuted, W.kp, st);
   if (!rc)

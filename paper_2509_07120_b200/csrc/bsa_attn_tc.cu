@@ -256,19 +256,29 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// 2^x for a pair on the FMA pipe (x <= ~8): round-to-nearest split
-// x = j + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (max rel err 7.7e-5,
-// far below the 16-bit rounding of P), exponent added as an integer.
+#ifndef BSA_TC_POLY_DEG
+#define BSA_TC_POLY_DEG 2
+#endif
+// 2^x for a pair on the FMA pipe (x < 128): round-to-nearest split
+// x = j + f, f in [-0.5, 0.5], minimax polynomial for 2^f, exponent added as
+// an integer.  Degree 3: max rel err 7.5e-5 (for fp16 P); degree 2: 1.7e-3,
+// below the 2^-9 rounding of a bf16 P, one f32x2 FMA cheaper.
+template <int DEG>
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
   const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
   const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
-  float2 p = __ffma2_rn(make_float2(0.05508868f, 0.05508868f), f,
-                        make_float2(0.24260405f, 0.24260405f));
-  p = __ffma2_rn(p, f, make_float2(0.6932762f, 0.6932762f));
-  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  float2 p;
+  if constexpr (DEG == 2) {
+    p = __ffma2_rn(make_float2(0.23842570f, 0.23842570f), f, make_float2(0.70344281f, 0.70344281f));
+    p = __ffma2_rn(p, f, make_float2(1.00044298f, 1.00044298f));
+  } else {
+    p = __ffma2_rn(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
+    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+    p = __ffma2_rn(p, f, make_float2(0.99992812f, 0.99992812f));
+  }
   // (t_bits << 23) == (j << 23) mod 2^32 because t = 1.5*2^23 + j
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
@@ -306,7 +316,7 @@ __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float
   for (int e = 0; e < 16; ++e) {
     const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
     float2 p;
-    if ((e & 7) < POLY) p = exp2_poly2(x);
+    if ((e & 7) < POLY) p = exp2_poly2<F16P ? 3 : BSA_TC_POLY_DEG>(x);
     else p = make_float2(ex2(x.x), ex2(x.y));
     if constexpr (SUM) rs[e & 3] = __fadd2_rn(rs[e & 3], p);
     if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
@@ -963,6 +973,7 @@ static int launch_pick(const CUtensorMap& mk, const CUtensorMap& mv, const AttnG
     case 1: return launch_variant<1, false, EXACT>(mk, mv, G, a, grid, st);
     case 2: return launch_variant<2, false, EXACT>(mk, mv, G, a, grid, st);
     case 3: return launch_variant<3, false, EXACT>(mk, mv, G, a, grid, st);
+    case 4: return launch_variant<4, false, EXACT>(mk, mv, G, a, grid, st);
     case 16: return launch_variant<0, true, EXACT>(mk, mv, G, a, grid, st);
     case 18: return launch_variant<2, true, EXACT>(mk, mv, G, a, grid, st);
     default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
