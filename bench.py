@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
+    ap.add_argument("--shard-chunk", type=int, default=4,
+                    help="heads per pipeline chunk of --mode sharded (comm overlaps kernels)")
     ap.add_argument("--e2e-chunk", type=int, default=2,
                     help="heads per pipeline chunk of the host-memory e2e leg")
     ap.add_argument("--specials", type=int, default=S_PER_FRAME,
@@ -187,13 +189,17 @@ def run_ours(a):
         plan = ShardPlan(lay, world)
         t0, t1 = plan.token_range(rank)
         q_in, k_in, v_in = (x[:, t0:t1].contiguous() for x in (q, k, v))
+        # second communicator: per-chunk mask gathers / output all-reduces do
+        # not queue behind the big Q/K/V gathers
+        comm = dist.new_group(backend="nccl") if world > 1 else None
     else:
         q_in, k_in, v_in = q, k, v
 
     def step(qq, kk, vv, timing=False):
         if sharded:
             return sharded_sparse_attention(qq, kk, vv, lay, pol, inputs="sharded",
-                                            return_mask=True)
+                                            return_mask=True, chunk_heads=a.shard_chunk,
+                                            comm_group=comm)
         mask = bsa.predict_mask(qq, kk, pol, layout=lay)
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
         return bsa.sparse_attention(job, timing=timing), mask

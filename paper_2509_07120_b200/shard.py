@@ -204,14 +204,42 @@ def sharded_predict_mask(q_full, k_full, layout: TokenLayout, policy: MaskPolicy
                                   counts.reshape(-1).contiguous(), h, g)
 
 
+def _gather_async(x_local: torch.Tensor, plan: ShardPlan, group):
+    """Start the padded all-gather of one frame shard; returns (work, parts)."""
+    pad_tok = plan.max_frames * plan.tokens_per_frame
+    h, n, d = x_local.shape
+    buf = torch.zeros((h, pad_tok, d), dtype=x_local.dtype, device=x_local.device)
+    buf[:, :n] = x_local
+    parts = [torch.empty_like(buf) for _ in range(plan.world)]
+    work = dist.all_gather(parts, buf, group=group, async_op=True)
+    return work, parts
+
+
+def _assemble(parts, plan: ShardPlan) -> torch.Tensor:
+    pieces = []
+    for r, part in enumerate(parts):
+        a, b = plan.token_range(r)
+        pieces.append(part[:, :b - a])
+    return torch.cat(pieces, dim=1)
+
+
 def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, group=None,
-                             inputs: str = "sharded", ops=None, return_mask: bool = False):
+                             inputs: str = "sharded", ops=None, return_mask: bool = False,
+                             chunk_heads: int | None = None, comm_group=None):
     """One block-sparse global-attention layer over every rank of `group`.
 
     inputs="sharded":    q/k/v are this rank's frames (ShardPlan.frame_range);
                          the result is this rank's frames of the output.
     inputs="replicated": q/k/v are the full sequence on every rank; the
                          result is the full output on every rank.
+
+    chunk_heads: pipeline the layer over chunks of heads (heads are
+    independent through the whole path). The Q/K/V all-gathers of every
+    chunk start at once, asynchronously, on `group`. Each chunk's mask
+    all-gather and output all-reduce go on `comm_group` (default: `group`;
+    pass a second communicator so they do not queue behind the big
+    gathers). So communication overlaps the previous chunks' kernels.
+    Results are bit-identical to the unchunked call.
     """
     if inputs not in ("sharded", "replicated"):
         raise ValueError(f"inputs must be 'sharded' or 'replicated', got {inputs!r}")
@@ -219,20 +247,52 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
     rank, world = _rank_world(group)
     g = policy.geometry
     plan = ShardPlan(layout, world, g.block_q, g.block_k)
-    if inputs == "sharded":
-        q_full = gather_sequence(q, plan, rank, group)
-        k_full = gather_sequence(k, plan, rank, group)
-        v_full = gather_sequence(v, plan, rank, group)
-    else:
-        q_full, k_full, v_full = q, k, v
-    if q_full.shape[1] != layout.total_tokens:
-        raise ValueError(
-            f"inputs have {q_full.shape[1]} tokens but layout describes {layout.total_tokens}")
-    mask = sharded_predict_mask(q_full, k_full, layout, policy, plan, rank, group, ops)
-    out = ops.attend(q_full, k_full, v_full, layout, mask, rank, world)
-    if world > 1:
-        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    H = q.shape[0]
+    if chunk_heads is not None and chunk_heads < 1:
+        raise ValueError(f"chunk_heads must be >= 1, got {chunk_heads}")
     if inputs == "sharded":
         t0, t1 = plan.token_range(rank)
+        if q.shape[1] != t1 - t0:
+            raise ValueError(f"rank {rank} holds {q.shape[1]} tokens, plan expects {t1 - t0}")
+    elif q.shape[1] != layout.total_tokens:
+        raise ValueError(
+            f"inputs have {q.shape[1]} tokens but layout describes {layout.total_tokens}")
+    chunk = chunk_heads or H
+    spans = [(a, min(H, a + chunk)) for a in range(0, H, chunk)]
+    cgroup = comm_group if comm_group is not None else group
+
+    pending = []
+    if inputs == "sharded" and world > 1:
+        # every chunk's Q/K/V gathers start now; chunk c's kernels only wait
+        # for chunk c's gathers
+        for a, b in spans:
+            pending.append([_gather_async(x[a:b], plan, group) for x in (q, k, v)])
+    outs, masks, reduces = [], [], []
+    for c, (a, b) in enumerate(spans):
+        if inputs == "sharded" and world > 1:
+            full = []
+            for work, parts in pending[c]:
+                work.wait()
+                full.append(_assemble(parts, plan))
+            qf, kf, vf = full
+        else:
+            qf, kf, vf = q[a:b], k[a:b], v[a:b]
+        mask = sharded_predict_mask(qf, kf, layout, policy, plan, rank, cgroup, ops)
+        out = ops.attend(qf, kf, vf, layout, mask, rank, world)
+        if world > 1:
+            reduces.append(dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup,
+                                           async_op=True))
+        outs.append(out)
+        masks.append(mask)
+    for work in reduces:
+        work.wait()
+    out = outs[0] if len(outs) == 1 else torch.cat(outs, dim=0)
+    if inputs == "sharded":
         out = out[:, t0:t1].contiguous()
-    return (out, mask) if return_mask else out
+    if not return_mask:
+        return out
+    if len(masks) == 1:
+        return out, masks[0]
+    bits = torch.cat([m.device_bits() for m in masks], dim=0)
+    counts = torch.cat([m.device_counts() for m in masks], dim=0)
+    return out, BlockMask._from_device(bits, counts, H, g)

@@ -99,5 +99,9 @@ def test_world1_process_group_end_to_end(bsa):
             bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, ref_mask))
         assert torch.equal(mask.device_bits(), ref_mask.device_bits())
         assert torch.equal(out, ref)
+        out2, mask2 = sharded_sparse_attention(q, k, v, lay, pol, return_mask=True,
+                                               chunk_heads=1)  # per-head pipeline
+        assert torch.equal(out2, ref)
+        assert torch.equal(mask2.device_bits(), ref_mask.device_bits())
     finally:
         dist.destroy_process_group()

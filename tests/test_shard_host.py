@@ -66,7 +66,7 @@ class OracleOps:
         # as long as the shards are disjoint and cover everything
         blocks = mask.blocks
         T = layout.total_tokens
-        out = np.zeros((H, T, D), dtype=np.float64)
+        out = np.zeros((q.shape[0], T, D), dtype=np.float64)
         rows = [t for t in range(T) if t % num_shards == shard]
         res = oracle.masked_attention_f64(q.numpy(), k.numpy(), v.numpy(), layout.frames,
                                           layout.patches_per_frame, layout.specials_per_frame,
@@ -81,7 +81,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, inputs, result_q):
+def _worker(rank, world, port, inputs, result_q, chunk=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -97,17 +97,18 @@ def _worker(rank, world, port, inputs, result_q):
         else:
             xs = [torch.from_numpy(x) for x in (q, k, v)]
         out, mask = sharded_sparse_attention(*xs, lay, pol, inputs=inputs, ops=OracleOps(),
-                                             return_mask=True)
+                                             return_mask=True, chunk_heads=chunk)
         result_q.put((rank, out.numpy(), mask.blocks.copy()))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, inputs):
+def _run(world, inputs, chunk=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, inputs, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, inputs, q, chunk))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -138,6 +139,17 @@ def test_frame_sharded_matches_single_process(world, single_process):
         assert np.array_equal(blocks, mask), f"rank {r}: gathered mask differs"
         t0, t1 = plan.token_range(r)
         assert out.shape == (H, t1 - t0, D)
+        np.testing.assert_allclose(out, ref[:, t0:t1], rtol=0, atol=1e-12)
+
+
+def test_head_chunked_pipeline_matches(single_process):
+    """chunk_heads=1: per-head async gathers / all-reduces, same result."""
+    lay, mask, ref = single_process
+    res = _run(2, "sharded", chunk=1)
+    plan = ShardPlan(lay, 2, BQ, BK)
+    for r, (out, blocks) in res.items():
+        assert np.array_equal(blocks, mask)
+        t0, t1 = plan.token_range(r)
         np.testing.assert_allclose(out, ref[:, t0:t1], rtol=0, atol=1e-12)
 
 
