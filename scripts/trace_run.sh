@@ -1,4 +1,5 @@
+# Pipeline trace of CTA 0 (debug): build the trace variant first with
+#   scripts/build_variants.sh tr:"-DBSA_TC_TRACE_BUILD"
+# then run this under gpurun and analyse with scripts/trace_analyze.py.
 mkdir -p gpurun_out
-BSA_TC_TRACE=gpurun_out/trace200.bin timeout -s KILL 200 python scripts/profile_step.py --steps 1 > gpurun_out/trace.log 2>&1
-timeout -s KILL 300 python -m pytest tests/test_gpu_attention.py -x -q 2>&1 | tail -3 > gpurun_out/t_attn.log
-timeout -s KILL 200 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-dense > gpurun_out/bench_nt.json 2>&1
+BSA_LIB_VARIANT=tr BSA_TC_TRACE=gpurun_out/trace200.bin timeout -s KILL 200 python scripts/profile_step.py --steps 1 > gpurun_out/trace.log 2>&1
