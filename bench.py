@@ -365,7 +365,11 @@ def run_ours(a):
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
                          "kernel": "bsa_tc_kernel", "algorithmic_flops_per_launch": flops,
-                         "dense_flops": dense_flops, "peak_source": peak_src},
+                         "dense_flops": dense_flops, "peak_source": peak_src,
+                         # the same kernel against the measured SUSTAINED cuBLAS bf16
+                         # figure (power-capped clocks, like this multi-second loop)
+                         "frac_of_sustained": (achieved_tf / float(peaks["bf16_tflops_sustained"])
+                                               if "bf16_tflops_sustained" in peaks else None)},
             "e2e": e2e,
             # per step: 2 pool8, scores, pw_plan, softsel, fallback, 3 pack,
             # schedule, bsa_tc_kernel + its exact-repair launch (ncu launch
