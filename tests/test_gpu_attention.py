@@ -239,3 +239,24 @@ def test_validation_errors(bsa):
     with pytest.raises(ValueError, match="heads"):
         bsa.SparseAttentionJob(bsa.AttentionInputs(q2, k2, v2), lay,
                                bsa.full_mask(bsa.BlockGeometry(64, 32, 16), 1))
+
+
+@pytest.mark.parametrize("frames,patches,specials,heads", [
+    (1, 30, 5, 1),      # T < one key tile, single q-block, ragged everything
+    (1, 64, 0, 1),      # no specials: the key stream starts with a patch block
+    (2, 129, 3, 3),     # q-block tail of 2 rows, key tail of 2 tokens
+    (3, 1369, 0, 1),    # VGGT frames without special tokens
+])
+def test_tc_edge_geometries(bsa, oracle, frames, patches, specials, heads):
+    lay = bsa.TokenLayout(frames, patches, specials)
+    q, k, v = make_qkv(heads, lay.total_tokens, 64, 101 + patches)
+    qd, kd, vd = _to_bf16(q, k, v)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    mask = bsa.predict_mask(qd, kd, bsa.MaskPolicy(0.4, 0.8, g), layout=lay)
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, mask)
+    assert bsa.attention_path(job) == "tc"
+    out = bsa.sparse_attention(job).float().cpu().numpy()
+    qb, kb, vb = (t.float().cpu().numpy() for t in (qd, kd, vd))
+    ref = oracle.masked_attention_f64(qb, kb, vb, frames, patches, specials, mask.blocks, 128, 64)
+    assert np.isfinite(out).all()
+    assert _rel(out, ref) <= BF16_REL_TOL
