@@ -209,6 +209,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -305,6 +312,23 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, i
 // The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
 // the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
 // V) instead of bf16 P.
+#ifndef BSA_TC_LD32
+#define BSA_TC_LD32 0
+#endif
+#ifndef BSA_TC_POLY_SPREAD
+#define BSA_TC_POLY_SPREAD 0
+#endif
+// which of each 8 consecutive pairs take the FMA-pipe polynomial: the first
+// POLY (SPREAD 0), or POLY spread evenly over the 8 (SPREAD 1: 0,3,6 / 0,2,4,6)
+template <int POLY>
+__device__ __forceinline__ constexpr bool poly_pair(int e) {
+  if constexpr (BSA_TC_POLY_SPREAD == 0 || POLY == 0) {
+    return (e & 7) < POLY;
+  } else {
+    return ((e & 7) * POLY) % 8 < POLY;
+  }
+}
+
 template <int POLY, bool F16P, bool SUM = true>
 __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float m,
                                           uint32_t p_taddr) {
@@ -316,7 +340,7 @@ __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float
   for (int e = 0; e < 16; ++e) {
     const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
     float2 p;
-    if ((e & 7) < POLY) p = exp2_poly2<F16P ? 3 : BSA_TC_POLY_DEG>(x);
+    if (poly_pair<POLY>(e)) p = exp2_poly2<F16P ? 3 : BSA_TC_POLY_DEG>(x);
     else p = make_float2(ex2(x.x), ex2(x.y));
     if constexpr (SUM) rs[e & 3] = __fadd2_rn(rs[e & 3], p);
     if constexpr (F16P) r[e] = cvt_h2(p.x, p.y);
@@ -704,8 +728,12 @@ __global__ void __maxnreg__(MAX_REGS)
             // this thread has already read
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + hh * 32;
+#if BSA_TC_LD32
+            tmem_ld32(s_col, sr);
+#else
             tmem_ld16(s_col, &sr[0]);
             tmem_ld16(s_col + 16, &sr[16]);
+#endif
             tmem_wait_ld();
             reg_fence16(&sr[0]);
             reg_fence16(&sr[16]);
