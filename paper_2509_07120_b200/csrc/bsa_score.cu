@@ -241,8 +241,14 @@ __device__ __forceinline__ void load8(const T* ptr, float (&v)[8]) {
   }
 }
 
+#ifndef BSA_POOL_MINB
+#define BSA_POOL_MINB 6
+#endif
+#ifndef BSA_POOL_UNROLL
+#define BSA_POOL_UNROLL 2
+#endif
 template <typename T>
-__global__ void __launch_bounds__(256) pool8_kernel(const T* __restrict__ x, int64_t sH,
+__global__ void __launch_bounds__(256, BSA_POOL_MINB) pool8_kernel(const T* __restrict__ x, int64_t sH,
                                                     int64_t sT, int64_t H, int64_t n, int d,
                                                     int block, Layout L, int gather,
                                                     float* __restrict__ out, int64_t nb) {
@@ -282,17 +288,18 @@ __global__ void __launch_bounds__(256) pool8_kernel(const T* __restrict__ x, int
         rp += (int64_t)S * sT;
       }
     };
-    // four rows in flight per step, added strictly in row order
+    // BSA_POOL_UNROLL rows in flight per step, added strictly in row order
+    constexpr int U = BSA_POOL_UNROLL;
     int64_t i = 8;
-    for (; i + 24 < stop; i += 32) {
-      float v[4][8];
+    for (; i + 8 * (U - 1) < stop; i += 8 * U) {
+      float v[U][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < U; ++q) {
         advance();
         load8<T>(rp, v[q]);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < U; ++q)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], v[q][c]);
     }
@@ -321,6 +328,115 @@ __global__ void __launch_bounds__(256) pool8_kernel(const T* __restrict__ x, int
   if (j == 0 && live) {
     float x0[8];
     load8<T>(row_ptr(r0), x0);
+    const float fl = (float)len;
+    float o[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = __fdiv_rn(len > 1 ? __fadd_rn(x0[c], acc[c]) : x0[c], fl);
+    float4* op = reinterpret_cast<float4*>(out + pr * d + cg * 8);
+    op[0] = make_float4(o[0], o[1], o[2], o[3]);
+    op[1] = make_float4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// cp.async-staged pool8 for bf16 rows (the bench shape): every thread issues
+// ALL its 16-byte row loads (its accumulator chain, its tail row, x0) as
+// cp.async into shared-memory slots laid out [slot][thread] (conflict-free
+// read-back), then sums them in exactly pool8's order.  No registers are
+// held by in-flight loads, so each SM keeps ~200 KB of reads in flight -- the
+// latency-bandwidth product HBM3e needs.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(uint4 t, float (&v)[8]) {
+  const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[q]));
+    v[2 * q] = f2.x;
+    v[2 * q + 1] = f2.y;
+  }
+}
+
+__global__ void __launch_bounds__(256) pool8a_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     int64_t sH, int64_t sT, int64_t H, int64_t n,
+                                                     int d, int block, Layout L, int gather,
+                                                     float* __restrict__ out, int64_t nb,
+                                                     int slots) {
+  extern __shared__ uint4 stage[];  // [slots][256]
+  const int cgs = d / 8;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (int)(t & 7);
+  const int glane = (int)(threadIdx.x & 31) & ~7;
+  const unsigned gmask = 0xFFu << glane;
+  const int64_t cgi = t >> 3;
+  const bool live = cgi < H * nb * cgs;
+  const int64_t pr = live ? cgi / cgs : 0;
+  const int cg = live ? (int)(cgi % cgs) : 0;
+  const int64_t h = pr / nb, b = pr % nb;
+  const int64_t r0 = b * block;
+  const int64_t len = live ? min((int64_t)block, n - r0) : 1;
+  const __nv_bfloat16* base = x + h * sH + cg * 8;
+  const uint32_t P = (uint32_t)L.P, S = (uint32_t)L.S, so = L.specials_first ? S : 0u;
+  auto row_ptr = [&](int64_t p) {
+    int64_t src = p;
+    if (gather) src = p + (int64_t)((uint32_t)p / P) * S + so;
+    return base + src * sT;
+  };
+  auto slot = [&](int k) { return &stage[k * 256 + threadIdx.x]; };
+  const int64_t first = r0 + 1, m = len - 1;
+  const int64_t stop = m >= 8 ? m - (m % 8) : 0;
+  const int nchain = (int)(stop / 8);      // rows of this accumulator chain
+  const int ntail = (int)(m - stop);
+  const int tail_slot = slots - 2, x0_slot = slots - 1;
+  // ---- issue every load of this thread ----
+  if (nchain > 0) {
+    uint32_t p = (uint32_t)(first + j);
+    uint32_t f = gather ? p / P : 0u, fend = gather ? (f + 1) * P : 0xFFFFFFFFu;
+    const __nv_bfloat16* rp = base + ((int64_t)p + (int64_t)f * S + (gather ? so : 0u)) * sT;
+    cp_async16(slot(0), rp);
+    for (int k = 1; k < nchain; ++k) {
+      p += 8;
+      rp += 8 * sT;
+      while (p >= fend) {  // crossed into the next frame: skip its specials
+        fend += P;
+        rp += (int64_t)S * sT;
+      }
+      cp_async16(slot(k), rp);
+    }
+  }
+  if (j < ntail) cp_async16(slot(tail_slot), row_ptr(first + stop + j));
+  if (j == 0 && live) cp_async16(slot(x0_slot), row_ptr(r0));
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  // ---- sum in pool8's exact order (own slots only: no block barrier) ----
+  float acc[8];
+  if (nchain > 0) {
+    bf16x8_to_f32(*slot(0), acc);
+    for (int k = 1; k < nchain; ++k) {
+      float v[8];
+      bf16x8_to_f32(*slot(k), v);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], v[c]);
+    }
+#pragma unroll
+    for (int sh = 1; sh < 8; sh <<= 1)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __shfl_xor_sync(gmask, acc[c], sh));
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = 0.0f;
+  }
+  float tv[8];
+  if (j < ntail) bf16x8_to_f32(*slot(tail_slot), tv);
+  for (int k = 0; k < ntail; ++k)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = __fadd_rn(acc[c], __shfl_sync(gmask, tv[c], glane + k));
+  if (j == 0 && live) {
+    float x0[8];
+    bf16x8_to_f32(*slot(x0_slot), x0);
     const float fl = (float)len;
     float o[8];
 #pragma unroll
@@ -1176,7 +1292,20 @@ static int launch_pool_t(const bsa_tensor* x, const Layout& L, bool gather, int6
   };
   // one warp-row per pooled row: lanes cover the head dim with 2 (d <= 64)
   // or 4 (d <= 128) columns each, i.e. fully coalesced 128/256-byte rows
-  if (d % 8 == 0 && block <= 129 && aligned(8) && (8 * sizeof(T)) % 16 == 0) {
+#ifndef BSA_POOL_ASYNC
+#define BSA_POOL_ASYNC 1
+#endif
+  if (BSA_POOL_ASYNC && sizeof(T) == 2 && d % 8 == 0 && block <= 129 && aligned(8)) {
+    const int64_t nb = ceil_div(n, block);
+    const int64_t threads = x->heads * nb * (d / 8) * 8;
+    const int slots = (block - 1) / 8 + 2;  // chain rows + tail row + x0
+    const size_t smem = (size_t)slots * 256 * 16;
+    BSA_CUDA_TRY(cudaFuncSetAttribute(pool8a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    pool8a_kernel<<<(unsigned)ceil_div(threads, 256), 256, smem, st>>>(
+        (const __nv_bfloat16*)x->data, x->stride_head, x->stride_token, x->heads, n, d, block, L,
+        gather ? 1 : 0, out, nb, slots);
+  } else if (d % 8 == 0 && block <= 129 && aligned(8) && (8 * sizeof(T)) % 16 == 0) {
     const int64_t nb = ceil_div(n, block);
     const int64_t threads = x->heads * nb * (d / 8) * 8;
     pool8_kernel<T><<<(unsigned)ceil_div(threads, 256), 256, 0, st>>>(
