@@ -10,26 +10,30 @@
 //               TMA-loads, per 64-key tile, the K and V chunk of the next
 //               selected block (the gather is done by TMA coordinates) into
 //               separate SW128 shared-memory rings (K runs VLAG tiles ahead).
-//   warp 9      MMA issuer: S = Q K^T with Q read from TMEM (tcgen05.mma .ts,
-//               kind::f16, M=128 N=64, fp32 in TMEM, two S buffers) and
-//               O += P V with P read from TMEM and V from shared memory;
+//   warp 9      MMA issuer (warp-uniform loop, elect.sync issues):
+//               S = Q K^T with Q read from TMEM (tcgen05.mma .ts, kind::f16,
+//               M=128 N=64, fp32, two S buffers) and O += P [V | 1] with P
+//               read from TMEM and V from shared memory (N=80: an all-ones
+//               block beside each V stage makes O[:,64] the row sum of P);
 //               tcgen05.commit -> mbarriers.  S(j+1) is in flight while the
 //               softmax warps work on tile j.
-//   warps 0-7   softmax + epilogue, TWO threads per query row: warp w (w<4)
-//               and warp w+4 own TMEM lanes 32w..32w+31 and split each S row
-//               into key halves 0-31 / 32-63 (columns 0-31 / 32-63 of the S
-//               tile); each half writes its P over its own S columns.  Four
-//               softmax warps per SM sub-partition hide each other's MUFU,
-//               TMEM-load and barrier latencies.
+//   warps 0-7   softmax + epilogue.  Warp w (w<4) and warp w+4 own TMEM lanes
+//               32w..32w+31.  Stale-max launch: the two warp groups take
+//               alternate key tiles (S buffer 0 / 1), full rows, in 32-column
+//               halves; four softmax warps per SM sub-partition keep the
+//               MUFU and FMA pipes busy.  Exact launch: the groups split
+//               every tile into key halves 0-31 / 32-63 instead.
+// exp2: 5 of every 8 pairs on MUFU (ex2.approx), 3 on the FMA pipe as a
+// degree-2 minimax polynomial (rel err 1.7e-3 < bf16 rounding of P).
 // Softmax offset ("stale max"): the row max of the item's first tile (the two
-// halves exchange it once through shared memory) is kept for the whole item;
-// online softmax does not depend on the offset, only overflow does.  Every
-// tile's P sum bounds its values; an item whose sum ever exceeds P_LIMIT
-// (scores grew by > 64 in log2 units -- never for attention logits of sane
-// scale) is listed and recomputed by a second, exact-max launch of the same
-// kernel (per-tile max exchanged between the halves, lazy 2^8 rescaling of O).
-// The row sum l is kept per half and combined in the epilogue.
-// TMEM (256 of 512 columns per CTA): S0|S1 (2x64, P over S) O (64) Q (32).
+// groups exchange it once through shared memory) is kept for the whole item;
+// online softmax does not depend on the offset, only overflow does.  An item
+// whose tensor-core row sum l ends non-finite or above 2^100 (scores grew by
+// ~100 log2 units beyond the first tile's max -- never for attention logits
+// of sane scale) is listed and recomputed by a second, exact-max launch of
+// the same kernel (per-tile max exchanged between the halves, lazy 2^8
+// rescaling of O, l summed in registers).
+// TMEM (256 of 512 columns per CTA): S0|S1 (2x64, P over S) O (80) Q (32).
 #include <cuda.h>
 
 #include <cstdio>
