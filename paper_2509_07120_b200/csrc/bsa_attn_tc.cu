@@ -55,8 +55,17 @@ namespace tc {
 // two column halves of every tile -- their phases interleave on the MUFU and
 // the per-tile overhead is paid half as often.
 constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
+#ifndef BSA_TC_SEPP
+#define BSA_TC_SEPP 0
+#endif
+// SEPP: P gets its own TMEM buffers instead of overwriting its S tile, so
+// S(j+2) can be computed as soon as the softmax has copied S(j) to
+// registers (not only after PV(j) has read P(j)).  The TMEM this costs
+// moves Q back to shared memory (S = Q K^T as an .ss MMA) and drops LSUM.
+constexpr bool SEPP = BSA_TC_SEPP != 0;
+constexpr bool QT = !SEPP;  // Q tile in TMEM (.ts S MMA), else TMA'd to smem
 #ifndef BSA_TC_LSUM
-#define BSA_TC_LSUM 1
+#define BSA_TC_LSUM (BSA_TC_SEPP ? 0 : 1)
 #endif
 // LSUM: the PV MMA runs with N = 80: columns 64-79 of its B operand are an
 // all-ones block kept beside every V stage (at the descriptor's LBO), so
@@ -64,10 +73,10 @@ constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
 // no additions.  Costs 25% more PV MMA work and 8 KB of smem per V stage.
 constexpr bool LSUM = BSA_TC_LSUM != 0;
 #ifndef BSA_TC_NK
-#define BSA_TC_NK (BSA_TC_LSUM ? 5 : 7)
+#define BSA_TC_NK (BSA_TC_SEPP ? 6 : BSA_TC_LSUM ? 5 : 7)
 #endif
 #ifndef BSA_TC_NV
-#define BSA_TC_NV (BSA_TC_LSUM ? 4 : 6)
+#define BSA_TC_NV (BSA_TC_SEPP ? 5 : BSA_TC_LSUM ? 4 : 6)
 #endif
 #ifndef BSA_TC_VLAG
 #define BSA_TC_VLAG 2
@@ -81,7 +90,9 @@ constexpr int NUM_THREADS = 320;
 constexpr int CTAS_PER_SM = 2;
 // registers per thread: two CTAs x 320 threads share 64K (8-register granules)
 constexpr int MAX_REGS = (65536 / (CTAS_PER_SM * NUM_THREADS)) / 8 * 8;
-constexpr int OFF_K = 0;
+constexpr int Q_BYTES = BQ * D * 2;     // 16 KB (SEPP: Q tile in smem)
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = QT ? 0 : Q_BYTES;
 constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
 constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ its ones block)
 constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // half-row exchange: 3 x 2 x 128 floats
@@ -90,7 +101,16 @@ constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;    // barriers/ring + alignment
 static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
 constexpr uint32_t TMEM_COLS = 256;
 // O: 64 columns (+16 row-sum columns with LSUM)
-constexpr uint32_t TM_S = 0, TM_O = 128, TM_Q = LSUM ? 224 : 192, O_COLS = LSUM ? 80 : 64;
+// SEPP: S0|S1 (2x64) P0|P1 (2x32) O (64); else S0|S1 (P over S) O (64|80) Q (32)
+constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = SEPP ? 192 : 128, TM_Q = LSUM ? 224 : 192,
+                   O_COLS = LSUM ? 80 : 64;
+static_assert(!(SEPP && LSUM), "SEPP leaves no TMEM for the row-sum columns");
+// TMEM column of the 16 packed-P columns that key half hh (32 keys) of
+// S buffer sb writes: its own P buffer (SEPP) or over its S columns
+__device__ __forceinline__ uint32_t p_col16(uint32_t sb, int hh, bool column_split) {
+  if constexpr (SEPP) return TM_P + sb * 32 + hh * 16;
+  return TM_S + sb * 64 + (column_split ? hh * 32 : hh * 16);
+}
 
 // barrier slots (8 bytes each) inside the barrier region
 enum {
@@ -106,7 +126,9 @@ enum {
   B_OEMPTY = B_OFULL + 1,   // [1]
   B_IFULL = B_OEMPTY + 1,   // [2]
   B_IEMPTY = B_IFULL + 2,   // [2]  8 softmax warps + MMA warp
-  B_COUNT = B_IEMPTY + 2
+  B_QEMPTY = B_IEMPTY + 2,  // [1]  (SEPP) Q smem tile free
+  B_SEMPTY = B_QEMPTY + 1,  // [2]  (SEPP) S tile copied to registers
+  B_COUNT = B_SEMPTY + 2
 };
 static_assert(B_COUNT * 8 + 32 <= 512, "barrier region");
 
@@ -450,8 +472,8 @@ constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
 // ---------------------------------------------------------------------------
 template <int POLY, bool F16P, bool EXACT>
 __global__ void __maxnreg__(MAX_REGS)
-    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                  AttnGeom G, TcArgs A) {
+    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -464,10 +486,12 @@ __global__ void __maxnreg__(MAX_REGS)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(BAR(B_QFULL), SM_WARPS);
+    mbar_init(BAR(B_QFULL), QT ? SM_WARPS : 1);
+    mbar_init(BAR(B_QEMPTY), 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(BAR(B_SFULL + i), 1);
       mbar_init(BAR(B_PFULL + i), (TILE_SPLIT && !EXACT) ? SM_WARPS / 2 : SM_WARPS);
+      mbar_init(BAR(B_SEMPTY + i), (TILE_SPLIT && !EXACT) ? SM_WARPS / 2 : SM_WARPS);
       mbar_init(BAR(B_PFREE + i), 1);
       mbar_init(BAR(B_IFULL + i), 1);
       mbar_init(BAR(B_IEMPTY + i), SM_WARPS + 1);
@@ -501,6 +525,7 @@ __global__ void __maxnreg__(MAX_REGS)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == PRODUCER_WARP && lane == 0) {
+    if (!QT) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
   }
@@ -536,6 +561,15 @@ __global__ void __maxnreg__(MAX_REGS)
       __syncwarp();
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
+      if constexpr (!QT) {
+        // Q tile -> smem once the previous item's last S MMA has read it
+        mbar_wait(BAR(B_QEMPTY), (it & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(BAR(B_QFULL), Q_BYTES);
+          tma_load_3d(sbase + OFF_Q, &tm_q, BAR(B_QFULL), 0, I.row0, I.h);
+        }
+        __syncwarp();
+      }
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
       KeyChunker ck(G, I.qb, mrow, CH);
@@ -581,8 +615,12 @@ __global__ void __maxnreg__(MAX_REGS)
     uint32_t it = 0, gs = 0, gp = 0;
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
+    const uint64_t dq = sdesc(sbase + OFF_Q, 16, 1024);  // (SEPP) Q in smem
     const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + OFF_V, 8192, 1024);
+    // SEPP: S(j) only needs the softmax to have copied S(j-2), so PV trails
+    // S by two tiles and the next S tile is always ready in time
+    constexpr int PV_LAG = SEPP ? 2 : 1;
     while (true) {
       const uint32_t slot = it & 1;
       mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
@@ -608,8 +646,10 @@ __global__ void __maxnreg__(MAX_REGS)
           for (int k = 0; k < CH / 16; ++k)
             if (BSA_TC_EXPERIMENT != 2)
               mma_ts(tmem + TM_O,
-                     tmem + TM_S + pb * 64 +
-                         ((TILE_SPLIT && !EXACT) ? k * 8 : (k >> 1) * 32 + (k & 1) * 8),
+                     tmem + (SEPP ? TM_P + pb * 32 + k * 8
+                                  : TM_S + pb * 64 +
+                                        ((TILE_SPLIT && !EXACT) ? k * 8
+                                                                : (k >> 1) * 32 + (k & 1) * 8)),
                      dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(B_PFREE + pb));
           tc_commit(BAR(B_VEMPTY + sv));
@@ -622,24 +662,32 @@ __global__ void __maxnreg__(MAX_REGS)
         const uint32_t sk = gs % NK, sb = gs & 1;
         mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
         if (lane == 0) BSA_TR(3, gs);
-        mbar_wait(BAR(B_PFREE + sb), ((gs >> 1) & 1) ^ 1);  // PV(gs-2) done
+        // S buffer free: SEPP -> the softmax copied S(gs-2) to registers;
+        // else P(gs-2) was written over it, so PV(gs-2) must be done
+        mbar_wait(BAR((SEPP ? B_SEMPTY : B_PFREE) + sb), ((gs >> 1) & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k)
-            if (BSA_TC_EXPERIMENT != 2)
+          for (int k = 0; k < D / 16; ++k) {
+            if (BSA_TC_EXPERIMENT == 2) continue;
+            if constexpr (QT)
               mma_ts(tmem + TM_S + sb * 64, tmem + TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
                      k > 0 ? 1u : 0u);
+            else
+              mma_ss(tmem + TM_S + sb * 64, dq + (uint64_t)(2 * k), dk + (uint64_t)(2 * k), id_s,
+                     k > 0 ? 1u : 0u);
+          }
           tc_commit(BAR(B_SFULL + sb));
           tc_commit(BAR(B_KEMPTY + sk));
+          if (!QT && j == ntiles - 1) tc_commit(BAR(B_QEMPTY));
           BSA_TR(1, gs);
         }
         __syncwarp();
         ++gs;
-        if (j >= 1) issue_pv(j - 1);
+        if (j >= PV_LAG) issue_pv(j - PV_LAG);
       }
-      issue_pv(ntiles - 1);
+      for (int jj = ntiles > PV_LAG ? ntiles - PV_LAG : 0; jj < ntiles; ++jj) issue_pv(jj);
       if (elect_one()) tc_commit(BAR(B_OFULL));
       __syncwarp();
       ++it;
@@ -667,7 +715,7 @@ __global__ void __maxnreg__(MAX_REGS)
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
-      {
+      if constexpr (QT) {
         // this thread's half of its query row of the packed partitioned Q ->
         // TMEM (16 columns of bf16 pairs: the A operand of S = Q K^T).  The
         // previous item's S MMAs are complete: their S tiles were consumed.
@@ -726,10 +774,15 @@ __global__ void __maxnreg__(MAX_REGS)
           if (lane == 0 && warp < 4) BSA_TR(4 + warp, gg);
           mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
           tc_fence_after();
+          if (SEPP && gg >= 2) {
+            // own P buffer: free once PV(gg-2) has read it
+            mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
+            tc_fence_after();
+          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            // 32 keys at a time; P (16 packed columns) overwrites S columns
-            // this thread has already read
+            // 32 keys at a time; P (16 packed columns) goes to this half's
+            // P columns (SEPP) or over S columns this thread has already read
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + hh * 32;
 #if BSA_TC_LD32
@@ -741,6 +794,12 @@ __global__ void __maxnreg__(MAX_REGS)
             tmem_wait_ld();
             reg_fence16(&sr[0]);
             reg_fence16(&sr[16]);
+            if (SEPP && hh == 1) {
+              // S(gg) is in registers: the MMA warp may compute S(gg+2) here
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
+            }
             float s[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
@@ -754,12 +813,12 @@ __global__ void __maxnreg__(MAX_REGS)
               uint32_t r[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
-              tmem_st16(tmem + lane_off + TM_S + sb * 64 + hh * 16, r);
+              tmem_st16(tmem + lane_off + p_col16(sb, hh, false), r);
             }
             const float lt = 1.0f;
 #else
             const float lt =
-                exp_half<POLY, F16P, !LSUM>(s, sl2, m, tmem + lane_off + TM_S + sb * 64 + hh * 16);
+                exp_half<POLY, F16P, !LSUM>(s, sl2, m, tmem + lane_off + p_col16(sb, hh, false));
 #endif
             if constexpr (!LSUM) {
               ovf |= !(lt <= P_LIMIT);
@@ -789,6 +848,11 @@ __global__ void __maxnreg__(MAX_REGS)
         tmem_wait_ld();
         reg_fence16(&sr[0]);
         reg_fence16(&sr[16]);
+        if constexpr (SEPP) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
+        }
         if (lane == 0 && warp < 4) BSA_TR(8 + warp, gg);
         float s[32];
 #pragma unroll
@@ -839,7 +903,11 @@ __global__ void __maxnreg__(MAX_REGS)
             }
           }
         }
-        const uint32_t p_col = tmem + lane_off + TM_S + sb * 64 + half * 32;
+        const uint32_t p_col = tmem + lane_off + p_col16(sb, half, true);
+        if (SEPP && gg >= 2) {
+          mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
+          tc_fence_after();
+        }
 #if BSA_TC_EXPERIMENT == 1
         float lt;
         {  // timing experiment: no exponentials (results are wrong)
@@ -987,27 +1055,29 @@ cudaEvent_t timing_events(int which) {
 }
 
 template <int POLY, bool F16P, bool EXACT>
-static int launch_variant(const CUtensorMap& mk, const CUtensorMap& mv, const AttnGeom& G,
+static int launch_variant(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const AttnGeom& G,
                           const TcArgs& a, int grid, cudaStream_t st) {
   auto kern = tc::bsa_tc_kernel<POLY, F16P, EXACT>;
   BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     tc::SMEM_BYTES));
-  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mk, mv, G, a);
+  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
 
 template <bool EXACT>
-static int launch_pick(const CUtensorMap& mk, const CUtensorMap& mv, const AttnGeom& G,
+static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                       const AttnGeom& G,
                        const TcArgs& a, int grid, cudaStream_t st) {
   switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {
-    case 0: return launch_variant<0, false, EXACT>(mk, mv, G, a, grid, st);
-    case 1: return launch_variant<1, false, EXACT>(mk, mv, G, a, grid, st);
-    case 2: return launch_variant<2, false, EXACT>(mk, mv, G, a, grid, st);
-    case 3: return launch_variant<3, false, EXACT>(mk, mv, G, a, grid, st);
-    case 4: return launch_variant<4, false, EXACT>(mk, mv, G, a, grid, st);
-    case 16: return launch_variant<0, true, EXACT>(mk, mv, G, a, grid, st);
-    case 18: return launch_variant<2, true, EXACT>(mk, mv, G, a, grid, st);
+    case 0: return launch_variant<0, false, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 1: return launch_variant<1, false, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 2: return launch_variant<2, false, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 3: return launch_variant<3, false, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 4: return launch_variant<4, false, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 16: return launch_variant<0, true, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 18: return launch_variant<2, true, EXACT>(mq, mk, mv, G, a, grid, st);
     default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
   }
 }
@@ -1017,7 +1087,9 @@ static int launch_pick(const CUtensorMap& mk, const CUtensorMap& mv, const AttnG
 // second launch reads a zero count and its CTAs exit at once).
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   CUtensorMap mk, mv;
-  int rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
+  CUtensorMap mq;
+  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);  // (SEPP) Q tile box 64 x 128 rows
+  if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
   if (!rc)
     rc = make_map(&mv, a.vp, G.H, G.T, tc::CH,
                   a.v_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
@@ -1033,7 +1105,7 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_flags, 0, (size_t)a.n_items * 4, st));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_count, 0, 4, st));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
-  rc = launch_pick<false>(mk, mv, G, a, grid, st);
+  rc = launch_pick<false>(mq, mk, mv, G, a, grid, st);
   if (rc) return rc;
   TcArgs r = a;  // repair launch
   r.items = a.ovf_list;
@@ -1041,7 +1113,7 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   r.work_counter = a.work_counter + 1;
   r.num_shards = 1;
   r.shard = 0;
-  rc = launch_pick<true>(mk, mv, G, r, sms, st);
+  rc = launch_pick<true>(mq, mk, mv, G, r, sms, st);
   if (rc) return rc;
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
   if (a.trace) {
