@@ -63,6 +63,10 @@ constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
 // registers (not only after PV(j) has read P(j)).  The TMEM this costs
 // moves Q back to shared memory (S = Q K^T as an .ss MMA) and drops LSUM.
 constexpr bool SEPP = BSA_TC_SEPP != 0;
+#ifndef BSA_TC_INORDER
+#define BSA_TC_INORDER 0
+#endif
+constexpr bool INORDER = BSA_TC_INORDER != 0;
 constexpr bool QT = !SEPP;  // Q tile in TMEM (.ts S MMA), else TMA'd to smem
 #ifndef BSA_TC_LSUM
 #define BSA_TC_LSUM (BSA_TC_SEPP ? 0 : 1)
@@ -663,8 +667,11 @@ __global__ void __maxnreg__(MAX_REGS)
         mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
         if (lane == 0) BSA_TR(3, gs);
         // S buffer free: SEPP -> the softmax copied S(gs-2) to registers;
-        // else P(gs-2) was written over it, so PV(gs-2) must be done
-        mbar_wait(BAR((SEPP ? B_SEMPTY : B_PFREE) + sb), ((gs >> 1) & 1) ^ 1);
+        // else P(gs-2) was written over it and PV(gs-2) must have read it.
+        // INORDER: PV(gs-2) was ISSUED (previous iteration) before this S MMA,
+        // and tcgen05.mma ops of a thread execute in issue order, so waiting
+        // for its completion is unnecessary.
+        if (SEPP || !INORDER) mbar_wait(BAR((SEPP ? B_SEMPTY : B_PFREE) + sb), ((gs >> 1) & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
