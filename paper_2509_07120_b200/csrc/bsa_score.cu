@@ -768,21 +768,33 @@ __device__ unsigned int search_keys(const unsigned int* keys, int64_t nk, unsign
 // target.  The integers compared are exactly those search_keys compares, so
 // the threshold is identical; it takes at most 4 passes instead of ~10.
 static_assert(SS_THREADS == 256, "one thread per radix bin");
+// Also returns the statistics of the keys strictly above the threshold and
+// equal to it (count and, for MASS, exact fixed-point mass), read off the
+// final digit's histogram -- the callers need no extra pass over the row.
+struct RadixStats {
+  unsigned int above_c, eq_c;
+  unsigned long long above_m, eq_m;
+};
+
 template <bool MASS>
 __device__ unsigned int radix_search(const unsigned int* keys, int64_t nk, unsigned int mn,
-                                     unsigned int mx, double tau, int64_t take) {
+                                     unsigned int mx, double tau, int64_t take,
+                                     RadixStats& st) {
   __shared__ unsigned int hc[256];
   __shared__ unsigned long long hm[256];
   __shared__ unsigned int wc[SS_WARPS];
   __shared__ unsigned long long wm[SS_WARPS];
-  __shared__ unsigned int s_digit, s_above_c;
-  __shared__ unsigned long long s_above_m;
+  __shared__ unsigned int s_digit, s_above_c, s_eq_c;
+  __shared__ unsigned long long s_above_m, s_eq_m;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   // bits above the highest one where mn and mx differ are common to all keys
   int hi = (mn == mx) ? 0 : 32 - __clz(mn ^ mx);  // undecided bits: [0, hi)
   unsigned int prefix = hi >= 32 ? 0u : (mn & (0xFFFFFFFFu << hi));
   unsigned int above_c = 0;
   unsigned long long above_m = 0;
+  // mn == mx: every key equals the threshold
+  unsigned int eq_c = (unsigned int)nk;
+  unsigned long long eq_m = MASS ? (unsigned long long)nk * fx52(mn) : 0ull;
   while (hi > 0) {
     const int width = hi < 8 ? hi : 8;
     const int shift = hi - width;
@@ -844,14 +856,22 @@ __device__ unsigned int radix_search(const unsigned int* keys, int64_t nk, unsig
       s_digit = (unsigned int)bin;
       s_above_c = tot_c - hc[bin];
       s_above_m = MASS ? tot_m - hm[bin] : 0ull;
+      s_eq_c = hc[bin];
+      s_eq_m = MASS ? hm[bin] : 0ull;
     }
     __syncthreads();
     prefix |= s_digit << shift;
     above_c = s_above_c;
     above_m = s_above_m;
+    eq_c = s_eq_c;  // final level (shift 0): keys equal to the threshold
+    eq_m = s_eq_m;
     __syncthreads();
     hi = shift;
   }
+  st.above_c = above_c;
+  st.above_m = above_m;
+  st.eq_c = eq_c;
+  st.eq_m = eq_m;
   return prefix;
 }
 
@@ -861,11 +881,14 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
                                 int64_t k_floor, SelShared& sh, unsigned int* scan_tmp,
                                 uint8_t* __restrict__ bits_row, int32_t* take_out) {
   // 1. validity: all keys non-negative (sign clear), finite, < 2
+  // (with tau > 0 the same pass sums the row's exact fixed-point mass)
   unsigned int mn = 0xffffffffu, mx = 0u;
+  unsigned long long mpart = 0;
   for (int64_t j = threadIdx.x; j < nk; j += SS_THREADS) {
     unsigned int k = keys[j];
     mn = min(mn, k);
     mx = max(mx, k);
+    if (tau > 0.0) mpart += fx52(k);
   }
   block_minmax_u(mn, mx, sh);
   if (mx >= KEY_TWO) return false;  // negative (sign bit), >= 2, inf or nan
@@ -875,22 +898,22 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
   unsigned int vstar = 0;
   int64_t istar = 0;
   bool have_star = false;
+  RadixStats rs{};
   if (tau > 0.0) {
     unsigned long long m_all;
-    unsigned int c_all, e_dummy;
-    mass_at_or_above(keys, nk, mn, sh, m_all, c_all, e_dummy);
+    unsigned int c_dummy, e_dummy;
+    block_sum2(mpart, 0u, 0u, sh, m_all, c_dummy, e_dummy);
     if ((double)m_all * 0x1p-52 < tau) {
       // total mass below tau: every prefix stays below, whole row selected
       if (mn < KEY_TINY || m_all >= (1ull << 53)) return false;
       cdf_len = nk;
     } else {
       // largest key t with mass(keys >= t) >= tau (8-ary search)
-      vstar = radix_search<true>(keys, nk, mn, mx, tau, 0);
+      vstar = radix_search<true>(keys, nk, mn, mx, tau, 0, rs);
       if (vstar < KEY_TINY) return false;
-      unsigned long long m_ge, m_gt;
-      unsigned int c_ge, c_gt, ties, e2;
-      mass_at_or_above(keys, nk, vstar, sh, m_ge, c_ge, ties);
-      mass_at_or_above(keys, nk, vstar + 1, sh, m_gt, c_gt, e2);
+      // statistics of keys > vstar and == vstar, from the search itself
+      const unsigned long long m_gt = rs.above_m, m_ge = rs.above_m + rs.eq_m;
+      const unsigned int c_gt = rs.above_c, ties = rs.eq_c;
       if (m_ge >= (1ull << 53)) return false;
       const unsigned long long vfx = fx52(vstar);
       // smallest i >= 1 with m_gt + i * v >= tau (all partial sums exact)
@@ -923,15 +946,11 @@ __device__ bool select_row_fast(const unsigned int* keys, int64_t nk, double tau
     need = nk;  // everything (ties at 0 included)
   } else if (have_star && take == cdf_len) {
     vt = vstar;
-    unsigned int c_gt, e2;
-    count_at_or_above(keys, nk, vstar + 1, sh, c_gt, e2);
-    need = take - (int64_t)c_gt;
+    need = take - (int64_t)rs.above_c;
   } else {
-    vt = radix_search<false>(keys, nk, mn, mx, 0.0, take);
-    unsigned int c_gt, e2;
-    if (vt == 0xffffffffu) c_gt = 0;
-    else count_at_or_above(keys, nk, vt + 1, sh, c_gt, e2);
-    need = take - (int64_t)c_gt;
+    RadixStats rc{};
+    vt = radix_search<false>(keys, nk, mn, mx, 0.0, take, rc);
+    need = take - (int64_t)rc.above_c;
   }
 
   // 4. bits: key > vt, or key == vt among the first `need` ties by index
