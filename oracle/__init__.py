@@ -18,7 +18,7 @@ Two parts:
 
 Pinning: ``tests/golden/make_golden.py`` ran the reference package
 (/root/reference/pkg/src/bsattn) in the build container and committed its
-outputs under ``tests/golden/``; ``tests/test_oracle_pin.py`` checks this
+outputs under ``tests/golden/``; ``tests/test_cpu_oracle_host.py`` checks this
 oracle against those fixtures on every run.
 """
 

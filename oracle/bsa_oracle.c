@@ -29,7 +29,7 @@
  * The third-party arithmetic (numpy 2.3.5 ufunc loops, scipy-openblas 0.3.30
  * SkylakeX sgemm) is not vendored under /root/reference; this restatement is
  * pinned against the reference's own outputs by tests/golden/make_golden.py
- * (fixtures committed under tests/golden/) and by tests/test_oracle_pin.py.
+ * (fixtures committed under tests/golden/) and by tests/test_cpu_oracle_host.py.
  *
  * Build: see oracle/Makefile (gcc -O2 -ffp-contract=off -pthread).
  */
