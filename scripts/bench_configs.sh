@@ -3,6 +3,7 @@
 # config 5 at 8 GPUs need torchrun on an 8-GPU box: see DESIGN.md.)
 mkdir -p gpurun_out/configs
 B="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e"
+timeout -s KILL 300 python scripts/bench_config1.py > gpurun_out/configs/c1_n8.json 2>&1
 # config 2: N=100 density sweep vs dense (tau = 0: exact density 1 - rho)
 for rho in 0.0 0.5 0.6 0.7 0.75 0.8 0.9; do
   timeout -s KILL 300 $B --frames 100 --rho $rho > gpurun_out/configs/c2_rho$rho.json 2>&1
