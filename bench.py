@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
     ap.add_argument("--shard-chunk", type=int, default=4,
                     help="heads per pipeline chunk of --mode sharded (comm overlaps kernels)")
+    ap.add_argument("--combine", default="allreduce", choices=["allreduce", "scatter"],
+                    help="--mode sharded output combine: NCCL sum all-reduce, or the kernel "
+                         "epilogue storing rows into the owners' buffers over NVLink (CUDA IPC)")
     ap.add_argument("--e2e-chunk", type=int, default=2,
                     help="heads per pipeline chunk of the host-memory e2e leg")
     ap.add_argument("--specials", type=int, default=S_PER_FRAME,
@@ -86,7 +89,9 @@ def workload_config(a, extra=None):
         "parallelism": (f"replicas x{a.gpus} (one independent layer per GPU, no collective)"
                         if a.mode == "replicas" else
                         f"sharded x{a.gpus} (one layer: frame-sharded inputs, NCCL all-gather "
-                        f"of Q/K/V, LPT-sharded rows, sum all-reduce)"),
+                        f"of Q/K/V, LPT-sharded rows, " +
+                        ("sum all-reduce)" if a.combine == "allreduce" else
+                         "epilogue scatter into peer buffers over NVLink)")),
     }
     if extra:
         cfg.update(extra)
@@ -192,6 +197,10 @@ def run_ours(a):
         # second communicator: per-chunk mask gathers / output all-reduces do
         # not queue behind the big Q/K/V gathers
         comm = dist.new_group(backend="nccl") if world > 1 else None
+        target = None
+        if a.combine == "scatter":
+            from paper_2509_07120_b200.shard import ScatterTarget
+            target = ScatterTarget(plan, H, d, rank, None, dev)
     else:
         q_in, k_in, v_in = q, k, v
 
@@ -199,7 +208,8 @@ def run_ours(a):
         if sharded:
             return sharded_sparse_attention(qq, kk, vv, lay, pol, inputs="sharded",
                                             return_mask=True, chunk_heads=a.shard_chunk,
-                                            comm_group=comm)
+                                            comm_group=comm, combine=a.combine,
+                                            scatter_target=target)
         mask = bsa.predict_mask(qq, kk, pol, layout=lay)
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
         return bsa.sparse_attention(job, timing=timing), mask

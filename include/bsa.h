@@ -138,6 +138,37 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
                          int32_t shard, int32_t num_shards, int32_t flags, void* ws,
                          size_t ws_bytes, void* stream);
 
+/* Multi-GPU output scatter (the fused compute + collective of the sharded
+ * path, paper_2509_07120_b200/shard.py).  Instead of writing a local
+ * (H, T, d) output, the attention epilogue writes the row of interleaved
+ * token t to the buffer of the rank that owns t:
+ *     out_ptrs[r] + (h * (token_begin[r+1] - token_begin[r]) + t - token_begin[r]) * d
+ * for token_begin[r] <= t < token_begin[r+1].  out_ptrs are peer pointers
+ * (bsa_ipc_open) so the stores go over NVLink as each tile finishes; no
+ * output all-reduce is needed.  out_ptrs (u64[world]) and token_begin
+ * (i64[world+1]) are DEVICE arrays.  Tensor-core path, bf16 output only.
+ * Replaces the reference's in-process result assembly (sparse.py:186-205). */
+typedef struct {
+  int32_t world;
+  const uint64_t* out_ptrs;
+  const int64_t* token_begin;
+} bsa_scatter;
+int bsa_sparse_attention_scatter(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                                 const bsa_layout* layout, int32_t block_q, int32_t block_k,
+                                 const uint8_t* mask_bits, const int32_t* counts, float scale,
+                                 int32_t shard, int32_t num_shards, int32_t flags,
+                                 const bsa_scatter* scatter, void* ws, size_t ws_bytes,
+                                 void* stream);
+
+/* CUDA IPC for the scatter buffers: allocate a device buffer and export its
+ * handle (BSA_IPC_HANDLE_BYTES opaque bytes); open a peer's handle (enables
+ * peer access); close / free. */
+#define BSA_IPC_HANDLE_BYTES 64
+int bsa_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+int bsa_ipc_open(const void* handle, void** dev_ptr);
+int bsa_ipc_close(void* dev_ptr);
+int bsa_ipc_free(void* dev_ptr);
+
 /* Device time (ms) of the last tensor-core attention kernel launched on this
  * host thread with BSA_FLAG_TIMING set (waits for it); -1 on error. */
 float bsa_last_kernel_ms(void);

@@ -47,6 +47,16 @@ class BsaTensor(ctypes.Structure):
     ]
 
 
+class BsaScatter(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("out_ptrs", ctypes.c_void_p),
+        ("token_begin", ctypes.c_void_p),
+    ]
+
+
+IPC_HANDLE_BYTES = 64
+
 _lib = None
 _lock = threading.Lock()
 
@@ -77,6 +87,12 @@ def _declare(L):
         "bsa_mask_selected_area": ([vp, i64, i64, i32, i32, vp, vp], ctypes.c_int),
         "bsa_mask_to_csr_workspace": ([i64, i64], sz),
         "bsa_mask_to_csr": ([vp, i64, i64, i64, vp, vp, vp, sz, vp], ctypes.c_int),
+        "bsa_sparse_attention_scatter": ([pt, pt, pt, pl, i32, i32, vp, vp, f32, i32, i32, i32,
+                                          ctypes.POINTER(BsaScatter), vp, sz, vp], ctypes.c_int),
+        "bsa_ipc_alloc": ([sz, ctypes.POINTER(vp), vp], ctypes.c_int),
+        "bsa_ipc_open": ([vp, ctypes.POINTER(vp)], ctypes.c_int),
+        "bsa_ipc_close": ([vp], ctypes.c_int),
+        "bsa_ipc_free": ([vp], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -94,7 +110,8 @@ def exported_symbols():
         "bsa_select_workspace", "bsa_select_blocks", "bsa_predict_mask_workspace",
         "bsa_predict_mask", "bsa_sparse_attention_workspace", "bsa_sparse_attention",
         "bsa_sparse_attention_path", "bsa_last_kernel_ms", "bsa_mask_selected_area", "bsa_mask_to_csr_workspace",
-        "bsa_mask_to_csr",
+        "bsa_mask_to_csr", "bsa_sparse_attention_scatter", "bsa_ipc_alloc", "bsa_ipc_open",
+        "bsa_ipc_close", "bsa_ipc_free",
     ]
 
 

@@ -117,6 +117,12 @@ struct TcArgs {
   int32_t* ovf_list;          // [n_items]
   int32_t* ovf_count;         // [1]
   const int32_t* n_items_dev; // exact-max launch: item count on the device (else null)
+  // multi-GPU output scatter (shard.py combine="scatter"): rows of token t
+  // go to out_ptrs[r] for token_begin[r] <= t < token_begin[r+1] (peer
+  // pointers: the epilogue writes over NVLink); scatter_world 0 = local out
+  int32_t scatter_world;
+  const unsigned long long* out_ptrs;
+  const int64_t* token_begin;
 };
 
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);

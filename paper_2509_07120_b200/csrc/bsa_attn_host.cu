@@ -11,6 +11,7 @@
 //   area_kernel      BlockMask.selected_area (maskpred.py:97-101).
 //   csr kernels      CSR view of the mask.
 #include <algorithm>
+#include <cstring>
 #include <cstdlib>
 
 #include "bsa_attn.cuh"
@@ -341,17 +342,18 @@ size_t bsa_sparse_attention_workspace(const bsa_layout* layout, int64_t heads, i
   return tc_ws_layout(nullptr, G).bytes + 256;
 }
 
-int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
-                         void* out, int32_t out_dtype, const bsa_layout* layout,
-                         int32_t block_q, int32_t block_k, const uint8_t* mask_bits,
-                         const int32_t* counts, float scale, int32_t inputs_permuted,
-                         int32_t shard, int32_t num_shards, int32_t flags, void* ws,
-                         size_t ws_bytes, void* stream) {
+static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                                 void* out, int32_t out_dtype, const bsa_layout* layout,
+                                 int32_t block_q, int32_t block_k, const uint8_t* mask_bits,
+                                 const int32_t* counts, float scale, int32_t inputs_permuted,
+                                 int32_t shard, int32_t num_shards, int32_t flags, void* ws,
+                                 size_t ws_bytes, void* stream, const bsa_scatter* scatter) {
   int rc = check_qkv(q, "q");
   if (!rc) rc = check_qkv(k, "k");
   if (!rc) rc = check_qkv(v, "v");
   if (rc) return rc;
-  if (!layout || !out || !mask_bits) return fail(BSA_EINVAL, "sparse_attention: null pointer");
+  if (!layout || (!out && !scatter) || !mask_bits)
+    return fail(BSA_EINVAL, "sparse_attention: null pointer");
   if (q->heads != k->heads || q->heads != v->heads || q->tokens != k->tokens ||
       q->tokens != v->tokens || q->dim != k->dim || q->dim != v->dim)
     return fail(BSA_EINVAL, "q/k/v shapes differ");
@@ -373,6 +375,13 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
     return fail(BSA_EUNSUPPORTED,
                 "tensor-core path needs bf16 inputs, head_dim 64, block_q 128, block_k 64");
   cudaStream_t st = (cudaStream_t)stream;
+  if (scatter) {
+    if (path != BSA_PATH_TC || out_dtype != BSA_BF16 || inputs_permuted)
+      return fail(BSA_EUNSUPPORTED,
+                  "output scatter needs the tensor-core path, bf16 output, source order");
+    if (scatter->world < 1 || scatter->world > 64 || !scatter->out_ptrs || !scatter->token_begin)
+      return fail(BSA_EINVAL, "invalid scatter descriptor");
+  }
   if (path == BSA_PATH_SIMT)
     return launch_simt_attention(q, k, v, out, out_dtype, G, mask_bits, inputs_permuted, scale,
                                  shard, num_shards, st);
@@ -442,6 +451,9 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
   a.ovf_list = W.ovf_list;
   a.ovf_count = W.ovf_count;
   a.n_items_dev = nullptr;
+  a.scatter_world = scatter ? scatter->world : 0;
+  a.out_ptrs = scatter ? reinterpret_cast<const unsigned long long*>(scatter->out_ptrs) : nullptr;
+  a.token_begin = scatter ? scatter->token_begin : nullptr;
   a.trace = nullptr;
   if (getenv("BSA_TC_TRACE")) {  // debug pipeline trace of CTA 0 (scripts/trace_analyze.py)
     static unsigned long long* tbuf = nullptr;
@@ -451,6 +463,57 @@ int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
     a.trace = tbuf;
   }
   return launch_tc_attention(G, a, st);
+}
+
+int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                         void* out, int32_t out_dtype, const bsa_layout* layout,
+                         int32_t block_q, int32_t block_k, const uint8_t* mask_bits,
+                         const int32_t* counts, float scale, int32_t inputs_permuted,
+                         int32_t shard, int32_t num_shards, int32_t flags, void* ws,
+                         size_t ws_bytes, void* stream) {
+  return sparse_attention_impl(q, k, v, out, out_dtype, layout, block_q, block_k, mask_bits,
+                               counts, scale, inputs_permuted, shard, num_shards, flags, ws,
+                               ws_bytes, stream, nullptr);
+}
+
+int bsa_sparse_attention_scatter(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                                 const bsa_layout* layout, int32_t block_q, int32_t block_k,
+                                 const uint8_t* mask_bits, const int32_t* counts, float scale,
+                                 int32_t shard, int32_t num_shards, int32_t flags,
+                                 const bsa_scatter* scatter, void* ws, size_t ws_bytes,
+                                 void* stream) {
+  if (!scatter) return fail(BSA_EINVAL, "sparse_attention_scatter: null scatter descriptor");
+  return sparse_attention_impl(q, k, v, nullptr, BSA_BF16, layout, block_q, block_k, mask_bits,
+                               counts, scale, 0, shard, num_shards, flags, ws, ws_bytes, stream,
+                               scatter);
+}
+
+int bsa_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out || bytes == 0) return fail(BSA_EINVAL, "ipc_alloc: invalid argument");
+  BSA_CUDA_TRY(cudaMalloc(dev_ptr, bytes));
+  cudaIpcMemHandle_t h;
+  BSA_CUDA_TRY(cudaIpcGetMemHandle(&h, *dev_ptr));
+  static_assert(sizeof(cudaIpcMemHandle_t) == BSA_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  return BSA_OK;
+}
+
+int bsa_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(BSA_EINVAL, "ipc_open: invalid argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  BSA_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return BSA_OK;
+}
+
+int bsa_ipc_close(void* dev_ptr) {
+  BSA_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return BSA_OK;
+}
+
+int bsa_ipc_free(void* dev_ptr) {
+  BSA_CUDA_TRY(cudaFree(dev_ptr));
+  return BSA_OK;
 }
 
 int bsa_mask_selected_area(const uint8_t* mask_bits, int64_t heads, int64_t patch_tokens,

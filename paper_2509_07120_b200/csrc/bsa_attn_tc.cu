@@ -958,6 +958,15 @@ __global__ void __maxnreg__(MAX_REGS)
       const bool store = row < I.rows;
       const int32_t pr = I.row0 + row;
       const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
+      // output row: local (H, T, d) buffer, or (multi-GPU scatter) the buffer
+      // of the rank owning token dst, (H, T_r, d), written over NVLink
+      __nv_bfloat16* orow_bf16 = (__nv_bfloat16*)A.out + ((int64_t)I.h * G.T + dst) * D;
+      if (A.scatter_world > 0 && store) {
+        int r = 0;
+        while (r + 1 < A.scatter_world && dst >= A.token_begin[r + 1]) ++r;
+        const int64_t t0 = A.token_begin[r], tr = A.token_begin[r + 1] - t0;
+        orow_bf16 = (__nv_bfloat16*)A.out_ptrs[r] + ((int64_t)I.h * tr + (dst - t0)) * D;
+      }
       const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / ltot;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -968,7 +977,7 @@ __global__ void __maxnreg__(MAX_REGS)
         if (store) {
           const int64_t base = ((int64_t)I.h * G.T + dst) * D + half * 32 + c * 16;
           if (A.out_bf16) {
-            uint4* op = reinterpret_cast<uint4*>((__nv_bfloat16*)A.out + base);
+            uint4* op = reinterpret_cast<uint4*>(orow_bf16 + half * 32 + c * 16);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               uint4 v;

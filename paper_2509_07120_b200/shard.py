@@ -18,8 +18,15 @@ process per GPU:
    bitset rows and counts, which are 18 MB at N=200.
 4. **Attend** this rank's share of the global LPT work list
    (`bsa_sparse_attention(shard, num_shards)`); other rows are left zero.
-5. **Combine** with an all-reduce (sum). Rows are disjoint, so `x + 0 = x`
-   and the sum is exact. Each rank returns the rows of its own frames.
+5. **Combine**, one of two ways:
+   * `combine="scatter"` (opt-in): fused into the kernel. Each rank
+     exports its output buffer over CUDA IPC once. The attention epilogue
+     stores every finished row straight into the owning rank's buffer over
+     NVLink (`bsa_sparse_attention_scatter`), tile by tile, overlapped with
+     the math; a one-element all-reduce then fences the ranks.
+   * `combine="allreduce"`: a sum all-reduce of zero-initialised outputs.
+     Rows are disjoint, so `x + 0 = x` and the sum is exact. Each rank
+     returns the rows of its own frames.
 
 Every row is computed by the same kernel with the same key order as on one
 GPU. The mask and the output are therefore bit-identical to the single-GPU
@@ -134,6 +141,28 @@ class DeviceOps:
                                     ws.data_ptr(), ws.numel(), N.stream_ptr()), "select_blocks")
         return bits, counts
 
+    def attend_scatter(self, q, k, v, layout: TokenLayout, mask: BlockMask, shard: int,
+                       num_shards: int, target: "ScatterTarget", head0: int = 0) -> None:
+        """The fused compute + combine: rows land in the owners' buffers."""
+        from . import _native as N
+        from .dense import AttentionInputs
+
+        g = mask.geometry
+        inp = AttentionInputs(q, k, v)
+        L = N.lib()
+        lay = N.layout_desc(layout)
+        need = L.bsa_sparse_attention_workspace(lay, q.shape[0], q.shape[2], g.block_q,
+                                                g.block_k, N.BSA_BF16, 0, 0)
+        ws = N.workspace(need, q.device)
+        ptrs = target.chunk_ptrs(head0)
+        sc = N.BsaScatter(target.world, ptrs.data_ptr(), target.token_begin.data_ptr())
+        counts = mask.device_counts()
+        N.check(L.bsa_sparse_attention_scatter(
+            N.tensor_desc(inp.q), N.tensor_desc(inp.k), N.tensor_desc(inp.v), lay, g.block_q,
+            g.block_k, mask.device_bits(q.device).data_ptr(), N.ptr(counts),
+            float(np.float32(inp.scale)), int(shard), int(num_shards), 0, sc, ws.data_ptr(),
+            ws.numel(), N.stream_ptr()), "sparse_attention_scatter")
+
     def attend(self, q, k, v, layout: TokenLayout, mask: BlockMask, shard: int,
                num_shards: int) -> torch.Tensor:
         from .dense import AttentionInputs
@@ -142,6 +171,77 @@ class DeviceOps:
         out = torch.zeros(q.shape, dtype=q.dtype, device=q.device)
         job = SparseAttentionJob(AttentionInputs(q, k, v), layout, mask)
         return sparse_attention(job, shard=shard, num_shards=num_shards, out=out)
+
+
+class _DevBuf:
+    """Zero-copy torch view of a raw device allocation (int16 words)."""
+
+    def __init__(self, ptr: int, shape, device):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i2",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+        self.device = device
+
+
+class ScatterTarget:
+    """Per-rank bf16 output buffers of one layer shape, exchanged once over
+    CUDA IPC: every rank holds device pointers to every rank's buffer, so the
+    attention epilogue can store rows directly where they belong."""
+
+    def __init__(self, plan: ShardPlan, heads: int, head_dim: int, rank: int, group=None,
+                 device=None):
+        import ctypes
+
+        from . import _native as N
+
+        self.device = torch.device(device or "cuda")
+        self.world, self.rank, self.heads, self.head_dim = plan.world, rank, heads, head_dim
+        self.rows = [plan.token_range(r)[1] - plan.token_range(r)[0] for r in range(plan.world)]
+        L = N.lib()
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_char * N.IPC_HANDLE_BYTES)()
+        nbytes = heads * self.rows[rank] * head_dim * 2
+        N.check(L.bsa_ipc_alloc(nbytes, ctypes.byref(own), handle), "ipc_alloc")
+        self._own = own.value
+        self._opened = []
+        ptrs = [0] * plan.world
+        ptrs[rank] = self._own
+        if plan.world > 1:
+            handles = [None] * plan.world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            for r in range(plan.world):
+                if r != rank:
+                    p = ctypes.c_void_p()
+                    N.check(L.bsa_ipc_open(handles[r], ctypes.byref(p)), "ipc_open")
+                    ptrs[r] = p.value
+                    self._opened.append(p.value)
+        self.base_ptrs = ptrs
+        tb = [plan.token_range(r)[0] for r in range(plan.world)] + [plan.layout.total_tokens]
+        self.token_begin = torch.tensor(tb, dtype=torch.int64, device=self.device)
+        self._chunk = {}
+        self.local = torch.as_tensor(
+            _DevBuf(self._own, (heads, self.rows[rank], head_dim), self.device),
+            device=self.device).view(torch.bfloat16)
+
+    def chunk_ptrs(self, head0: int) -> torch.Tensor:
+        """Per-rank pointers to head `head0` of each buffer (device u64[world])."""
+        if head0 not in self._chunk:
+            p = [b + head0 * n * self.head_dim * 2 for b, n in zip(self.base_ptrs, self.rows)]
+            self._chunk[head0] = torch.tensor(p, dtype=torch.int64, device=self.device)
+        return self._chunk[head0]
+
+    def close(self, group=None):
+        """Unmap the peers' buffers, then free this rank's. Collective when
+        world > 1: no rank frees its buffer while a peer still maps it."""
+        from . import _native as N
+        L = N.lib()
+        for p in self._opened:
+            L.bsa_ipc_close(p)
+        self._opened = []
+        if self.world > 1 and dist.is_available() and dist.is_initialized():
+            dist.barrier(group=group)
+        if self._own:
+            L.bsa_ipc_free(self._own)
+            self._own = 0
 
 
 def _rank_world(group):
@@ -225,7 +325,8 @@ def _assemble(parts, plan: ShardPlan) -> torch.Tensor:
 
 def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, group=None,
                              inputs: str = "sharded", ops=None, return_mask: bool = False,
-                             chunk_heads: int | None = None, comm_group=None):
+                             chunk_heads: int | None = None, comm_group=None,
+                             combine: str = "allreduce", scatter_target=None):
     """One block-sparse global-attention layer over every rank of `group`.
 
     inputs="sharded":    q/k/v are this rank's frames (ShardPlan.frame_range);
@@ -240,9 +341,21 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
     pass a second communicator so they do not queue behind the big
     gathers). So communication overlaps the previous chunks' kernels.
     Results are bit-identical to the unchunked call.
+
+    combine="scatter" (sharded inputs, DeviceOps): the kernel epilogue writes
+    every output row straight into the owning rank's buffer over NVLink
+    (ScatterTarget; pass a persistent one to reuse the IPC mapping across
+    layers). No output all-reduce is needed. Returns this rank's rows.
+    Reusing a target is safe: a peer's next-layer kernel cannot start before
+    its Q/K/V all-gathers, which this rank only joins after it has copied
+    the previous layer's rows out of the buffer (same stream order).
     """
     if inputs not in ("sharded", "replicated"):
         raise ValueError(f"inputs must be 'sharded' or 'replicated', got {inputs!r}")
+    if combine not in ("allreduce", "scatter"):
+        raise ValueError(f"combine must be 'allreduce' or 'scatter', got {combine!r}")
+    if combine == "scatter" and inputs != "sharded":
+        raise ValueError("combine='scatter' returns this rank's frames: needs inputs='sharded'")
     ops = ops or DeviceOps()
     rank, world = _rank_world(group)
     g = policy.geometry
@@ -261,6 +374,7 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
     spans = [(a, min(H, a + chunk)) for a in range(0, H, chunk)]
     cgroup = comm_group if comm_group is not None else group
 
+    own_target = False
     pending = []
     if inputs == "sharded" and world > 1:
         # every chunk's Q/K/V gathers start now; chunk c's kernels only wait
@@ -278,17 +392,33 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
         else:
             qf, kf, vf = q[a:b], k[a:b], v[a:b]
         mask = sharded_predict_mask(qf, kf, layout, policy, plan, rank, cgroup, ops)
-        out = ops.attend(qf, kf, vf, layout, mask, rank, world)
-        if world > 1:
-            reduces.append(dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup,
-                                           async_op=True))
-        outs.append(out)
+        if combine == "scatter":
+            if scatter_target is None:
+                scatter_target = ScatterTarget(plan, H, q.shape[2], rank, group, q.device)
+                own_target = True
+            ops.attend_scatter(qf, kf, vf, layout, mask, rank, world, scatter_target, head0=a)
+        else:
+            out = ops.attend(qf, kf, vf, layout, mask, rank, world)
+            if world > 1:
+                reduces.append(dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup,
+                                               async_op=True))
+            outs.append(out)
         masks.append(mask)
     for work in reduces:
         work.wait()
-    out = outs[0] if len(outs) == 1 else torch.cat(outs, dim=0)
-    if inputs == "sharded":
-        out = out[:, t0:t1].contiguous()
+    if combine == "scatter":
+        if world > 1:
+            # every rank's kernels (and so its peer stores into our buffer)
+            # are complete once this tiny all-reduce completes
+            dist.all_reduce(torch.zeros(1, device=q.device), group=cgroup)
+        out = scatter_target.local.clone()
+        if own_target:
+            torch.cuda.current_stream().synchronize()
+            scatter_target.close(group)
+    else:
+        out = outs[0] if len(outs) == 1 else torch.cat(outs, dim=0)
+        if inputs == "sharded":
+            out = out[:, t0:t1].contiguous()
     if not return_mask:
         return out
     if len(masks) == 1:

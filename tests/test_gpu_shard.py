@@ -105,3 +105,80 @@ def test_world1_process_group_end_to_end(bsa):
         assert torch.equal(mask2.device_bits(), ref_mask.device_bits())
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_scatter_epilogue_emulated_ranks(bsa, world):
+    """The fused combine: the kernel epilogue stores each row into the buffer
+    of the rank owning its frame (here: `world` buffers on one GPU, reached
+    through the same pointer table the NVLink peers use)."""
+    import torch
+    from paper_2509_07120_b200.shard import DeviceOps, ShardPlan
+
+    lay, q, k, v, pol = _setup(bsa, frames=6, heads=3)
+    ref_mask = bsa.predict_mask(q, k, pol, layout=lay)
+    ref = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, ref_mask))
+    plan = ShardPlan(lay, world)
+    H, T, d = q.shape
+    bufs = [torch.full((H, plan.token_range(r)[1] - plan.token_range(r)[0], d), float("nan"),
+                       dtype=torch.bfloat16, device="cuda") for r in range(world)]
+
+    class Target:  # what ScatterTarget provides, minus the IPC
+        pass
+    t = Target()
+    t.world = world
+    t.token_begin = torch.tensor([plan.token_range(r)[0] for r in range(world)] + [T],
+                                 dtype=torch.int64, device="cuda")
+    t.chunk_ptrs = lambda head0: torch.tensor(
+        [b.data_ptr() + head0 * b.shape[1] * d * 2 for b in bufs], dtype=torch.int64,
+        device="cuda")
+    ops = DeviceOps()
+    # every shard of a 2-way LPT split, and a per-head chunked call
+    for s in range(2):
+        ops.attend_scatter(q, k, v, lay, ref_mask, s, 2, t)
+    torch.cuda.synchronize()
+    for r in range(world):
+        t0, t1 = plan.token_range(r)
+        assert torch.equal(bufs[r], ref[:, t0:t1]), f"rank {r} buffer differs"
+    for b in bufs:
+        b.fill_(float("nan"))
+    for h in range(H):
+        m_h = bsa.BlockMask._from_device(ref_mask.device_bits()[h * ref_mask.geometry.nq_blocks:
+                                                               (h + 1) * ref_mask.geometry.nq_blocks],
+                                         ref_mask.device_counts()[h * ref_mask.geometry.nq_blocks:
+                                                                  (h + 1) * ref_mask.geometry.nq_blocks],
+                                         1, ref_mask.geometry)
+        ops.attend_scatter(q[h:h + 1], k[h:h + 1], v[h:h + 1], lay, m_h, 0, 1, t, head0=h)
+    torch.cuda.synchronize()
+    for r in range(world):
+        t0, t1 = plan.token_range(r)
+        assert torch.equal(bufs[r], ref[:, t0:t1])
+
+
+def test_world1_scatter_combine(bsa):
+    import torch
+    import torch.distributed as dist
+    from paper_2509_07120_b200.shard import ScatterTarget, ShardPlan, sharded_sparse_attention
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        lay, q, k, v, pol = _setup(bsa)
+        ref_mask = bsa.predict_mask(q, k, pol, layout=lay)
+        ref = bsa.sparse_attention(
+            bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, ref_mask))
+        out = sharded_sparse_attention(q, k, v, lay, pol, combine="scatter")
+        assert torch.equal(out, ref)
+        tgt = ScatterTarget(ShardPlan(lay, 1), q.shape[0], q.shape[2], 0)
+        for _ in range(2):  # persistent target reused across layers, chunked
+            out2 = sharded_sparse_attention(q, k, v, lay, pol, combine="scatter",
+                                            scatter_target=tgt, chunk_heads=1)
+            assert torch.equal(out2, ref)
+        tgt.close()
+        with pytest.raises(ValueError):
+            sharded_sparse_attention(q, k, v, lay, pol, combine="scatter", inputs="replicated")
+    finally:
+        dist.destroy_process_group()
