@@ -5,35 +5,35 @@
 // online softmax, sparse.py:89-131) for bf16 inputs, head_dim 64, block_q
 // 128, block_k 64.
 //
-// Persistent, warp-specialised, TWO CTAs per SM, 320 threads (10 warps) each:
-//   warp 8      producer: pops LPT-ordered work items (atomic counter) and
-//               TMA-loads, per 64-key tile, the K and V chunk of the next
-//               selected block (the gather is done by TMA coordinates) into
-//               separate SW128 shared-memory rings (K runs VLAG tiles ahead).
-//   warp 9      MMA issuer (warp-uniform loop, elect.sync issues):
-//               S = Q K^T with Q read from TMEM (tcgen05.mma .ts, kind::f16,
-//               M=128 N=64, fp32, two S buffers) and O += P [V | 1] with P
-//               read from TMEM and V from shared memory (N=80: an all-ones
-//               block beside each V stage makes O[:,64] the row sum of P);
-//               tcgen05.commit -> mbarriers.  S(j+1) is in flight while the
-//               softmax warps work on tile j.
-//   warps 0-7   softmax + epilogue.  Warp w (w<4) and warp w+4 own TMEM lanes
-//               32w..32w+31.  Stale-max launch: the two warp groups take
-//               alternate key tiles (S buffer 0 / 1), full rows, in 32-column
-//               halves; four softmax warps per SM sub-partition keep the
-//               MUFU and FMA pipes busy.  Exact launch: the groups split
-//               every tile into key halves 0-31 / 32-63 instead.
+// Persistent, warp-specialised.  Stale-max launch: ONE CTA per SM, 640
+// threads (20 warps), all 512 TMEM columns:
+//   warps 16/17 K and V producers: walk the item's key tiles (contiguous
+//               strip, then the selected blocks, generated warp-parallel from
+//               the mask bits) and TMA-load each 64-key K / V chunk (the gather
+//               is done by TMA coordinates) into SW128 shared-memory rings.
+//   warp 18     S issuer: S = Q K^T with Q read from TMEM (tcgen05.mma .ts,
+//               kind::f16, M=128 N=64, fp32) into S buffer j % 6.
+//   warp 19     PV issuer: O += P [V | 1] with P read from TMEM and V from
+//               shared memory (N=80: an all-ones block beside each V stage
+//               makes O[:,64] the row sum of P).  Both issuers are
+//               warp-uniform loops with elect.sync issue and tcgen05.commit
+//               -> mbarriers.
+//   warps 0-15  softmax + epilogue, four groups of four warps; warp w owns
+//               TMEM lanes 32(w%4)..+31.  Group j % 4 takes key tile j, whole
+//               rows, in 32-column halves.  Four softmax warps per SM
+//               sub-partition keep the MUFU and FMA pipes busy.
 // exp2: 5 of every 8 pairs on MUFU (ex2.approx), 3 on the FMA pipe as a
 // degree-2 minimax polynomial (rel err 1.7e-3 < bf16 rounding of P).
-// Softmax offset ("stale max"): the row max of the item's first tile (the two
-// groups exchange it once through shared memory) is kept for the whole item;
-// online softmax does not depend on the offset, only overflow does.  An item
-// whose tensor-core row sum l ends non-finite or above 2^100 (scores grew by
-// ~100 log2 units beyond the first tile's max -- never for attention logits
-// of sane scale) is listed and recomputed by a second, exact-max launch of
-// the same kernel (per-tile max exchanged between the halves, lazy 2^8
+// Softmax offset ("stale max"): the row max of the item's first tile (shared
+// once through shared memory) is kept for the whole item; online softmax does
+// not depend on the offset, only overflow does.  An item whose tensor-core
+// row sum l ends non-finite or above 2^100 (scores grew by ~100 log2 units
+// beyond the first tile's max -- never for attention logits of sane scale)
+// is listed and recomputed by a second, exact-max launch of the same kernel
+// (two CTAs per SM, 10 warps each, two groups splitting every tile into key
+// halves 0-31 / 32-63, per-tile max exchanged between the halves, lazy 2^8
 // rescaling of O, l summed in registers).
-// TMEM (256 of 512 columns per CTA): S0|S1 (2x64, P over S) O (80) Q (32).
+// TMEM (stale max, 512 columns): S0..S5 (6x64, P over S) | O (80) | Q (32).
 #include <cuda.h>
 
 #include <cstdio>
@@ -47,94 +47,92 @@ namespace tc {
 #ifndef BSA_TC_EXPERIMENT
 #define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
 #endif
-#ifndef BSA_TC_TILESPLIT
-#define BSA_TC_TILESPLIT 1
+#ifndef BSA_TC_WIDE
+#define BSA_TC_WIDE 1
 #endif
-// stale-max launch: the two warp groups (warps 0-3, 4-7) take alternate key
-// tiles (S buffer 0 / 1) of every row, full 64 columns each, instead of the
-// two column halves of every tile -- their phases interleave on the MUFU and
-// the per-tile overhead is paid half as often.
-constexpr bool TILE_SPLIT = BSA_TC_TILESPLIT != 0;
-#ifndef BSA_TC_SEPP
-#define BSA_TC_SEPP 0
+#ifndef BSA_TC_NB
+#define BSA_TC_NB 6
 #endif
-// SEPP: P gets its own TMEM buffers instead of overwriting its S tile, so
-// S(j+2) can be computed as soon as the softmax has copied S(j) to
-// registers (not only after PV(j) has read P(j)).  The TMEM this costs
-// moves Q back to shared memory (S = Q K^T as an .ss MMA) and drops LSUM.
-constexpr bool SEPP = BSA_TC_SEPP != 0;
-#ifndef BSA_TC_INORDER
-#define BSA_TC_INORDER 0
-#endif
-constexpr bool INORDER = BSA_TC_INORDER != 0;
-constexpr bool QT = !SEPP;  // Q tile in TMEM (.ts S MMA), else TMA'd to smem
-#ifndef BSA_TC_LSUM
-#define BSA_TC_LSUM (BSA_TC_SEPP ? 0 : 1)
-#endif
-// LSUM: the PV MMA runs with N = 80: columns 64-79 of its B operand are an
-// all-ones block kept beside every V stage (at the descriptor's LBO), so
-// O[:, 64] accumulates the row sum of P in fp32 and the softmax threads do
-// no additions.  Costs 25% more PV MMA work and 8 KB of smem per V stage.
-constexpr bool LSUM = BSA_TC_LSUM != 0;
-#ifndef BSA_TC_NK
-#define BSA_TC_NK (BSA_TC_SEPP ? 6 : BSA_TC_LSUM ? 5 : 7)
-#endif
-#ifndef BSA_TC_NV
-#define BSA_TC_NV (BSA_TC_SEPP ? 5 : BSA_TC_LSUM ? 4 : 6)
-#endif
-#ifndef BSA_TC_VLAG
-#define BSA_TC_VLAG 2
+#ifndef BSA_TC_NG
+#define BSA_TC_NG 4
 #endif
 constexpr int BQ = 128, CH = 64, D = 64;
-constexpr int NK = BSA_TC_NK, NV = BSA_TC_NV, VLAG = BSA_TC_VLAG;
 constexpr int CHUNK_BYTES = CH * D * 2;  // 8 KB (one K or V tile)
-constexpr int SM_WARPS = 8;              // softmax warps (two per TMEM lane quarter)
-constexpr int PRODUCER_WARP = 8, MMA_WARP = 9;
-constexpr int NUM_THREADS = 320;
-constexpr int CTAS_PER_SM = 2;
-// registers per thread: two CTAs x 320 threads share 64K (8-register granules)
-constexpr int MAX_REGS = (65536 / (CTAS_PER_SM * NUM_THREADS)) / 8 * 8;
-constexpr int Q_BYTES = BQ * D * 2;     // 16 KB (SEPP: Q tile in smem)
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = QT ? 0 : Q_BYTES;
-constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
-constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ its ones block)
-constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // half-row exchange: 3 x 2 x 128 floats
-constexpr int OFF_BAR = OFF_XCH + 3 * 2 * BQ * 4;
-constexpr int SMEM_BYTES = OFF_BAR + 512 + 1024;    // barriers/ring + alignment slack
-static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
-constexpr uint32_t TMEM_COLS = 256;
-// O: 64 columns (+16 row-sum columns with LSUM)
-// SEPP: S0|S1 (2x64) P0|P1 (2x32) O (64); else S0|S1 (P over S) O (64|80) Q (32)
-constexpr uint32_t TM_S = 0, TM_P = 128, TM_O = SEPP ? 192 : 128, TM_Q = LSUM ? 224 : 192,
-                   O_COLS = LSUM ? 80 : 64;
-static_assert(!(SEPP && LSUM), "SEPP leaves no TMEM for the row-sum columns");
-// TMEM column of the 16 packed-P columns that key half hh (32 keys) of
-// S buffer sb writes: its own P buffer (SEPP) or over its S columns
-__device__ __forceinline__ uint32_t p_col16(uint32_t sb, int hh, bool column_split) {
-  if constexpr (SEPP) return TM_P + sb * 32 + hh * 16;
-  return TM_S + sb * 64 + (column_split ? hh * 32 : hh * 16);
-}
+// O: 64 columns + 16 row-sum columns.  The PV MMA runs with N = 80: columns
+// 64-79 of its B operand are an all-ones block kept beside every V stage (at
+// the descriptor's LBO), so O[:, 64] accumulates the row sum of P in fp32
+// and the stale-max softmax does no additions.
+#ifndef BSA_TC_LSUM
+#define BSA_TC_LSUM 1
+#endif
+constexpr bool LSUM = BSA_TC_LSUM != 0;  // else the softmax sums P rows in registers
+constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 
-// barrier slots (8 bytes each) inside the barrier region
-enum {
-  B_QFULL = 0,              // [1]  Q row halves in TMEM (8 softmax warps)
-  B_KFULL = 1,              // [NK]
-  B_KEMPTY = B_KFULL + NK,  // [NK]
-  B_VFULL = B_KEMPTY + NK,  // [NV]
-  B_VEMPTY = B_VFULL + NV,  // [NV]
-  B_SFULL = B_VEMPTY + NV,  // [2]
-  B_PFULL = B_SFULL + 2,    // [2]  8 softmax warps
-  B_PFREE = B_PFULL + 2,    // [2]  PV done: P/S buffer reusable
-  B_OFULL = B_PFREE + 2,    // [1]
-  B_OEMPTY = B_OFULL + 1,   // [1]
-  B_IFULL = B_OEMPTY + 1,   // [2]
-  B_IEMPTY = B_IFULL + 2,   // [2]  8 softmax warps + MMA warp
-  B_QEMPTY = B_IEMPTY + 2,  // [1]  (SEPP) Q smem tile free
-  B_SEMPTY = B_QEMPTY + 1,  // [2]  (SEPP) S tile copied to registers
-  B_COUNT = B_SEMPTY + 2
+// Launch shapes.  WIDE (the stale-max launch): ONE CTA per SM owning all 512
+// TMEM columns, four softmax warp groups and NB = 6 S/P buffers; tile j goes
+// to group j % 4 and buffer j % NB.  S(j) only waits for PV(j - NB), so a
+// group does not wait on the P(j) -> PV(j) -> S(j+2) chain that two buffers
+// per CTA imposed.  One SM's worth of tiles is too much for one producer and
+// one MMA warp sharing the sub-partitions with 16 softmax warps (~900 clk of
+// waits and issues per tile, measured), so K and V each get a producer warp
+// and S and PV each get an issuer warp (SPLIT).
+// Narrow (the exact-max repair launch): two CTAs per SM, 256 columns each,
+// two groups splitting every tile into column halves, two buffers, one
+// producer and one MMA warp.
+template <bool WIDE>
+struct Cfg {
+  static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warp groups (4 warps: the 4 lane quarters)
+  static constexpr int NB = WIDE ? BSA_TC_NB : 2;  // S buffers (64 columns, P over S)
+  static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
+  static constexpr int SM_WARPS = 4 * NG;
+  // SPLIT: S MMAs and PV MMAs come from two issuer warps (one warp issuing
+  // both for a whole SM cannot keep up: ~900 clk of waits and issues per tile)
+  static constexpr bool SPLIT = WIDE;
+  // SPLIT also gives K and V their own producer warps
+  static constexpr int PRODUCER_WARP = SM_WARPS, VPROD_WARP = SPLIT ? SM_WARPS + 1 : SM_WARPS,
+                       MMA_WARP = VPROD_WARP + 1, PV_WARP = SPLIT ? MMA_WARP + 1 : MMA_WARP;
+  static constexpr int NUM_THREADS = 32 * (PV_WARP + 1);
+  // warps other than the K producer that consume the item ring
+  static constexpr int RING_CONSUMERS = SM_WARPS + (SPLIT ? 3 : 1);
+  static constexpr int QUEUE = 256;  // (SPLIT) per-producer queue of key-tile starts
+  static constexpr int CTAS_PER_SM = WIDE ? 1 : 2;
+  // registers per thread: each SM sub-partition has 16K registers and holds
+  // every 4th warp of the SM's CTAs (8-register granules)
+  static constexpr int WARPS_PER_SMSP = (CTAS_PER_SM * NUM_THREADS / 32 + 3) / 4;
+  static constexpr int MAX_REGS = (16384 / (32 * WARPS_PER_SMSP)) / 8 * 8;
+  static constexpr int NK = WIDE ? 8 : 5, NV = WIDE ? (LSUM ? 6 : 10) : 4;
+  static constexpr int VLAG = 2;  // (one producer warp) K(j) is loaded VLAG tiles before V(j)
+  static constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ ones block)
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
+  static constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // [3][NG][128] floats
+  static constexpr int OFF_QUEUE = OFF_XCH + 3 * NG * BQ * 4;  // (SPLIT) [2][QUEUE] int32
+  static constexpr int OFF_BAR = OFF_QUEUE + (SPLIT ? 2 * QUEUE * 4 : 0);
+  static constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
+  static constexpr uint32_t TMEM_COLS = WIDE ? 512 : 256;
+  // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last)
+  static constexpr uint32_t TM_S = 0, TM_O = NB * 64, TM_Q = TMEM_COLS - 32;
+  // barrier slots (8 bytes each) inside the barrier region
+  static constexpr int B_QFULL = 0;              // [1]  Q in TMEM (all softmax warps)
+  static constexpr int B_KFULL = 1;              // [NK]
+  static constexpr int B_KEMPTY = B_KFULL + NK;  // [NK]
+  static constexpr int B_VFULL = B_KEMPTY + NK;  // [NV]
+  static constexpr int B_VEMPTY = B_VFULL + NV;  // [NV]
+  static constexpr int B_SFULL = B_VEMPTY + NV;  // [NB]
+  static constexpr int B_PFULL = B_SFULL + NB;   // [NB] the warps of the tile
+  static constexpr int B_PFREE = B_PFULL + NB;   // [NB] PV done: S/P buffer reusable
+  static constexpr int B_OFULL = B_PFREE + NB;   // [1]
+  static constexpr int B_OEMPTY = B_OFULL + 1;   // [1]
+  static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
+  static constexpr int B_IEMPTY = B_IFULL + 2;   // [2]  softmax warps + MMA warp(s)
+  static constexpr int B_COUNT = B_IEMPTY + 2;
+  static_assert(B_COUNT * 8 + 32 <= 1024, "barrier region");
+  static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
+  static_assert(TM_O + O_COLS <= TM_Q, "TMEM columns");
+  static_assert(LEAD >= 1 && LEAD < NB, "S(j+LEAD) must only wait for a PV issued earlier");
 };
-static_assert(B_COUNT * 8 + 32 <= 512, "barrier region");
+using CfgMain = Cfg<BSA_TC_WIDE != 0>;
+using CfgExact = Cfg<false>;
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -177,6 +175,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 #endif
+}
+// two phase waits at once (both try_waits in flight before one branch): for
+// issuer warps whose barriers are usually complete already
+__device__ __forceinline__ void mbar_wait2(uint32_t a, uint32_t pa, uint32_t b, uint32_t pb) {
+  asm volatile(
+      "{\n\t.reg .pred P1, P2;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P2, [%2], %3;\n\t"
+      "and.pred P1, P1, P2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(pa), "r"(b), "r"(pb)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -254,6 +265,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
       "r"(r[15])
       : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -342,9 +358,6 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int b_mn_major, i
 // The argument is formed in fp32 with f32x2 FMAs.  POLY of every 8 pairs use
 // the FMA-pipe polynomial, the rest MUFU.EX2; F16P selects fp16 P (for fp16
 // V) instead of bf16 P.
-#ifndef BSA_TC_LD32
-#define BSA_TC_LD32 0
-#endif
 #ifndef BSA_TC_POLY_SPREAD
 #define BSA_TC_POLY_SPREAD 0
 #endif
@@ -394,10 +407,6 @@ __device__ __forceinline__ float max32(const float (&s)[32]) {
   return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
 }
 
-// named barrier between the two warps that share a TMEM lane quarter
-__device__ __forceinline__ void pair_sync(int quarter) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-}
 
 // ---------------------------------------------------------------------------
 // work item decoding
@@ -475,61 +484,68 @@ constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
 // the items the stale-max launch listed.
 // ---------------------------------------------------------------------------
 template <int POLY, bool F16P, bool EXACT>
-__global__ void __maxnreg__(MAX_REGS)
+__global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
+  using C = Cfg<BSA_TC_WIDE != 0 && !EXACT>;
+  constexpr int NG = C::NG, NB = C::NB, NK = C::NK, NV = C::NV, VLAG = C::VLAG;
+  constexpr int SM_WARPS = C::SM_WARPS;
+  // warps that write one tile's P: one group (stale max, whole tiles), or
+  // both groups (exact max, column halves of every tile)
+  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4;
+  static_assert(!EXACT || NG == 2, "the exact launch splits tiles into two column halves");
+  (void)tm_q;  // Q goes to TMEM from the softmax warps' registers
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = sbase + OFF_BAR;
+  const uint32_t bar0 = sbase + C::OFF_BAR;
   auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
-  volatile int32_t* item_ring = (volatile int32_t*)(smem + OFF_BAR + 8 * B_COUNT);
-  uint32_t* tmem_holder = (uint32_t*)(smem + OFF_BAR + 8 * B_COUNT + 16);
-  float* xch = (float*)(smem + OFF_XCH);  // [3][2][128]: first-tile max, tile max, l
+  volatile int32_t* item_ring = (volatile int32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT);
+  uint32_t* tmem_holder = (uint32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT + 16);
+  float* xch = (float*)(smem + C::OFF_XCH);  // [3][NG][128]: first-tile max, tile max, l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    mbar_init(BAR(B_QFULL), QT ? SM_WARPS : 1);
-    mbar_init(BAR(B_QEMPTY), 1);
+    mbar_init(BAR(C::B_QFULL), SM_WARPS);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(BAR(C::B_SFULL + i), 1);
+      mbar_init(BAR(C::B_PFULL + i), TILE_WARPS);
+      mbar_init(BAR(C::B_PFREE + i), 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(BAR(B_SFULL + i), 1);
-      mbar_init(BAR(B_PFULL + i), (TILE_SPLIT && !EXACT) ? SM_WARPS / 2 : SM_WARPS);
-      mbar_init(BAR(B_SEMPTY + i), (TILE_SPLIT && !EXACT) ? SM_WARPS / 2 : SM_WARPS);
-      mbar_init(BAR(B_PFREE + i), 1);
-      mbar_init(BAR(B_IFULL + i), 1);
-      mbar_init(BAR(B_IEMPTY + i), SM_WARPS + 1);
+      mbar_init(BAR(C::B_IFULL + i), 1);
+      mbar_init(BAR(C::B_IEMPTY + i), C::RING_CONSUMERS);
     }
     for (int s = 0; s < NK; ++s) {
-      mbar_init(BAR(B_KFULL + s), 1);
-      mbar_init(BAR(B_KEMPTY + s), 1);
+      mbar_init(BAR(C::B_KFULL + s), 1);
+      mbar_init(BAR(C::B_KEMPTY + s), 1);
     }
     for (int s = 0; s < NV; ++s) {
-      mbar_init(BAR(B_VFULL + s), 1);
-      mbar_init(BAR(B_VEMPTY + s), 1);
+      mbar_init(BAR(C::B_VFULL + s), 1);
+      mbar_init(BAR(C::B_VEMPTY + s), 1);
     }
-    mbar_init(BAR(B_OFULL), 1);
-    mbar_init(BAR(B_OEMPTY), SM_WARPS);
+    mbar_init(BAR(C::B_OFULL), 1);
+    mbar_init(BAR(C::B_OEMPTY), SM_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (LSUM) {
     // the all-ones half of every V stage: B columns 64-79 of the PV MMA (any
     // swizzle permutation of ones is ones)
     const uint32_t one2 = F16P ? 0x3C003C00u : 0x3F803F80u;
-    for (int i = threadIdx.x; i < NV * CHUNK_BYTES / 4; i += NUM_THREADS) {
+    for (int i = threadIdx.x; i < NV * CHUNK_BYTES / 4; i += C::NUM_THREADS) {
       const int st = i / (CHUNK_BYTES / 4), w = i % (CHUNK_BYTES / 4);
-      reinterpret_cast<uint32_t*>(smem + OFF_V + st * V_STAGE + CHUNK_BYTES)[w] = one2;
+      reinterpret_cast<uint32_t*>(smem + C::OFF_V + st * C::V_STAGE + CHUNK_BYTES)[w] = one2;
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == MMA_WARP) {
+  if (warp == C::MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)), "n"(TMEM_COLS)
+                     smem_u32(tmem_holder)), "n"(C::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (warp == PRODUCER_WARP && lane == 0) {
-    if (!QT) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_q) : "memory");
+  if (warp == C::PRODUCER_WARP && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
   }
@@ -543,7 +559,108 @@ __global__ void __maxnreg__(MAX_REGS)
   else n_work = A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards
                                  : A.n_items;
 
-  if (warp == PRODUCER_WARP) {
+  if (C::SPLIT && (warp == C::PRODUCER_WARP || warp == C::VPROD_WARP)) {
+    // ======================= K / V producers (SPLIT; one elected lane issues) ===
+    // Each warp walks the item's key tiles itself: the contiguous strip, then
+    // the selected blocks in ascending order, generated warp-parallel (32
+    // mask bytes per step: popc + warp scan) into a shared-memory queue, so
+    // the per-tile cost is one queue read, one barrier wait and one TMA.
+    const bool is_k = warp == C::PRODUCER_WARP;
+    int32_t* queue = reinterpret_cast<int32_t*>(smem + C::OFF_QUEUE) + (is_k ? 0 : C::QUEUE);
+    uint32_t it = 0, gx = 0;
+    while (true) {
+      const uint32_t slot = it & 1;
+      int32_t code;
+      if (is_k) {
+        int64_t w = 0;
+        if (lane == 0) w = atomicAdd(A.work_counter, 1);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        code = -1;
+        if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
+        mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
+        if (elect_one()) {
+          item_ring[slot] = code;
+          mbar_arrive(BAR(C::B_IFULL + slot));
+        }
+        __syncwarp();
+      } else {
+        mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
+        code = item_ring[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
+      }
+      if (code < 0) break;
+      const Item I = decode(G, code, A.counts, A.bits);
+      const uint8_t* mrow =
+          I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
+      const int64_t nbytes = I.qb >= 0 ? G.mask_row_bytes : 0;
+      int64_t pos = 0, bp = 0;
+      const int64_t end = I.qb < 0 ? G.T : G.Ts;
+      int qh = 0, qt = 0;
+      for (int j = 0; j < I.nchunks; ++j) {
+        if (qh == qt) {
+          qh = 0;
+          qt = 0;
+          if (pos < end) {
+            const int64_t left = (end - pos + CH - 1) / CH;
+            const int n = (int)(left < C::QUEUE ? left : C::QUEUE);
+            for (int e = lane; e < n; e += 32) queue[e] = (int32_t)(pos + (int64_t)e * CH);
+            pos += (int64_t)n * CH;
+            qt = n;
+          } else {
+            while (qt == 0 && bp < nbytes) {
+              const int64_t b = bp + lane;
+              uint32_t byte = b < nbytes ? mrow[b] : 0u;
+              const int c = __popc(byte);
+              int incl = c;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+              }
+              int k = incl - c;
+              while (byte) {
+                const int bit = __ffs(byte) - 1;
+                byte &= byte - 1;
+                queue[k++] = (int32_t)(G.Ts + (b * 8 + bit) * CH);
+              }
+              qt = __shfl_sync(0xffffffffu, incl, 31);
+              bp += 32;
+            }
+            if (qt == 0) {  // mask and counts disagree: keep the pipeline moving
+              queue[0] = (int32_t)G.Ts;
+              qt = 1;
+            }
+          }
+          __syncwarp();
+        }
+        const int32_t s0 = queue[qh++];
+        if (is_k) {
+          const uint32_t st = gx % NK;
+          if (lane == 0) BSA_TR(9, gx);
+          mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(BAR(C::B_KFULL + st), CHUNK_BYTES);
+            tma_load_3d(sbase + C::OFF_K + st * CHUNK_BYTES, &tm_k, BAR(C::B_KFULL + st), 0, s0,
+                        I.h);
+            BSA_TR(0, gx);
+          }
+        } else {
+          const uint32_t st = gx % NV;
+          mbar_wait(BAR(C::B_VEMPTY + st), ((gx / NV) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(BAR(C::B_VFULL + st), CHUNK_BYTES);
+            tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0,
+                        I.h);
+            BSA_TR(6, gx);
+          }
+        }
+        __syncwarp();
+        ++gx;
+      }
+      ++it;
+    }
+  } else if (warp == C::PRODUCER_WARP) {
     // ======================= producer (whole warp; one elected lane issues) =====
     // K(j) is issued VLAG tiles before V(j): a K tile is released as soon as
     // its S MMA completes, a V tile only after its PV MMA.
@@ -557,32 +674,24 @@ __global__ void __maxnreg__(MAX_REGS)
       if (w < n_work)
         code = A.items[(!EXACT && A.num_shards > 1) ? w * A.num_shards + A.shard : w];
       const uint32_t slot = it & 1;
-      mbar_wait(BAR(B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
+      mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
       if (elect_one()) {
         item_ring[slot] = code;
-        mbar_arrive(BAR(B_IFULL + slot));
+        mbar_arrive(BAR(C::B_IFULL + slot));
       }
       __syncwarp();
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
-      if constexpr (!QT) {
-        // Q tile -> smem once the previous item's last S MMA has read it
-        mbar_wait(BAR(B_QEMPTY), (it & 1) ^ 1);
-        if (elect_one()) {
-          mbar_expect_tx(BAR(B_QFULL), Q_BYTES);
-          tma_load_3d(sbase + OFF_Q, &tm_q, BAR(B_QFULL), 0, I.row0, I.h);
-        }
-        __syncwarp();
-      }
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
       KeyChunker ck(G, I.qb, mrow, CH);
       auto load_v = [&](int32_t s0) {
         const uint32_t st = gv % NV;
-        mbar_wait(BAR(B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
+        mbar_wait(BAR(C::B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
+        if (lane == 0) BSA_TR(6, gv);
         if (elect_one()) {
-          mbar_expect_tx(BAR(B_VFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_V + st * V_STAGE, &tm_v, BAR(B_VFULL + st), 0, s0, I.h);
+          mbar_expect_tx(BAR(C::B_VFULL + st), CHUNK_BYTES);
+          tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0, I.h);
         }
         __syncwarp();
         ++gv;
@@ -592,10 +701,12 @@ __global__ void __maxnreg__(MAX_REGS)
         int64_t s0;
         int l0;
         ck.next(s0, l0);
-        mbar_wait(BAR(B_KEMPTY + st), ((gk / NK) & 1) ^ 1);
+        if (lane == 0) BSA_TR(9, gk);
+        mbar_wait(BAR(C::B_KEMPTY + st), ((gk / NK) & 1) ^ 1);
         if (elect_one()) {
-          mbar_expect_tx(BAR(B_KFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + OFF_K + st * CHUNK_BYTES, &tm_k, BAR(B_KFULL + st), 0, (int)s0, I.h);
+          mbar_expect_tx(BAR(C::B_KFULL + st), CHUNK_BYTES);
+          tma_load_3d(sbase + C::OFF_K + st * CHUNK_BYTES, &tm_k, BAR(C::B_KFULL + st), 0, (int)s0,
+                      I.h);
           BSA_TR(0, gk);
         }
         __syncwarp();
@@ -610,157 +721,183 @@ __global__ void __maxnreg__(MAX_REGS)
         if (q < I.nchunks) load_v(vq[q]);
       ++it;
     }
-  } else if (warp == MMA_WARP) {
-    // ======================= MMA issuer (whole warp; one elected lane issues) ===
+  } else if (warp == C::MMA_WARP || warp == C::PV_WARP) {
+    // ======================= MMA issuers (whole warp; one elected lane issues) ==
     // Descriptors are built once; per tile only the stage offset (address >> 4,
     // no carry out of the 14-bit field: smem < 256 KB) is added.  S(j) goes
-    // into buffer j&1 once PV(j-2), which read P from it, has completed; PV(j)
-    // trails S(j+1).
+    // into buffer j % NB once PV(j - NB), which read P from it, has completed.
+    // SPLIT: warp MMA_WARP issues every S, warp PV_WARP every PV; else one
+    // warp issues S(j + LEAD) before PV(j).
+    const bool do_s = warp == C::MMA_WARP, do_pv = warp == C::PV_WARP;
     uint32_t it = 0, gs = 0, gp = 0;
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
-    const uint64_t dq = sdesc(sbase + OFF_Q, 16, 1024);  // (SEPP) Q in smem
-    const uint64_t dk0 = sdesc(sbase + OFF_K, 16, 1024);
-    const uint64_t dv0 = sdesc(sbase + OFF_V, 8192, 1024);
-    // SEPP: S(j) only needs the softmax to have copied S(j-2), so PV trails
-    // S by two tiles and the next S tile is always ready in time
-    constexpr int PV_LAG = SEPP ? 2 : 1;
+    const uint64_t dk0 = sdesc(sbase + C::OFF_K, 16, 1024);
+    const uint64_t dv0 = sdesc(sbase + C::OFF_V, 8192, 1024);
     while (true) {
       const uint32_t slot = it & 1;
-      mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
+      mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
       const int32_t code = item_ring[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(BAR(B_IEMPTY + slot));
+      if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
-      mbar_wait(BAR(B_QFULL), it & 1);
-      tc_fence_after();
-      auto issue_pv = [&](int jj) {
-        const uint32_t sv = gp % NV, pb = gp & 1;
-        mbar_wait(BAR(B_PFULL + pb), (gp >> 1) & 1);
-        mbar_wait(BAR(B_VFULL + sv), (gp / NV) & 1);
-        if (jj == 0) mbar_wait(BAR(B_OEMPTY), (it & 1) ^ 1);
+      if (do_s) {
+        mbar_wait(BAR(C::B_QFULL), it & 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint64_t dv = dv0 + (uint64_t)((sv * V_STAGE) >> 4);
-          // keys 16k..16k+15.  Tile split: P packed contiguously over S columns
-          // 0-31; column split: half k>>1 wrote its P over S columns 32*(k>>1)
-#pragma unroll
-          for (int k = 0; k < CH / 16; ++k)
-            if (BSA_TC_EXPERIMENT != 2)
-              mma_ts(tmem + TM_O,
-                     tmem + (SEPP ? TM_P + pb * 32 + k * 8
-                                  : TM_S + pb * 64 +
-                                        ((TILE_SPLIT && !EXACT) ? k * 8
-                                                                : (k >> 1) * 32 + (k & 1) * 8)),
-                     dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
-          tc_commit(BAR(B_PFREE + pb));
-          tc_commit(BAR(B_VEMPTY + sv));
-          BSA_TR(2, gp);
-        }
-        __syncwarp();
-        ++gp;
-      };
-      for (int j = 0; j < ntiles; ++j) {
-        const uint32_t sk = gs % NK, sb = gs & 1;
-        mbar_wait(BAR(B_KFULL + sk), (gs / NK) & 1);
+      }
+      auto issue_s = [&]() {
+        const uint32_t sk = gs % NK, sb = gs % NB;
+        if (lane == 0) BSA_TR(11, gs);
+#ifdef BSA_TC_TRACE_BUILD
+        mbar_wait(BAR(C::B_KFULL + sk), (gs / NK) & 1);
         if (lane == 0) BSA_TR(3, gs);
-        // S buffer free: SEPP -> the softmax copied S(gs-2) to registers;
-        // else P(gs-2) was written over it and PV(gs-2) must have read it.
-        // INORDER: PV(gs-2) was ISSUED (previous iteration) before this S MMA,
-        // and tcgen05.mma ops of a thread execute in issue order, so waiting
-        // for its completion is unnecessary.
-        if (SEPP || !INORDER) mbar_wait(BAR((SEPP ? B_SEMPTY : B_PFREE) + sb), ((gs >> 1) & 1) ^ 1);
+        mbar_wait(BAR(C::B_PFREE + sb), ((gs / NB) & 1) ^ 1);
+        if (lane == 0) BSA_TR(13, gs);
+#else
+        mbar_wait2(BAR(C::B_KFULL + sk), (gs / NK) & 1, BAR(C::B_PFREE + sb), ((gs / NB) & 1) ^ 1);
+#endif
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             if (BSA_TC_EXPERIMENT == 2) continue;
-            if constexpr (QT)
-              mma_ts(tmem + TM_S + sb * 64, tmem + TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
-                     k > 0 ? 1u : 0u);
-            else
-              mma_ss(tmem + TM_S + sb * 64, dq + (uint64_t)(2 * k), dk + (uint64_t)(2 * k), id_s,
-                     k > 0 ? 1u : 0u);
+            mma_ts(tmem + C::TM_S + sb * 64, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
+                   k > 0 ? 1u : 0u);
           }
-          tc_commit(BAR(B_SFULL + sb));
-          tc_commit(BAR(B_KEMPTY + sk));
-          if (!QT && j == ntiles - 1) tc_commit(BAR(B_QEMPTY));
+          tc_commit(BAR(C::B_SFULL + sb));
+          tc_commit(BAR(C::B_KEMPTY + sk));
           BSA_TR(1, gs);
         }
         __syncwarp();
         ++gs;
-        if (j >= PV_LAG) issue_pv(j - PV_LAG);
+      };
+      auto issue_pv = [&](int jj) {
+        const uint32_t sv = gp % NV, pb = gp % NB;
+        if (lane == 0) BSA_TR(10, gp);
+#ifdef BSA_TC_TRACE_BUILD
+        mbar_wait(BAR(C::B_PFULL + pb), (gp / NB) & 1);
+        if (lane == 0) BSA_TR(7, gp);
+        mbar_wait(BAR(C::B_VFULL + sv), (gp / NV) & 1);
+        if (lane == 0) BSA_TR(5, gp);
+#else
+        mbar_wait2(BAR(C::B_PFULL + pb), (gp / NB) & 1, BAR(C::B_VFULL + sv), (gp / NV) & 1);
+#endif
+        if (jj == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dv = dv0 + (uint64_t)((sv * C::V_STAGE) >> 4);
+          // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
+          // column halves: half k>>1 wrote its P over S columns 32*(k>>1)
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k)
+            if (BSA_TC_EXPERIMENT != 2)
+              mma_ts(tmem + C::TM_O,
+                     tmem + C::TM_S + pb * 64 + (EXACT ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
+                     dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
+          tc_commit(BAR(C::B_PFREE + pb));
+          tc_commit(BAR(C::B_VEMPTY + sv));
+          BSA_TR(2, gp);
+        }
+        __syncwarp();
+        ++gp;
+      };
+      if constexpr (C::SPLIT) {
+        if (do_s) {
+          for (int j = 0; j < ntiles; ++j) issue_s();
+        } else {
+          for (int j = 0; j < ntiles; ++j) issue_pv(j);
+        }
+      } else {
+        const int lead = ntiles < C::LEAD ? ntiles : C::LEAD;
+        for (int j = 0; j < lead; ++j) issue_s();
+        for (int j = 0; j < ntiles; ++j) {
+          if (j + C::LEAD < ntiles) issue_s();
+          issue_pv(j);
+        }
       }
-      for (int jj = ntiles > PV_LAG ? ntiles - PV_LAG : 0; jj < ntiles; ++jj) issue_pv(jj);
-      if (elect_one()) tc_commit(BAR(B_OFULL));
-      __syncwarp();
+      if (do_pv) {
+        if (elect_one()) tc_commit(BAR(C::B_OFULL));
+        __syncwarp();
+      }
       ++it;
     }
   } else {
-    // ======================= softmax warps 0..7 =======================
-    const int half = warp >> 2, quarter = warp & 3;
+    // ======================= softmax warps =======================
+    const int grp = warp >> 2, quarter = warp & 3;
     const int row = quarter * 32 + lane;  // TMEM lane == query row in the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float sl2 = A.scale_log2;
     const float NEG_INF = -__int_as_float(0x7f800000);
-    // largest tile sum (hence P value) accepted with the stale offset: keeps P
-    // and the fp32 accumulators far from overflow (fp16 P: its 65504 range)
+    // (no LSUM) largest tile sum (hence P value) accepted with the stale
+    // offset: keeps P and the fp32 accumulators far from overflow (fp16 P:
+    // its 65504 range)
     const float P_LIMIT = F16P ? 32768.0f : 18446744073709551616.0f;
-    float* x_first = xch;            // [2][128]
-    float* x_tile = xch + 2 * BQ;    // [2][128] (EXACT)
-    float* x_l = xch + 4 * BQ;       // [2][128]
+    (void)P_LIMIT;
+    float* x_first = xch;              // [NG][128]
+    float* x_tile = xch + NG * BQ;     // [NG][128] (EXACT)
+    float* x_l = xch + 2 * NG * BQ;    // [NG][128] (EXACT)
+    // TMEM column of keys 32*hh..32*hh+31 of tile gg's S
+    auto s_half_col = [&](uint32_t gg, int hh) -> uint32_t {
+      return C::TM_S + (gg % NB) * 64 + hh * 32;
+    };
+    // the NG warps sharing this TMEM lane quarter
+    auto quarter_sync = [&]() {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "n"(32 * NG) : "memory");
+    };
     uint32_t it = 0, g = 0;
     while (true) {
       const uint32_t slot = it & 1;
-      mbar_wait(BAR(B_IFULL + slot), (it >> 1) & 1);
+      mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
       const int32_t code = item_ring[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(BAR(B_IEMPTY + slot));
+      if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
       if (code < 0) break;
       const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
-      if constexpr (QT) {
-        // this thread's half of its query row of the packed partitioned Q ->
-        // TMEM (16 columns of bf16 pairs: the A operand of S = Q K^T).  The
-        // previous item's S MMAs are complete: their S tiles were consumed.
+      {
+        // this warp's 64/NG dimensions of its query row of the packed
+        // partitioned Q -> TMEM (bf16 pairs: the A operand of S = Q K^T).  The
+        // previous item's S MMAs are complete: its epilogue waited for O.
+        // 16-dimension chunks c (8 packed columns) with c % NG == grp
         const int32_t pr = I.row0 + row;
-        uint32_t qr[16];
-        if (pr < (int32_t)G.T) {
-          const uint4* src =
-              reinterpret_cast<const uint4*>(A.qp + ((int64_t)I.h * G.T + pr) * D + half * 32);
+        for (int c = grp; c < 4; c += NG) {
+          uint32_t qr[8];
+          if (pr < (int32_t)G.T) {
+            const uint4* src =
+                reinterpret_cast<const uint4*>(A.qp + ((int64_t)I.h * G.T + pr) * D + c * 16);
+            const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+            qr[0] = v0.x; qr[1] = v0.y; qr[2] = v0.z; qr[3] = v0.w;
+            qr[4] = v1.x; qr[5] = v1.y; qr[6] = v1.z; qr[7] = v1.w;
+          } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint4 v = __ldg(src + c);
-            qr[4 * c] = v.x; qr[4 * c + 1] = v.y; qr[4 * c + 2] = v.z; qr[4 * c + 3] = v.w;
+            for (int e = 0; e < 8; ++e) qr[e] = 0u;
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) qr[c] = 0u;
+          tmem_st8(tmem + lane_off + C::TM_Q + c * 8, qr);
         }
-        tmem_st16(tmem + lane_off + TM_Q + half * 16, qr);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(B_QFULL));
+        if (lane == 0) mbar_arrive(BAR(C::B_QFULL));
       }
       float m = NEG_INF, l = 0.0f;
       bool ovf = false;
-      if constexpr (TILE_SPLIT && !EXACT) {
-        const int grp = half;                 // serves S buffer `grp`: tiles with (g+j)&1 == grp
-        const int first_grp = (int)(g & 1);   // group that owns the item's tile 0
+      if constexpr (!EXACT) {
+        // ---- stale max: group grp takes tiles j with (g + j) % NG == grp ----
+        const int first_grp = (int)(g % NG);  // group that owns the item's tile 0
         if (grp == first_grp) {
-          // tile 0's row max (both column halves) becomes the item's offset
-          mbar_wait(BAR(B_SFULL + grp), (g >> 1) & 1);
+          // tile 0's row max becomes the item's offset
+          const uint32_t sb = g % NB;
+          mbar_wait(BAR(C::B_SFULL + sb), (g / NB) & 1);
           tc_fence_after();
           const int len0 = chunk_len(I, 0);
           float mx = NEG_INF;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t sr[32];
-            const uint32_t s_col = tmem + lane_off + TM_S + grp * 64 + hh * 32;
+            const uint32_t s_col = tmem + lane_off + s_half_col(g, hh);
             tmem_ld16(s_col, &sr[0]);
             tmem_ld16(s_col + 16, &sr[16]);
             tmem_wait_ld();
@@ -773,40 +910,26 @@ __global__ void __maxnreg__(MAX_REGS)
           }
           x_first[row] = mx;
         }
-        pair_sync(quarter);
+        quarter_sync();
         m = x_first[row] * sl2;
-        for (int j = (grp - first_grp) & 1; j < ntiles; j += 2) {
-          const uint32_t gg = g + j, sb = grp;
+        for (int j = (grp - first_grp + NG) % NG; j < ntiles; j += NG) {
+          const uint32_t gg = g + j, sb = gg % NB;
           const int len = chunk_len(I, j);
-          if (lane == 0 && warp < 4) BSA_TR(4 + warp, gg);
-          mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
+          if (lane == 0 && quarter == 0) BSA_TR(4, gg);
+          mbar_wait(BAR(C::B_SFULL + sb), (gg / NB) & 1);
           tc_fence_after();
-          if (SEPP && gg >= 2) {
-            // own P buffer: free once PV(gg-2) has read it
-            mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
-            tc_fence_after();
-          }
+          if (lane == 0 && quarter == 0) BSA_TR(8, gg);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            // 32 keys at a time; P (16 packed columns) goes to this half's
-            // P columns (SEPP) or over S columns this thread has already read
+            // 32 keys at a time; their P (16 packed columns) goes over S
+            // columns this thread has already read
             uint32_t sr[32];
-            const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + hh * 32;
-#if BSA_TC_LD32
-            tmem_ld32(s_col, sr);
-#else
+            const uint32_t s_col = tmem + lane_off + s_half_col(gg, hh);
             tmem_ld16(s_col, &sr[0]);
             tmem_ld16(s_col + 16, &sr[16]);
-#endif
             tmem_wait_ld();
             reg_fence16(&sr[0]);
             reg_fence16(&sr[16]);
-            if (SEPP && hh == 1) {
-              // S(gg) is in registers: the MMA warp may compute S(gg+2) here
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
-            }
             float s[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
@@ -815,86 +938,71 @@ __global__ void __maxnreg__(MAX_REGS)
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
+            const uint32_t p_col = tmem + lane_off + C::TM_S + sb * 64 + hh * 16;
 #if BSA_TC_EXPERIMENT == 1
-            {
+            {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
 #pragma unroll
               for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
-              tmem_st16(tmem + lane_off + p_col16(sb, hh, false), r);
+              tmem_st16(p_col, r);
             }
-            const float lt = 1.0f;
 #else
-            const float lt =
-                exp_half<POLY, F16P, !LSUM>(s, sl2, m, tmem + lane_off + p_col16(sb, hh, false));
-#endif
+            const float lt = exp_half<POLY, F16P, !LSUM>(s, sl2, m, p_col);
             if constexpr (!LSUM) {
               ovf |= !(lt <= P_LIMIT);
               l += lt;
             }
+#endif
           }
-          if (lane == 0 && warp < 4) BSA_TR(12 + warp, gg);
+          if (lane == 0 && quarter == 0) BSA_TR(12, gg);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(BAR(B_PFULL + sb));
-            if (warp < 4) BSA_TR(16 + warp, gg);
+            mbar_arrive(BAR(C::B_PFULL + sb));
+            if (quarter == 0) BSA_TR(16, gg);
           }
         }
-      } else
-      for (int j = 0; j < ntiles; ++j) {
-        const uint32_t gg = g + j, sb = gg & 1;
-        const int len = chunk_len(I, j) - half * 32;  // valid keys of this half
-        if (lane == 0 && warp < 4) BSA_TR(4 + warp, gg);
-        mbar_wait(BAR(B_SFULL + sb), (gg >> 1) & 1);
-        tc_fence_after();
-        uint32_t sr[32];
-        const uint32_t s_col = tmem + lane_off + TM_S + sb * 64 + half * 32;
-        tmem_ld16(s_col, &sr[0]);
-        tmem_ld16(s_col + 16, &sr[16]);
-        tmem_wait_ld();
-        reg_fence16(&sr[0]);
-        reg_fence16(&sr[16]);
-        if constexpr (SEPP) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(BAR(B_SEMPTY + sb));
-        }
-        if (lane == 0 && warp < 4) BSA_TR(8 + warp, gg);
-        float s[32];
+      } else {
+        // ---- exact max: the two groups split every tile into key halves ----
+        const int half = grp;
+        for (int j = 0; j < ntiles; ++j) {
+          const uint32_t gg = g + j, sb = gg % NB;
+          const int len = chunk_len(I, j) - half * 32;  // valid keys of this half
+          mbar_wait(BAR(C::B_SFULL + sb), (gg / NB) & 1);
+          tc_fence_after();
+          uint32_t sr[32];
+          const uint32_t s_col = tmem + lane_off + C::TM_S + sb * 64 + half * 32;
+          tmem_ld16(s_col, &sr[0]);
+          tmem_ld16(s_col + 16, &sr[16]);
+          tmem_wait_ld();
+          reg_fence16(&sr[0]);
+          reg_fence16(&sr[16]);
+          float s[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
-        if (len < 32) {
+          for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
+          if (len < 32) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e >= len) s[e] = NEG_INF;
-        }
-        if constexpr (!EXACT) {
-          if (j == 0) {
-            // first tile: the row max over both halves becomes the offset
-            x_first[half * BQ + row] = max32(s);
-            pair_sync(quarter);
-            m = fmaxf(x_first[row], x_first[BQ + row]) * sl2;
+            for (int e = 0; e < 32; ++e)
+              if (e >= len) s[e] = NEG_INF;
           }
-        } else {
           // exact offset: tile max over both halves, lazy (2^8) rescaling
-          float* xt = x_tile;
-          xt[half * BQ + row] = max32(s);
-          pair_sync(quarter);
-          const float mnew = fmaxf(m, fmaxf(xt[row], xt[BQ + row]) * sl2);
-          pair_sync(quarter);  // both halves read before the next tile's write
+          x_tile[half * BQ + row] = max32(s);
+          quarter_sync();
+          const float mnew = fmaxf(m, fmaxf(x_tile[row], x_tile[BQ + row]) * sl2);
+          quarter_sync();  // both halves read before the next tile's write
           const bool need = mnew > m + 8.0f;
           if (__any_sync(0xffffffffu, need)) {
             const float alpha = need ? ex2(m - mnew) : 1.0f;
             if (j > 0) {
               // O must be stable: wait for PV of the previous tile; each half
               // rescales its 32 columns of O
-              mbar_wait(BAR(B_PFREE + ((gg - 1) & 1)), ((gg - 1) >> 1) & 1);
+              mbar_wait(BAR(C::B_PFREE + (gg - 1) % NB), ((gg - 1) / NB) & 1);
               tc_fence_after();
 #pragma unroll
               for (int c = 0; c < 2; ++c) {
                 uint32_t orr[16];
-                const uint32_t oc = tmem + lane_off + TM_O + half * 32 + c * 16;
+                const uint32_t oc = tmem + lane_off + C::TM_O + half * 32 + c * 16;
                 tmem_ld16(oc, orr);
                 tmem_wait_ld();
                 reg_fence16(orr);
@@ -909,47 +1017,30 @@ __global__ void __maxnreg__(MAX_REGS)
               m = mnew;
             }
           }
-        }
-        const uint32_t p_col = tmem + lane_off + p_col16(sb, half, true);
-        if (SEPP && gg >= 2) {
-          mbar_wait(BAR(B_PFREE + sb), ((gg - 2) >> 1) & 1);
-          tc_fence_after();
-        }
-#if BSA_TC_EXPERIMENT == 1
-        float lt;
-        {  // timing experiment: no exponentials (results are wrong)
-          uint32_t r[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) r[e] = pack_bf16(s[2 * e], s[2 * e + 1]);
-          tmem_st16(p_col, r);
-          lt = 1.0f;
-        }
-#else
-        const float lt = exp_half<POLY, F16P>(s, sl2, m, p_col);
-#endif
-        if (!EXACT) ovf |= !(lt <= P_LIMIT);
-        l += lt;
-        if (lane == 0 && warp < 4) BSA_TR(12 + warp, gg);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(BAR(B_PFULL + sb));
-          if (warp < 4) BSA_TR(16 + warp, gg);
+          l += exp_half<POLY, F16P>(s, sl2, m, tmem + lane_off + C::TM_S + sb * 64 + half * 32);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(C::B_PFULL + sb));
         }
       }
-      // epilogue: O / l.  The halves combine l; each writes its 32 columns.
-      x_l[half * BQ + row] = l;
-      pair_sync(quarter);
-      float ltot = x_l[row] + x_l[BQ + row];
-      mbar_wait(BAR(B_OFULL), it & 1);
+      // ---- epilogue: O / l; each warp writes its 64/NG columns of the row ----
+      float ltot = 0.0f;
+      if constexpr (EXACT || !LSUM) {
+        x_l[grp * BQ + row] = l;
+        quarter_sync();
+#pragma unroll
+        for (int q = 0; q < NG; ++q) ltot += x_l[q * BQ + row];
+        if (!EXACT) ovf |= !(ltot <= 1.2676506e30f);
+      }
+      mbar_wait(BAR(C::B_OFULL), it & 1);
       tc_fence_after();
-      if constexpr (LSUM && TILE_SPLIT && !EXACT) {
+      if constexpr (!EXACT && LSUM) {
         // row sum of P from the tensor core (O column 64); an overflowed
         // stale offset shows up as inf / a huge sum -> exact repair launch
         uint32_t lr;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                     : "=r"(lr) : "r"(tmem + lane_off + TM_O + 64));
+                     : "=r"(lr) : "r"(tmem + lane_off + C::TM_O + 64));
         tmem_wait_ld();
         asm volatile("" : "+r"(lr));
         ltot = __uint_as_float(lr);
@@ -968,16 +1059,16 @@ __global__ void __maxnreg__(MAX_REGS)
         orow_bf16 = (__nv_bfloat16*)A.out_ptrs[r] + ((int64_t)I.h * tr + (dst - t0)) * D;
       }
       const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / ltot;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      // 16-column chunks c with c % NG == grp
+      for (int c = grp; c < 4; c += NG) {
+        const int col0 = c * 16;
         uint32_t orr[16];
-        tmem_ld16(tmem + lane_off + TM_O + half * 32 + c * 16, orr);
+        tmem_ld16(tmem + lane_off + C::TM_O + col0, orr);
         tmem_wait_ld();
         reg_fence16(orr);
         if (store) {
-          const int64_t base = ((int64_t)I.h * G.T + dst) * D + half * 32 + c * 16;
           if (A.out_bf16) {
-            uint4* op = reinterpret_cast<uint4*>(orow_bf16 + half * 32 + c * 16);
+            uint4* op = reinterpret_cast<uint4*>(orow_bf16 + col0);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               uint4 v;
@@ -988,7 +1079,7 @@ __global__ void __maxnreg__(MAX_REGS)
               op[q] = v;
             }
           } else {
-            float4* op = reinterpret_cast<float4*>((float*)A.out + base);
+            float4* op = reinterpret_cast<float4*>((float*)A.out + ((int64_t)I.h * G.T + dst) * D + col0);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               op[q] = make_float4(__uint_as_float(orr[4 * q]) * inv, __uint_as_float(orr[4 * q + 1]) * inv,
@@ -998,11 +1089,11 @@ __global__ void __maxnreg__(MAX_REGS)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(BAR(B_OEMPTY));
+      if (lane == 0) mbar_arrive(BAR(C::B_OEMPTY));
       if constexpr (!EXACT) {
         // stale offset overflowed somewhere in this item: list it once for
         // the exact-max launch (which rewrites all of its rows)
-        if (__any_sync(0xffffffffu, ovf) && lane == 0) {
+        if ((grp == 0 || !LSUM) && __any_sync(0xffffffffu, ovf) && lane == 0) {
           if (atomicCAS(&A.ovf_flags[code], 0, 1) == 0) A.ovf_list[atomicAdd(A.ovf_count, 1)] = code;
         }
       }
@@ -1013,9 +1104,10 @@ __global__ void __maxnreg__(MAX_REGS)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == MMA_WARP) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(C::TMEM_COLS)
                  : "memory");
   }
 }
@@ -1058,7 +1150,7 @@ static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, in
   return BSA_OK;
 }
 
-size_t tc_smem_bytes() { return tc::SMEM_BYTES; }
+size_t tc_smem_bytes() { return tc::CfgMain::SMEM_BYTES; }
 
 // events bracketing the most recent timed attention-kernel launch (per thread)
 cudaEvent_t timing_events(int which) {
@@ -1074,10 +1166,11 @@ template <int POLY, bool F16P, bool EXACT>
 static int launch_variant(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                           const AttnGeom& G,
                           const TcArgs& a, int grid, cudaStream_t st) {
+  using C = tc::Cfg<BSA_TC_WIDE != 0 && !EXACT>;
   auto kern = tc::bsa_tc_kernel<POLY, F16P, EXACT>;
   BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::SMEM_BYTES));
-  kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
+                                    C::SMEM_BYTES));
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
@@ -1104,7 +1197,7 @@ static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   CUtensorMap mk, mv;
   CUtensorMap mq;
-  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);  // (SEPP) Q tile box 64 x 128 rows
+  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);  // unused by the kernel (Q goes via registers)
   if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
   if (!rc)
     rc = make_map(&mv, a.vp, G.H, G.T, tc::CH,
@@ -1117,7 +1210,7 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
                              ? (a.n_items - a.shard + a.num_shards - 1) / a.num_shards
                              : a.n_items;
   const int grid =
-      (int)std::min<int64_t>((int64_t)sms * tc::CTAS_PER_SM, std::max<int64_t>(1, n_work));
+      (int)std::min<int64_t>((int64_t)sms * tc::CfgMain::CTAS_PER_SM, std::max<int64_t>(1, n_work));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_flags, 0, (size_t)a.n_items * 4, st));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_count, 0, 4, st));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
