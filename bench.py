@@ -68,8 +68,9 @@ def parse():
     ap.add_argument("--combine", default="allreduce", choices=["allreduce", "scatter"],
                     help="--mode sharded output combine: NCCL sum all-reduce, or the kernel "
                          "epilogue storing rows into the owners' buffers over NVLink (CUDA IPC)")
-    ap.add_argument("--e2e-chunk", type=int, default=2,
-                    help="heads per pipeline chunk of the host-memory e2e leg")
+    ap.add_argument("--e2e-chunk", default="auto",
+                    help="head chunks of the host-memory e2e leg: 'auto' (1,3,4,..,4,3,1), "
+                         "heads per chunk, or a comma list of chunk sizes")
     ap.add_argument("--specials", type=int, default=S_PER_FRAME,
                     help="special tokens per frame (VGGT 5; pi3: 4 register tokens, no camera)")
     return ap.parse_args()
@@ -321,7 +322,12 @@ def run_ours(a):
             # public host-memory entry point: per-head-chunk pipeline with the
             # H2D / D2H copies overlapped with the kernels (pipeline.py)
             from paper_2509_07120_b200.pipeline import HostLayerPipeline
-            pipe = HostLayerPipeline(H, T, d, torch.bfloat16, chunk_heads=a.e2e_chunk)
+            if a.e2e_chunk == "auto":
+                chunks = "auto"
+            else:
+                sizes = [int(x) for x in str(a.e2e_chunk).split(",")]
+                chunks = sizes[0] if len(sizes) == 1 else sizes
+            pipe = HostLayerPipeline(H, T, d, torch.bfloat16, chunk_heads=chunks)
 
             def e2e_step():
                 pipe.run(hq, hk, hv, lay, pol, out=hout)
@@ -348,7 +354,7 @@ def run_ours(a):
         e2e = {"value": a.frames * layers / (e2e_ms * 1e-3), "unit": "frames/s",
                "ms_per_step": e2e_ms,
                "path": ("pipeline.HostLayerPipeline: pinned host Q/K/V in, host output back, "
-                        f"H2D/D2H overlapped with the kernels per {a.e2e_chunk}-head chunk"
+                        f"H2D/D2H overlapped with the kernels per head chunk ({a.e2e_chunk})"
                         if not sharded else "H2D + shard.sharded_sparse_attention + D2H"),
                "h2d_bytes_per_step": 3 * q_in.numel() * 2, "d2h_bytes_per_step": q_in.numel() * 2}
 

@@ -25,17 +25,49 @@ from .maskpred import BlockMask, MaskPolicy, predict_mask
 from .sparse import SparseAttentionJob, sparse_attention
 
 
+def ramp_chunks(heads: int, peak: int = 4) -> list[int]:
+    """Chunk sizes 1, 3, peak, ..., peak, 3, 1: one-head chunks at both ends
+    keep the uncovered first H2D and last D2H short; larger middle chunks
+    keep the kernels efficient (measured best at H=16: 1,3,4,4,3,1)."""
+    if heads <= 2:
+        return [1] * heads
+    ends = [1, 3] if heads >= 8 else [1]
+    mid = heads - 2 * sum(ends)
+    n = -(-mid // peak)  # middle chunks, as even as possible
+    sizes = [mid // n + (1 if i < mid % n else 0) for i in range(n)] if mid else []
+    return ends + sizes + ends[::-1]
+
+
 class HostLayerPipeline:
     """Reusable device buffers and streams for repeated layers of one shape."""
 
     def __init__(self, heads: int, tokens: int, head_dim: int, dtype=torch.bfloat16,
-                 chunk_heads: int = 2, device=None):
-        if chunk_heads < 1:
-            raise ValueError(f"chunk_heads must be >= 1, got {chunk_heads}")
+                 chunk_heads="auto", device=None):
+        """chunk_heads: heads per pipeline chunk, the list of chunk sizes
+        (summing to `heads`), or "auto" (ramp_chunks). Small first and last
+        chunks shorten the ramp: the first H2D and the last D2H are the only
+        uncovered copies."""
+        if isinstance(chunk_heads, str):
+            if chunk_heads != "auto":
+                raise ValueError(f"chunk_heads must be an int, a list or 'auto', got {chunk_heads!r}")
+            sizes = ramp_chunks(heads)
+        elif isinstance(chunk_heads, int):
+            if chunk_heads < 1:
+                raise ValueError(f"chunk_heads must be >= 1, got {chunk_heads}")
+            c = min(chunk_heads, heads)
+            sizes = [min(c, heads - h0) for h0 in range(0, heads, c)]
+        else:
+            sizes = [int(x) for x in chunk_heads]
+            if any(x < 1 for x in sizes) or sum(sizes) != heads:
+                raise ValueError(f"chunk sizes {sizes} must be >= 1 and sum to {heads}")
         self.device = torch.device(device or "cuda")
         self.shape = (heads, tokens, head_dim)
         self.dtype = dtype
-        self.chunk = min(chunk_heads, heads)
+        self.chunks = []
+        h0 = 0
+        for x in sizes:
+            self.chunks.append((h0, h0 + x))
+            h0 += x
         self.bufs = [torch.empty(self.shape, dtype=dtype, device=self.device) for _ in range(3)]
         self.obuf = torch.empty(self.shape, dtype=dtype, device=self.device)
         self.s_in = torch.cuda.Stream(self.device)
@@ -55,12 +87,11 @@ class HostLayerPipeline:
                                  f"device-resident inputs)")
         if out is None:
             out = torch.empty(self.shape, dtype=self.dtype, pin_memory=True)
-        H = self.shape[0]
         dq, dk, dv = self.bufs
         comp = torch.cuda.current_stream(self.device)
         masks = []
         done_in, done_comp = [], []
-        chunks = [(h0, min(H, h0 + self.chunk)) for h0 in range(0, H, self.chunk)]
+        chunks = self.chunks
         # the copy-in stream must not overwrite buffers a previous call still reads
         self.s_in.wait_stream(comp)
         for a, b in chunks:
@@ -89,11 +120,11 @@ class HostLayerPipeline:
         return (out, masks) if return_masks else out
 
 
-def attend_from_host(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, chunk_heads: int = 2,
+def attend_from_host(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, chunk_heads="auto",
                      out=None):
     """One-shot convenience wrapper around HostLayerPipeline."""
     p = HostLayerPipeline(q.shape[0], q.shape[1], q.shape[2], q.dtype, chunk_heads)
     return p.run(q, k, v, layout, policy, out)
 
 
-__all__ = ["HostLayerPipeline", "attend_from_host", "BlockMask"]
+__all__ = ["HostLayerPipeline", "attend_from_host", "ramp_chunks", "BlockMask"]

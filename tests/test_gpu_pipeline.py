@@ -6,7 +6,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("chunk", [1, 2, 3])
+@pytest.mark.parametrize("chunk", [1, 2, 3, "auto", [2, 1, 2]])
 def test_pipeline_equals_device_path(chunk):
     import torch
     import paper_2509_07120_b200 as bsa
