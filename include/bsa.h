@@ -192,6 +192,31 @@ int bsa_mask_to_csr(const uint8_t* mask_bits, int64_t heads, int64_t nq, int64_t
                     void* stream);
 size_t bsa_mask_to_csr_workspace(int64_t heads, int64_t nq);
 
+/* ---- dense attention statistics without the (H, T, T) map ----------------
+ * the reference materialises the post-softmax map
+ * (dense_attention_map, dense.py:79-102) and reduces it on the CPU
+ * (quadrant_stats, analysis.py:47-74).  These stream S = Q K^T through the
+ * tensor cores instead (bf16 q/k in source token order, head_dim 64).
+ *
+ * bsa_attention_row_stats: row_stats (H, T, 5) fp32 in source token order,
+ *   per query row with x = s * scale * log2(e) over all T keys:
+ *   [0] m = max x, [1] sum over special keys of 2^(x - m), [2] the same over
+ *   patch keys, [3] max x over special keys, [4] max x over patch keys.
+ *   So p(row, key) = 2^(x - m) / ([1] + [2]).
+ * bsa_block_attention_map: from those row stats, block_map (H, nq, nk) fp32
+ *   (block_q 128, block_k 64 over the patch tokens, the BlockMask geometry):
+ *   the attention mass of patch q-block qb on patch k-block kb, i.e. the
+ *   mean over the q-block's rows of the summed probabilities of the
+ *   k-block's keys.  Deterministic (fixed reduction order).
+ * Both pack q/k into the workspace (bsa_attention_stats_workspace bytes). */
+size_t bsa_attention_stats_workspace(const bsa_layout* layout, int64_t heads);
+int bsa_attention_row_stats(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* layout,
+                            float scale, float* row_stats, void* ws, size_t ws_bytes,
+                            void* stream);
+int bsa_block_attention_map(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* layout,
+                            float scale, const float* row_stats, float* block_map, void* ws,
+                            size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -322,3 +322,57 @@ def dense_attention_port(q, k, v, row_chunk=256):
             s /= s.sum(axis=1, keepdims=True)
             out[hh, r0:r0 + row_chunk] = s @ v[hh]
     return out
+
+
+# ---- dense attention-map statistics -----------------
+# Checkers for paper_2509_07120_b200.analysis: the reference's
+# dense_attention_map (dense.py:79-102) in float64, its quadrant_stats
+# (analysis.py:47-74), and the block-granular attention mass at the
+# BlockMask geometry.
+
+def attention_map_f64(q, k) -> np.ndarray:
+    """Post-softmax map (H, T, T) in float64 (dense.py:79-102)."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    scale = float(np.float32(head_scale(q.shape[2])))
+    out = np.empty((q.shape[0], q.shape[1], k.shape[1]), dtype=np.float64)
+    for h in range(q.shape[0]):
+        s = (q[h] @ k[h].T) * scale
+        s -= s.max(axis=1, keepdims=True)
+        e = np.exp(s)
+        out[h] = e / e.sum(axis=1, keepdims=True)
+    return out
+
+
+def quadrant_stats_f64(p, frames: int, patches: int, specials: int, specials_first: bool = True):
+    """(means, maxes) dicts of (H,) arrays per quadrant, analysis.py:47-74."""
+    n = frames * (patches + specials)
+    is_special = np.zeros(n, dtype=bool)
+    perm, _ = partition_perm(frames, patches, specials, specials_first)
+    is_special[perm[:frames * specials]] = True
+    groups = {"S2S": (is_special, is_special), "S2P": (is_special, ~is_special),
+              "P2S": (~is_special, is_special), "P2P": (~is_special, ~is_special)}
+    means, maxes = {}, {}
+    for quad, (qs, ks) in groups.items():
+        if not qs.any() or not ks.any():
+            continue
+        sub = p[:, qs][:, :, ks]
+        means[quad] = sub.mean(axis=(1, 2))
+        maxes[quad] = sub.max(axis=(1, 2))
+    return means, maxes
+
+
+def block_attention_map_f64(p, frames: int, patches: int, specials: int, block_q: int = 128,
+                            block_k: int = 64) -> np.ndarray:
+    """(H, nq, nk): mean over the rows of each patch q-block of the summed
+    probabilities of each patch k-block (partitioned patch order)."""
+    pidx = patch_indices(frames, patches, specials)
+    pp = p[:, pidx][:, :, pidx]
+    tp = len(pidx)
+    nq, nk = -(-tp // block_q), -(-tp // block_k)
+    out = np.zeros((p.shape[0], nq, nk), dtype=np.float64)
+    for a in range(nq):
+        rows = pp[:, a * block_q:(a + 1) * block_q]
+        for b in range(nk):
+            out[:, a, b] = rows[:, :, b * block_k:(b + 1) * block_k].sum(axis=2).mean(axis=1)
+    return out

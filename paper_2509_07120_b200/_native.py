@@ -93,6 +93,9 @@ def _declare(L):
         "bsa_ipc_open": ([vp, ctypes.POINTER(vp)], ctypes.c_int),
         "bsa_ipc_close": ([vp], ctypes.c_int),
         "bsa_ipc_free": ([vp], ctypes.c_int),
+        "bsa_attention_stats_workspace": ([pl, i64], sz),
+        "bsa_attention_row_stats": ([pt, pt, pl, f32, vp, vp, sz, vp], ctypes.c_int),
+        "bsa_block_attention_map": ([pt, pt, pl, f32, vp, vp, vp, sz, vp], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -111,7 +114,8 @@ def exported_symbols():
         "bsa_predict_mask", "bsa_sparse_attention_workspace", "bsa_sparse_attention",
         "bsa_sparse_attention_path", "bsa_last_kernel_ms", "bsa_mask_selected_area", "bsa_mask_to_csr_workspace",
         "bsa_mask_to_csr", "bsa_sparse_attention_scatter", "bsa_ipc_alloc", "bsa_ipc_open",
-        "bsa_ipc_close", "bsa_ipc_free",
+        "bsa_ipc_close", "bsa_ipc_free", "bsa_attention_stats_workspace",
+        "bsa_attention_row_stats", "bsa_block_attention_map",
     ]
 
 

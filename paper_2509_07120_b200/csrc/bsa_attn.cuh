@@ -128,5 +128,9 @@ struct TcArgs {
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);
 cudaEvent_t timing_events(int which);
 size_t tc_smem_bytes();
+// source-order (f32|bf16) Q/K/V -> contiguous bf16 [specials | patches]
+// (bsa_attn_host.cu; also used by the dense-statistics kernels)
+int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
+                cudaStream_t st);
 
 }  // namespace bsa

@@ -273,8 +273,8 @@ static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G) {
   return w;
 }
 
-static int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
-                       cudaStream_t st) {
+int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
+                cudaStream_t st) {
   const int64_t total = G.H * G.T * (G.d / 8);
   const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
   const bool bf = x->dtype == BSA_BF16;

@@ -24,7 +24,15 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))  # tests/
 
-from golden_inputs import CASES_ATTN, CASES_SCORE, SCORE_POLICIES, make_qkv, sample_rows  # noqa: E402
+from golden_inputs import (  # noqa: E402
+    CASES_ATTN,
+    CASES_MAP,
+    CASES_SCORE,
+    SCORE_POLICIES,
+    bf16_round,
+    make_qkv,
+    sample_rows,
+)
 
 import bsattn  # noqa: E402  (the reference, via PYTHONPATH)
 from bsattn import (  # noqa: E402
@@ -37,6 +45,8 @@ from bsattn import (  # noqa: E402
     predict_mask,
     sparse_attention,
 )
+from bsattn.analysis import quadrant_stats  # noqa: E402
+from bsattn.dense import dense_attention_map  # noqa: E402
 from bsattn.maskpred import block_pool, pooled_scores, select_blocks  # noqa: E402
 
 
@@ -96,12 +106,47 @@ def attn_case(name, frames, patches, specials, heads, d, seed, block_q, block_k,
     print(f"attn_{name}: T={lay.total_tokens} ({time.time() - t0:.1f}s)")
 
 
+def map_case(name, frames, patches, specials, heads, d, seed):
+    """Reference dense_attention_map (dense.py:79-102) + quadrant_stats
+    (analysis.py:47-74) on bf16-rounded q/k, and the block-granular mass
+    (mean over a 128-row patch q-block of the summed probabilities of a
+    64-key patch k-block) of that same reference map."""
+    t0 = time.time()
+    lay = TokenLayout(frames, patches, specials)
+    q, k, v = make_qkv(heads, lay.total_tokens, d, seed)
+    q, k = bf16_round(q), bf16_round(k)
+    maps = dense_attention_map(AttentionInputs(q, k, v))
+    st = quadrant_stats(maps, lay)
+    pidx = patch_token_indices(lay)
+    pp = maps[:, pidx][:, :, pidx].astype(np.float64)
+    tp = lay.patch_tokens
+    nq, nk = -(-tp // 128), -(-tp // 64)
+    bm = np.zeros((heads, nq, nk), dtype=np.float64)
+    for a in range(nq):
+        rows = pp[:, a * 128:(a + 1) * 128]
+        for b in range(nk):
+            bm[:, a, b] = rows[:, :, b * 64:(b + 1) * 64].sum(axis=2).mean(axis=1)
+    out = dict(frames=frames, patches=patches, specials=specials, heads=heads, d=d, seed=seed,
+               block_map=bm.astype(np.float32), quads=np.array(sorted(st.means)))
+    for quad in st.means:
+        out[f"mean_{quad}"] = st.means[quad]
+        out[f"max_{quad}"] = st.maxes[quad]
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: T={lay.total_tokens} ({time.time() - t0:.1f}s)")
+
+
 def main():
     print("reference bsattn", bsattn.__version__, "numpy", np.__version__)
+    only = sys.argv[1:]  # optional case names
     for c in CASES_SCORE:
-        score_case(**c)
+        if not only or c["name"] in only:
+            score_case(**c)
     for c in CASES_ATTN:
-        attn_case(**c)
+        if not only or c["name"] in only:
+            attn_case(**c)
+    for c in CASES_MAP:
+        if not only or c["name"] in only:
+            map_case(**c)
 
 
 if __name__ == "__main__":

@@ -67,3 +67,17 @@ def sample_rows(layout, block_q: int) -> np.ndarray:
         fr, loc = divmod(pi, p)
         rows.add(fr * per + s + loc)
     return np.array(sorted(rows), dtype=np.int64)
+
+# dense attention-map statistics: q, k rounded to bf16 first
+CASES_MAP = [
+    dict(name="map_spec", frames=3, patches=300, specials=5, heads=2, d=64, seed=31),
+    dict(name="map_nospec", frames=1, patches=777, specials=0, heads=2, d=64, seed=32),
+    dict(name="map_pi3", frames=4, patches=257, specials=4, heads=3, d=64, seed=33),
+]
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """float32 -> nearest bf16 (ties to even), returned as float32."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
