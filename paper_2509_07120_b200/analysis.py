@@ -146,6 +146,40 @@ def quadrant_stats_from_rows(row_stats: torch.Tensor, layout: TokenLayout) -> Qu
     return QuadrantStats(means=means, maxes=maxes, heads=int(row_stats.shape[0]))
 
 
+def quadrant_stats(attn_map, layout: TokenLayout, row_sum_tol: float = 1e-5) -> QuadrantStats:
+    """Reduce a materialised (heads, N, N) post-softmax map into per-quadrant
+    statistics, as analysis.py:47-74 (same validation and messages), on the
+    GPU. For maps too large to materialise use attention_quadrant_stats."""
+    dev = N.require_cuda()
+    if isinstance(attn_map, torch.Tensor):
+        a = attn_map.to(dev, torch.float32)
+    else:
+        arr = np.asarray(attn_map, dtype=np.float32)
+        if arr.ndim == 0 or min(arr.shape) < 1:
+            raise ValueError(f"attn_map has a zero-sized dimension: {arr.shape}")
+        if not np.isfinite(arr).all():
+            raise ValueError("attn_map contains non-finite values")
+        a = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+    if a.dim() != 3 or a.shape[1] != a.shape[2]:
+        raise ValueError(f"attn_map must be (heads, N, N), got {tuple(a.shape)}")
+    n = layout.total_tokens
+    if a.shape[1] != n:
+        raise ValueError(f"map covers {a.shape[1]} tokens, layout describes {n}")
+    sums = a.sum(dim=2, dtype=torch.float64)
+    if float((sums - 1.0).abs().max()) > row_sum_tol:
+        raise ValueError("rows do not sum to 1; expected a post-softmax map")
+    sp = _special_mask(layout, dev)
+    groups = {"S2S": (sp, sp), "S2P": (sp, ~sp), "P2S": (~sp, sp), "P2P": (~sp, ~sp)}
+    means, maxes = {}, {}
+    for quad, (qsel, ksel) in groups.items():
+        if not bool(qsel.any()) or not bool(ksel.any()):
+            continue
+        sub = a[:, qsel][:, :, ksel]
+        means[quad] = sub.double().mean(dim=(1, 2)).cpu().numpy()
+        maxes[quad] = sub.amax(dim=(1, 2)).double().cpu().numpy()
+    return QuadrantStats(means=means, maxes=maxes, heads=int(a.shape[0]))
+
+
 def attention_quadrant_stats(inp: AttentionInputs, layout: TokenLayout) -> QuadrantStats:
     """quadrant_stats(dense_attention_map(inp), layout) without the map."""
     return quadrant_stats_from_rows(attention_row_stats(inp, layout), layout)
@@ -165,4 +199,5 @@ def mask_recall(block_map, mask) -> np.ndarray | torch.Tensor:
 
 
 __all__ = ["QuadrantStats", "QUADRANTS", "attention_row_stats", "block_attention_map",
-           "quadrant_stats_from_rows", "attention_quadrant_stats", "mask_recall"]
+           "quadrant_stats", "quadrant_stats_from_rows", "attention_quadrant_stats",
+           "mask_recall"]

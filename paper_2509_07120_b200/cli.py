@@ -8,10 +8,13 @@ so its flows (tests/test_cli.py:44-112) run unchanged on the GPU:
     attend  .bsat q/k/v (+ .bsm) -> .bsat output, dense or block-sparse
             (+ --report per-head CSV)
     bench   dense vs sparse sweep, reference CSV schema (+ --with-predict)
+    analyze quadrant statistics, reference CSV schema: of a materialised
+            --map (as the reference), or streamed from --q/--k without the
+            map (analysis.py)
 
-``analyze``, ``correspond``, ``layerdrop`` and ``synth`` work on materialised
-attention maps or generate inputs. They are outside the data-parallel path
- and exit with a message.
+``correspond``, ``layerdrop`` and ``synth`` work on materialised attention
+maps or generate inputs. They are outside the data-parallel path (SURVEY.md
+§2.1) and exit with a message.
 """
 
 from __future__ import annotations
@@ -27,7 +30,7 @@ from .maskpred import MaskPolicy, predict_mask, read_mask, write_mask
 from .sparse import SparseAttentionJob, sparse_attention, sparse_attention_stats
 from .tensorio import read_tensor, write_tensor
 
-OUT_OF_SCOPE = ("analyze", "correspond", "layerdrop", "synth")
+OUT_OF_SCOPE = ("correspond", "layerdrop", "synth")
 
 
 def _fmt(x: float) -> str:
@@ -130,6 +133,45 @@ def _cmd_out_of_scope(args) -> None:
                      "it is outside the B200 data-parallel path (use the reference package)")
 
 
+def _cmd_analyze(args) -> None:
+    """cli.py:133-153: quadrant statistics CSV (layer, head, quadrant, mean,
+    max), then per-quadrant mean/std rows over heads."""
+    from .analysis import attention_quadrant_stats, quadrant_stats
+
+    if (args.map is None) == (args.q is None):
+        raise SystemExit("analyze needs either --map or --q/--k")
+    if args.map is not None:
+        attn_map = read_tensor(args.map)
+        if attn_map.ndim == 2:
+            attn_map = attn_map[None]
+        layout = layout_from_args(args, attn_map.shape[1])
+        stats = quadrant_stats(attn_map, layout)
+    else:
+        if args.k is None:
+            raise SystemExit("--q needs --k")
+        q, k = read_tensor(args.q), read_tensor(args.k)
+        if q.ndim == 2:
+            q, k = q[None], k[None]
+        if q.shape != k.shape:
+            raise SystemExit(f"q {q.shape} and k {k.shape} differ")
+        layout = layout_from_args(args, q.shape[1])
+        stats = attention_quadrant_stats(AttentionInputs(q, k, k), layout)
+    out = open(args.csv, "w", newline="") if args.csv else sys.stdout
+    try:
+        w = csv.writer(out)
+        w.writerow(["layer", "head", "quadrant", "mean", "max"])
+        for quad in stats.means:
+            for h in range(stats.heads):
+                w.writerow([args.layer, h, quad, _fmt(stats.means[quad][h]),
+                            _fmt(stats.maxes[quad][h])])
+        for quad, (mm, ms, xm, xs) in stats.aggregate().items():
+            w.writerow([args.layer, "mean", quad, _fmt(mm), _fmt(xm)])
+            w.writerow([args.layer, "std", quad, _fmt(ms), _fmt(xs)])
+    finally:
+        if args.csv:
+            out.close()
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="bsattn-b200",
                                  description="B200 block-sparse global attention toolkit")
@@ -180,6 +222,15 @@ def build_parser() -> argparse.ArgumentParser:
                    help="append the scoring-stage time (predict_ms) column")
     _block_flags(p)
     p.set_defaults(fn=_cmd_bench)
+
+    p = sub.add_parser("analyze", help="quadrant statistics of an attention map")
+    p.add_argument("--map", default=None, help=".bsat post-softmax map, (H,N,N) or (N,N)")
+    p.add_argument("--q", default=None, help="(instead of --map) .bsat Q, (H,N,64)")
+    p.add_argument("--k", default=None, help="(with --q) .bsat K: statistics without the map")
+    p.add_argument("--csv", default=None, help="output CSV path (stdout if omitted)")
+    p.add_argument("--layer", type=int, default=0, help="layer label for the CSV")
+    _layout_flags(p)
+    p.set_defaults(fn=_cmd_analyze)
 
     for name in OUT_OF_SCOPE:
         p = sub.add_parser(name, help="(out of scope in the B200 build)")

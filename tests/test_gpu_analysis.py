@@ -103,3 +103,56 @@ def test_config1_rows_vs_oracle(bsa):
     count = {"S2S": ns * ns, "S2P": ns * npch, "P2S": npch * ns, "P2P": npch * npch}
     for quad in sums:
         np.testing.assert_allclose(st.means[quad], sums[quad] / count[quad], rtol=2e-4)
+
+
+# ---- quadrant_stats on a materialised map: the reference's own tests
+# (test_analysis.py:44-100) --------------------------------------------------
+
+def _uniform_map(heads, n):
+    return np.full((heads, n, n), 1.0 / n, dtype=np.float32)
+
+
+def _flat_loop_oracle(attn_map, layout, bsa):
+    h, n, _ = attn_map.shape
+    spec = set(bsa.special_token_indices(layout).tolist())
+    sums = {q: np.zeros(h) for q in ("S2S", "S2P", "P2S", "P2P")}
+    counts = {q: 0 for q in sums}
+    maxes = {q: np.full(h, -np.inf) for q in sums}
+    for qi in range(n):
+        for ki in range(n):
+            quad = ("S" if qi in spec else "P") + "2" + ("S" if ki in spec else "P")
+            counts[quad] += 1
+            sums[quad] += attn_map[:, qi, ki]
+            maxes[quad] = np.maximum(maxes[quad], attn_map[:, qi, ki])
+    return ({q: sums[q] / counts[q] for q in sums if counts[q]},
+            {q: maxes[q] for q in maxes if counts[q]}, counts)
+
+
+def test_quadrant_stats_reference_cases(bsa):
+    from paper_2509_07120_b200.analysis import quadrant_stats
+
+    lay = bsa.TokenLayout(frames=2, patches_per_frame=6, specials_per_frame=2)
+    n = lay.total_tokens
+    st = quadrant_stats(_uniform_map(2, n), lay)
+    for quad in ("S2S", "S2P", "P2S", "P2P"):
+        np.testing.assert_allclose(st.means[quad], 1.0 / n, atol=1e-7)
+        np.testing.assert_allclose(st.maxes[quad], 1.0 / n, atol=1e-7)
+    lay0 = bsa.TokenLayout(frames=1, patches_per_frame=8, specials_per_frame=0)
+    st0 = quadrant_stats(_uniform_map(1, 8), lay0)
+    assert set(st0.means) == {"P2P"}
+    rng = np.random.default_rng(0)
+    lay2 = bsa.TokenLayout(frames=2, patches_per_frame=5, specials_per_frame=2)
+    n2 = lay2.total_tokens
+    m = np.exp(rng.standard_normal((2, n2, n2)).astype(np.float32))
+    m /= m.sum(axis=2, keepdims=True)
+    st2 = quadrant_stats(m, lay2)
+    means, maxes, counts = _flat_loop_oracle(m, lay2, bsa)
+    for quad in means:
+        np.testing.assert_allclose(st2.means[quad], means[quad], atol=1e-6)
+        np.testing.assert_allclose(st2.maxes[quad], maxes[quad], atol=1e-6)
+    assert sum(counts.values()) == n2 * n2
+    with pytest.raises(ValueError, match="sum"):
+        quadrant_stats(np.ones((1, 4, 4), dtype=np.float32),
+                       bsa.TokenLayout(frames=1, patches_per_frame=4, specials_per_frame=0))
+    agg = quadrant_stats(_uniform_map(3, 4), bsa.TokenLayout(1, 4, 0)).aggregate()
+    assert agg["P2P"][0] == pytest.approx(0.25) and agg["P2P"][1] == pytest.approx(0.0)
