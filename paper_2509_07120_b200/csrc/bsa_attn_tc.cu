@@ -124,7 +124,7 @@ struct Cfg {
   static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
   static constexpr int B_IEMPTY = B_IFULL + 2;   // [2]  softmax warps + MMA warp(s)
   static constexpr int B_COUNT = B_IEMPTY + 2;
-  static_assert(B_COUNT * 8 + 32 <= 1024, "barrier region");
+  static_assert(B_COUNT * 8 + 96 <= 1024, "barrier region");
   static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
   static_assert(TM_O + O_COLS <= TM_Q, "TMEM columns");
   static_assert(LEAD >= 1 && LEAD < NB, "S(j+LEAD) must only wait for a PV issued earlier");
@@ -239,8 +239,23 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = sbase + C::OFF_BAR;
   auto BAR = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+  // item ring: two slots of [code, decoded Item (8 fields)].  The producer
+  // decodes (two dependent global loads) while it waits for the slot, so the
+  // other warps start the next item without those loads.
   volatile int32_t* item_ring = (volatile int32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT);
-  uint32_t* tmem_holder = (uint32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT + 16);
+  uint32_t* tmem_holder = (uint32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT + 80);
+  auto ring_put = [&](uint32_t slot, int32_t code, const Item& I) {
+    volatile int32_t* r = item_ring + slot * 9;
+    r[0] = code;
+    r[1] = I.h; r[2] = I.qb; r[3] = I.row0; r[4] = I.rows;
+    r[5] = I.nchunks; r[6] = I.last_len; r[7] = I.nsc; r[8] = I.spec_last;
+  };
+  auto ring_get = [&](uint32_t slot, Item& I) -> int32_t {
+    volatile int32_t* r = item_ring + slot * 9;
+    I.h = r[1]; I.qb = r[2]; I.row0 = r[3]; I.rows = r[4];
+    I.nchunks = r[5]; I.last_len = r[6]; I.nsc = r[7]; I.spec_last = r[8];
+    return r[0];
+  };
   float* xch = (float*)(smem + C::OFF_XCH);  // [3][NG][128]: first-tile max, tile max, l
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -310,26 +325,27 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     while (true) {
       const uint32_t slot = it & 1;
       int32_t code;
+      Item I;
       if (is_k) {
         int64_t w = 0;
         if (lane == 0) w = atomicAdd(A.work_counter, 1);
         w = __shfl_sync(0xffffffffu, w, 0);
         code = -1;
         if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
+        if (code >= 0) I = decode(G, code, A.counts, A.bits);
         mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
         if (elect_one()) {
-          item_ring[slot] = code;
+          ring_put(slot, code, I);
           mbar_arrive(BAR(C::B_IFULL + slot));
         }
         __syncwarp();
       } else {
         mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
-        code = item_ring[slot];
+        code = ring_get(slot, I);
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
       }
       if (code < 0) break;
-      const Item I = decode(G, code, A.counts, A.bits);
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
       const int64_t nbytes = I.qb >= 0 ? G.mask_row_bytes : 0;
@@ -412,15 +428,16 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       int32_t code = -1;
       if (w < n_work)
         code = A.items[(!EXACT && A.num_shards > 1) ? w * A.num_shards + A.shard : w];
+      Item I;
+      if (code >= 0) I = decode(G, code, A.counts, A.bits);
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
       if (elect_one()) {
-        item_ring[slot] = code;
+        ring_put(slot, code, I);
         mbar_arrive(BAR(C::B_IFULL + slot));
       }
       __syncwarp();
       if (code < 0) break;
-      const Item I = decode(G, code, A.counts, A.bits);
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
       KeyChunker ck(G, I.qb, mrow, CH);
@@ -476,11 +493,11 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     while (true) {
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
-      const int32_t code = item_ring[slot];
+      Item I;
+      const int32_t code = ring_get(slot, I);
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
       if (code < 0) break;
-      const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
       if (do_s) {
         mbar_wait(BAR(C::B_QFULL), it & 1);
@@ -590,12 +607,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     while (true) {
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
-      const int32_t code = item_ring[slot];
+      Item I;
+      const int32_t code = ring_get(slot, I);
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(C::B_IEMPTY + slot));
       if (code < 0) break;
-      const Item I = decode(G, code, A.counts, A.bits);
       const int ntiles = I.nchunks;
+      if (warp == 0 && lane == 0) BSA_TR(14, it);
       {
         // this warp's 64/NG dimensions of its query row of the packed
         // partitioned Q -> TMEM (bf16 pairs: the A operand of S = Q K^T).  The
@@ -772,8 +790,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         for (int q = 0; q < NG; ++q) ltot += x_l[q * BQ + row];
         if (!EXACT) ovf |= !(ltot <= 1.2676506e30f);
       }
+      if (warp == 0 && lane == 0) BSA_TR(15, it);
       mbar_wait(BAR(C::B_OFULL), it & 1);
       tc_fence_after();
+      if (warp == 0 && lane == 0) BSA_TR(17, it);
       if constexpr (!EXACT && LSUM) {
         // row sum of P from the tensor core (O column 64); an overflowed
         // stale offset shows up as inf / a huge sum -> exact repair launch
@@ -829,6 +849,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(BAR(C::B_OEMPTY));
+      if (warp == 0 && lane == 0) BSA_TR(18, it);
       if constexpr (!EXACT) {
         // stale offset overflowed somewhere in this item: list it once for
         // the exact-max launch (which rewrites all of its rows)
