@@ -486,6 +486,8 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     // warp issues S(j + LEAD) before PV(j).
     const bool do_s = warp == C::MMA_WARP, do_pv = warp == C::PV_WARP;
     uint32_t it = 0, gs = 0, gp = 0;
+    uint32_t sk = 0, kph = 0, sb = 0, sph = 0;  // S issue: K stage, S buffer (+ phases)
+    uint32_t pb = 0, pph = 0, sv = 0, vph = 0;  // PV issue: P buffer, V stage
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
     const uint64_t dk0 = sdesc(sbase + C::OFF_K, 16, 1024);
@@ -503,25 +505,26 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         mbar_wait(BAR(C::B_QFULL), it & 1);
         tc_fence_after();
       }
+      // ring cursors (stage, phase), advanced incrementally: no div/mod on the
+      // issue path, which runs at ~1/5 of an SMSP's issue slots
       auto issue_s = [&]() {
-        const uint32_t sk = gs % NK, sb = gs % NB;
         if (lane == 0) BSA_TR(11, gs);
 #ifdef BSA_TC_TRACE_BUILD
-        mbar_wait(BAR(C::B_KFULL + sk), (gs / NK) & 1);
+        mbar_wait(BAR(C::B_KFULL + sk), kph);
         if (lane == 0) BSA_TR(3, gs);
-        mbar_wait(BAR(C::B_PFREE + sb), ((gs / NB) & 1) ^ 1);
+        mbar_wait(BAR(C::B_PFREE + sb), sph ^ 1);
         if (lane == 0) BSA_TR(13, gs);
 #else
-        mbar_wait2(BAR(C::B_KFULL + sk), (gs / NK) & 1, BAR(C::B_PFREE + sb), ((gs / NB) & 1) ^ 1);
+        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR(C::B_PFREE + sb), sph ^ 1);
 #endif
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t dk = dk0 + (uint64_t)((sk * CHUNK_BYTES) >> 4);
+          const uint64_t dk = dk0 + (uint64_t)(sk * (CHUNK_BYTES >> 4));
+          const uint32_t ds = tmem + C::TM_S + sb * 64;
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             if (BSA_TC_EXPERIMENT == 2) continue;
-            mma_ts(tmem + C::TM_S + sb * 64, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s,
-                   k > 0 ? 1u : 0u);
+            mma_ts(ds, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s, k > 0 ? 1u : 0u);
           }
           tc_commit(BAR(C::B_SFULL + sb));
           tc_commit(BAR(C::B_KEMPTY + sk));
@@ -529,29 +532,30 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
         __syncwarp();
         ++gs;
+        if (++sk == (uint32_t)NK) { sk = 0; kph ^= 1; }
+        if (++sb == (uint32_t)NB) { sb = 0; sph ^= 1; }
       };
       auto issue_pv = [&](int jj) {
-        const uint32_t sv = gp % NV, pb = gp % NB;
         if (lane == 0) BSA_TR(10, gp);
 #ifdef BSA_TC_TRACE_BUILD
-        mbar_wait(BAR(C::B_PFULL + pb), (gp / NB) & 1);
+        mbar_wait(BAR(C::B_PFULL + pb), pph);
         if (lane == 0) BSA_TR(7, gp);
-        mbar_wait(BAR(C::B_VFULL + sv), (gp / NV) & 1);
+        mbar_wait(BAR(C::B_VFULL + sv), vph);
         if (lane == 0) BSA_TR(5, gp);
 #else
-        mbar_wait2(BAR(C::B_PFULL + pb), (gp / NB) & 1, BAR(C::B_VFULL + sv), (gp / NV) & 1);
+        mbar_wait2(BAR(C::B_PFULL + pb), pph, BAR(C::B_VFULL + sv), vph);
 #endif
         if (jj == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t dv = dv0 + (uint64_t)((sv * C::V_STAGE) >> 4);
+          const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
+          const uint32_t pa = tmem + C::TM_S + pb * 64;
           // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
           // column halves: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k)
             if (BSA_TC_EXPERIMENT != 2)
-              mma_ts(tmem + C::TM_O,
-                     tmem + C::TM_S + pb * 64 + (EXACT ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
+              mma_ts(tmem + C::TM_O, pa + (EXACT ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
                      dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(C::B_PFREE + pb));
           tc_commit(BAR(C::B_VEMPTY + sv));
@@ -559,6 +563,8 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
         __syncwarp();
         ++gp;
+        if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
+        if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
       };
       if constexpr (C::SPLIT) {
         if (do_s) {
