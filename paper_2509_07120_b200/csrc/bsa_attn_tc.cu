@@ -135,30 +135,6 @@ using CfgExact = Cfg<false>;
 #ifndef BSA_TC_POLY_DEG
 #define BSA_TC_POLY_DEG 2
 #endif
-// 2^x for a pair on the FMA pipe (x < 128): round-to-nearest split
-// x = j + f, f in [-0.5, 0.5], minimax polynomial for 2^f, exponent added as
-// an integer.  Degree 3: max rel err 7.5e-5 (for fp16 P); degree 2: 1.7e-3,
-// below the 2^-9 rounding of a bf16 P, one f32x2 FMA cheaper.
-template <int DEG>
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.0f);
-  x.y = fmaxf(x.y, -126.0f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
-  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
-  float2 p;
-  if constexpr (DEG == 2) {
-    p = __ffma2_rn(make_float2(0.23842570f, 0.23842570f), f, make_float2(0.70344281f, 0.70344281f));
-    p = __ffma2_rn(p, f, make_float2(1.00044298f, 1.00044298f));
-  } else {
-    p = __ffma2_rn(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
-    p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
-    p = __ffma2_rn(p, f, make_float2(0.99992812f, 0.99992812f));
-  }
-  // (t_bits << 23) == (j << 23) mod 2^32 because t = 1.5*2^23 + j
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
 
 // P = exp2(s * scale_log2 - m) for one 32-key half row, written to TMEM as
 // packed 16-bit pairs (one tcgen05.st.32x32b.x16); returns the fp32 sum.
