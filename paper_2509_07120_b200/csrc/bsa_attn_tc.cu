@@ -929,6 +929,7 @@ static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
     case 4: return launch_variant<4, false, EXACT>(mq, mk, mv, G, a, grid, st);
     case 16: return launch_variant<0, true, EXACT>(mq, mk, mv, G, a, grid, st);
     case 18: return launch_variant<2, true, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 19: return launch_variant<3, true, EXACT>(mq, mk, mv, G, a, grid, st);
     default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
   }
 }

@@ -260,3 +260,35 @@ def test_tc_edge_geometries(bsa, oracle, frames, patches, specials, heads):
     ref = oracle.masked_attention_f64(qb, kb, vb, frames, patches, specials, mask.blocks, 128, 64)
     assert np.isfinite(out).all()
     assert _rel(out, ref) <= BF16_REL_TOL
+
+
+def test_tc_fp16_v_variant_in_subprocess():
+    """The opt-in fp16 P·V variant (BSA_TC_F16P=1: V stored as fp16 with an
+    exact per-head power-of-two scale, P in fp16) stays within the bf16
+    tolerance. The switch is read once per process, hence the subprocess."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, "tests")
+import oracle, paper_2509_07120_b200 as bsa
+from golden_inputs import make_qkv
+lay = bsa.TokenLayout(3, 300, 5)
+q, k, v = make_qkv(2, lay.total_tokens, 64, 77)
+v = v * 300.0  # exercise the per-head scale
+qd, kd, vd = (torch.from_numpy(x).to("cuda", torch.bfloat16) for x in (q, k, v))
+g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+mask = bsa.predict_mask(qd, kd, bsa.MaskPolicy(0.4, 0.8, g), layout=lay)
+out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(qd, kd, vd), lay, mask))
+qb, kb, vb = (t.float().cpu().numpy() for t in (qd, kd, vd))
+ref = oracle.masked_attention_f64(qb, kb, vb, 3, 300, 5, mask.blocks, 128, 64)
+err = np.abs(out.float().cpu().numpy() - ref).max() / np.abs(ref).max()
+print(err)
+assert err <= 2e-2, err
+'''
+    import os
+    env = dict(os.environ, BSA_TC_F16P="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
