@@ -99,6 +99,39 @@ class GlobalAttentionStack:
 
     __call__ = forward
 
+    def layer_statistics(self, x: torch.Tensor, layout: TokenLayout,
+                         policy: MaskPolicy | None = None, mode: str = "sparse") -> list[dict]:
+        """The paper's per-layer attention analysis (§4.x "Visualizing
+        Attention Maps": mean / max attention of the special/patch quadrants
+        against layer index), streamed on the GPU without any T x T map
+        (analysis.py). With a policy, each layer also reports the mean
+        fraction of patch attention mass its predicted mask keeps
+        (mask_recall), the per-layer tau/rho selection signal. The stack runs
+        forward in `mode` while the statistics are taken."""
+        from .analysis import attention_quadrant_stats, block_attention_map, mask_recall
+
+        if x.shape != (layout.total_tokens, self.dim):
+            raise ValueError(f"x must be ({layout.total_tokens}, {self.dim}), got {tuple(x.shape)}")
+        T, C = x.shape
+        H, d = self.heads, self.head_dim
+        rows = []
+        for i, blk in enumerate(self.blocks):
+            h = F.layer_norm(x, (C,), blk.ln_w, blk.ln_b)
+            qkv = F.linear(h, blk.qkv_w, blk.qkv_b).view(T, 3, H, d).permute(1, 2, 0, 3)
+            inp = AttentionInputs(qkv[0], qkv[1], qkv[2])
+            st = attention_quadrant_stats(inp, layout)
+            row = {"layer": i, "means": st.means, "maxes": st.maxes}
+            if policy is not None:
+                mask = predict_mask(qkv[0], qkv[1], policy, layout=layout)
+                row["recall"] = float(mask_recall(block_attention_map(inp, layout), mask).mean())
+            rows.append(row)
+            x = x + self.attention(x, blk, layout, policy, mode)
+            if blk.mlp is not None:
+                lw, lb, w1, b1, w2, b2 = blk.mlp
+                hm = F.layer_norm(x, (self.dim,), lw, lb)
+                x = x + F.linear(F.gelu(F.linear(hm, w1, b1)), w2, b2)
+        return rows
+
 
 def policy_for(layout: TokenLayout, tau: float, rho: float, block_q: int = 128,
                block_k: int = 64) -> MaskPolicy:

@@ -36,3 +36,32 @@ def test_stack_sparse_runs_and_validates():
         stack(x[:-1], lay, policy_for(lay, 0.4, 0.8), "sparse")
     with pytest.raises(ValueError):
         stack(x, lay, None, "sparse")
+
+
+def test_layer_statistics_match_materialised_maps():
+    """Per-layer streamed quadrant stats equal quadrant_stats of the dense
+    map of the same layer's q/k (small N, 3 layers)."""
+    import numpy as np
+    import torch
+    import torch.nn.functional as F
+    import paper_2509_07120_b200 as bsa
+    from paper_2509_07120_b200.analysis import quadrant_stats
+    from paper_2509_07120_b200.stack import GlobalAttentionStack, policy_for
+
+    lay = bsa.TokenLayout(2, 300, 5)
+    st = GlobalAttentionStack(layers=3, seed=1)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.randn((lay.total_tokens, st.dim), generator=g, device="cuda").to(torch.bfloat16)
+    rows = st.layer_statistics(x, lay, policy_for(lay, 0.0, 0.75), mode="dense")
+    assert [r["layer"] for r in rows] == [0, 1, 2]
+    T, C = x.shape
+    for r, blk in zip(rows, st.blocks):
+        h = F.layer_norm(x, (C,), blk.ln_w, blk.ln_b)
+        qkv = F.linear(h, blk.qkv_w, blk.qkv_b).view(T, 3, 16, 64).permute(1, 2, 0, 3)
+        s = torch.matmul(qkv[0].float(), qkv[1].float().transpose(1, 2)) * 0.125
+        ref = quadrant_stats(torch.softmax(s.double(), dim=-1).float(), lay)
+        for quad in ref.means:
+            np.testing.assert_allclose(r["means"][quad], ref.means[quad], rtol=2e-3)
+            np.testing.assert_allclose(r["maxes"][quad], ref.maxes[quad], rtol=2e-3)
+        assert 0.0 < r["recall"] <= 1.0
+        x = x + st.attention(x, blk, lay, None, "dense")
