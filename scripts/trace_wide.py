@@ -38,7 +38,7 @@ if (t[[5, 6, 7, 9, 10, 11]] > 0).all(axis=0).sum() > 60:
           ' -> PV issued', med(v[2] - v[5]))
     print('V(j) TMA issued -> VFULL passed', med(v[5] - v[6]))
 if (t[13] > 0).sum() > 60:
-    nb = 8
+    nb = 6
     print(f'S warp: KFULL passed -> PFREE passed {med(v[13] - v[3]):.0f};  PV(j-{nb}) issued -> PFREE seen by S(j) {med(v[13][nb:] - v[2][:-nb]):.0f}')
     print(f'S(j) issue vs P(j-{nb}) published {med(v[1][nb:] - v[16][:-nb]):.0f};  S(j) issued vs P(j-4) published {med(v[1][4:] - v[16][:-4]):.0f}')
     print('S warp loop: S(j) issued -> S(j+1) issued', med(np.diff(v[1])))
