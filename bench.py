@@ -23,7 +23,12 @@ Multi-GPU (torchrun, NCCL), timing is the max over ranks:
                      (paper_2509_07120_b200/shard.py): frame-sharded Q/K/V,
                      NCCL all-gather of Q/K/V, row-split scoring + mask
                      all-gather, LPT-sharded attention, sum all-reduce
-                     ("scaling": "strong").
+                     ("scaling": "strong").  --combine scatter replaces the
+                     all-reduce with the attention epilogue storing rows
+                     into the owning rank's buffer over NVLink (CUDA IPC).
+
+The e2e leg runs the same layer from pinned host memory through
+pipeline.HostLayerPipeline (H2D / kernels / D2H overlapped per head chunk).
 """
 
 from __future__ import annotations
