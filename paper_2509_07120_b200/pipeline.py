@@ -96,15 +96,19 @@ class HostLayerPipeline:
         self.s_in.wait_stream(comp)
         for a, b in chunks:
             with torch.cuda.stream(self.s_in):
+                # Q and K first: scoring can start while V is still in flight
                 dq[a:b].copy_(q[a:b], non_blocking=True)
                 dk[a:b].copy_(k[a:b], non_blocking=True)
+                ev_qk = torch.cuda.Event()
+                ev_qk.record(self.s_in)
                 dv[a:b].copy_(v[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(self.s_in)
-                done_in.append(ev)
-        for (a, b), ev_in in zip(chunks, done_in):
-            comp.wait_event(ev_in)
+                ev_v = torch.cuda.Event()
+                ev_v.record(self.s_in)
+                done_in.append((ev_qk, ev_v))
+        for (a, b), (ev_qk, ev_v) in zip(chunks, done_in):
+            comp.wait_event(ev_qk)
             mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout)
+            comp.wait_event(ev_v)
             job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b]), layout, mask)
             sparse_attention(job, out=self.obuf[a:b])
             ev = torch.cuda.Event()
