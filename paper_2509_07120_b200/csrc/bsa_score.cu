@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
       }
     }
     __syncthreads();
+#pragma unroll 8
     for (int c = 0; c < kc; ++c) {
       const float4 qa = *reinterpret_cast<const float4*>(&qs[c][tr * 8]);
       const float4 qb = *reinterpret_cast<const float4*>(&qs[c][tr * 8 + 4]);
