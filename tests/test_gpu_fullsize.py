@@ -87,3 +87,37 @@ def test_config5_single_gpu_leg_n1000(bsa):
     out = bsa.sparse_attention(job)
     _check_rows(bsa, lay, q, k, v, mask, out, heads=(1,))
     assert torch.equal(bsa.sparse_attention(job), out)
+
+
+def test_cdf_policy_full_size_mask_exact(bsa):
+    """tau > 0 (the CDF branch with the exact fixed-point mass search) at the
+    bench size: head 3's whole mask bit-exact against the C oracle."""
+    import torch
+    lay, q, k, _ = _inputs(bsa, 200, 4, 2)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    pol = bsa.MaskPolicy(0.4, 0.8, g)
+    mask = bsa.predict_mask(q, k, pol, layout=lay)
+    assert bool((mask.device_counts() >= pol.min_blocks).all())
+    pidx = torch.from_numpy(bsa.patch_token_indices(lay)).cuda()
+    qp, kp = (t[3:4, pidx].float().cpu().numpy() for t in (q, k))
+    om, oc = oracle.predict_mask(qp, kp, 128, 64, 0.4, 0.8)
+    assert np.array_equal(om[0], mask.blocks[3])
+
+
+def test_pi3_shape_n300(bsa):
+    """Config 4: pi3-shaped layer, 4 register tokens per frame, N=300."""
+    import torch
+    lay = bsa.TokenLayout(300, 1369, 4)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn((2, lay.total_tokens, 64), generator=gen, device="cuda")
+               .to(torch.bfloat16) for _ in range(3))
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    pol = bsa.MaskPolicy(0.0, 0.75, g)
+    mask = bsa.predict_mask(q, k, pol, layout=lay)
+    assert bool((mask.device_counts() == pol.min_blocks).all())
+    pidx = torch.from_numpy(bsa.patch_token_indices(lay)).cuda()
+    qp, kp = (t[0:1, pidx].float().cpu().numpy() for t in (q, k))
+    om, _ = oracle.predict_mask(qp, kp, 128, 64, 0.0, 0.75)
+    assert np.array_equal(om[0], mask.blocks[0])
+    out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask))
+    _check_rows(bsa, lay, q, k, v, mask, out, heads=(0,))
