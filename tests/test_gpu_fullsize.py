@@ -121,3 +121,17 @@ def test_pi3_shape_n300(bsa):
     assert np.array_equal(om[0], mask.blocks[0])
     out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask))
     _check_rows(bsa, lay, q, k, v, mask, out, heads=(0,))
+
+
+def test_host_pipeline_full_size_equals_device_path(bsa):
+    """bench.py's e2e leg: the head-chunked host-memory pipeline at N=200, 16
+    heads gives exactly the device-resident result."""
+    import torch
+    from paper_2509_07120_b200.pipeline import HostLayerPipeline
+    lay, q, k, v = _inputs(bsa, 200, 16, 0)
+    pol = bsa.MaskPolicy(0.0, 0.75, bsa.BlockGeometry(lay.patch_tokens, 128, 64))
+    mask = bsa.predict_mask(q, k, pol, layout=lay)
+    ref = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask))
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    out = HostLayerPipeline(16, lay.total_tokens, 64).run(hq, hk, hv, lay, pol)
+    assert torch.equal(out, ref.cpu())
