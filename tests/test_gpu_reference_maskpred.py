@@ -139,3 +139,19 @@ def test_predict_mask_shapes_and_token_check(bsa):
     q = rng.standard_normal((1, 100, 8)).astype(np.float32)
     with pytest.raises(ValueError, match="patch tokens"):
         bsa.predict_mask(q, q, bsa.MaskPolicy(0.5, 0.5, _geom(bsa, 99)))
+
+
+def test_row_softmax_reference_cases(bsa):
+    """test_tensorio.py TestRowSoftmax of the reference."""
+    np.testing.assert_allclose(bsa.row_softmax(np.zeros((1, 4), np.float32)), [[0.25] * 4],
+                               atol=1e-7)
+    out = bsa.row_softmax(np.array([[1000.0, 0.0]], np.float32))
+    np.testing.assert_allclose(out, [[1.0, 0.0]], atol=1e-6)
+    assert np.isfinite(out).all()
+    rng = np.random.default_rng(3)
+    out = bsa.row_softmax(rng.standard_normal((4, 6)).astype(np.float32), scale=0.37)
+    np.testing.assert_allclose(out.sum(axis=1), np.ones(4), atol=1e-6)
+    assert (out >= 0).all() and (out <= 1).all()
+    expected = np.exp([6.0, 0.0]) / np.exp([6.0, 0.0]).sum()
+    np.testing.assert_allclose(bsa.row_softmax(np.array([[2.0, 0.0]], np.float32), scale=3.0)[0],
+                               expected, atol=1e-6)
