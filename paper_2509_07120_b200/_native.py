@@ -149,8 +149,23 @@ def check(rc: int, what: str):
     raise RuntimeError(f"{what}: {msg}")
 
 
-def stream_ptr() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def stream_ptr(device=None) -> int:
+    """The current stream of `device` (default: the current device)."""
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def on_device(device):
+    """Make `device` current for a launch: kernels run on the device that
+    holds the tensors, never on whichever device happens to be current."""
+    return torch.cuda.device(device)
+
+
+def all_finite(*tensors: torch.Tensor) -> bool:
+    """True when no element of the (device) tensors is NaN or +-inf: one
+    min/max reduction per tensor (no full-size temporaries), one sync.  The
+    reference's as_f32 rejects non-finite inputs (tensorio.py:47-59)."""
+    ext = [torch.stack(torch.aminmax(t.detach())).float() for t in tensors]
+    return bool(torch.isfinite(torch.cat(ext)).all())
 
 
 def ptr(t) -> int | None:

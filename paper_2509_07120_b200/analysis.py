@@ -84,10 +84,11 @@ def attention_row_stats(inp: AttentionInputs, layout: TokenLayout) -> torch.Tens
     out = torch.empty((H, T, 5), dtype=torch.float32, device=q.device)
     ws = _workspace(layout, H, q.device)
     L = N.lib()
-    N.check(L.bsa_attention_row_stats(N.tensor_desc(q), N.tensor_desc(k), N.layout_desc(layout),
-                                      float(np.float32(inp.scale)), out.data_ptr(),
-                                      ws.data_ptr(), ws.numel(), N.stream_ptr()),
-            "attention_row_stats")
+    with N.on_device(q.device):
+        N.check(L.bsa_attention_row_stats(N.tensor_desc(q), N.tensor_desc(k),
+                                          N.layout_desc(layout), float(np.float32(inp.scale)),
+                                          out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                          N.stream_ptr()), "attention_row_stats")
     return out
 
 
@@ -106,10 +107,11 @@ def block_attention_map(inp: AttentionInputs, layout: TokenLayout, row_stats=Non
     out = torch.empty((H, nq, nk), dtype=torch.float32, device=q.device)
     ws = _workspace(layout, H, q.device)
     L = N.lib()
-    N.check(L.bsa_block_attention_map(N.tensor_desc(q), N.tensor_desc(k), N.layout_desc(layout),
-                                      float(np.float32(inp.scale)), row_stats.data_ptr(),
-                                      out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
-            "block_attention_map")
+    with N.on_device(q.device):
+        N.check(L.bsa_block_attention_map(N.tensor_desc(q), N.tensor_desc(k),
+                                          N.layout_desc(layout), float(np.float32(inp.scale)),
+                                          row_stats.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                          ws.numel(), N.stream_ptr()), "block_attention_map")
     return out.cpu().numpy() if inp.numpy_io else out
 
 

@@ -23,13 +23,13 @@ from . import _native as N
 DEFAULT_MAP_ELEMENT_CAP = 2**31
 
 
-def _as_input(x, name: str, dev):
+def _as_input(x, name: str, dev, validate: bool):
     if isinstance(x, torch.Tensor):
         t = x
         if t.dtype not in (torch.float32, torch.bfloat16):
             t = t.float()
         if t.device.type != "cuda":
-            if not torch.isfinite(t).all():
+            if validate and not torch.isfinite(t).all():
                 raise ValueError(f"{name} contains non-finite values")
             t = t.to(dev)
         return t, False
@@ -38,19 +38,25 @@ def _as_input(x, name: str, dev):
         raise ValueError(f"{name} must have at least one dimension")
     if min(a.shape) < 1:
         raise ValueError(f"{name} has a zero-sized dimension: {a.shape}")
-    if not np.isfinite(a).all():
+    if validate and not np.isfinite(a).all():
         raise ValueError(f"{name} contains non-finite values")
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev), True
 
 
 class AttentionInputs:
-    """Per-head query/key/value tensors of shape (heads, tokens, head_dim)."""
+    """Per-head query/key/value tensors of shape (heads, tokens, head_dim).
 
-    def __init__(self, q, k, v):
+    Like the reference (dense.py:20-55, as_f32 on each of q/k/v) it rejects
+    non-finite values; for device tensors the scan is one min/max reduction
+    per tensor, skipped with ``validate=False`` by callers that already
+    validated.  Mixed dtypes are promoted to fp32 (the reference makes all
+    three fp32)."""
+
+    def __init__(self, q, k, v, *, validate: bool = True):
         dev = N.require_cuda()
-        self.q, np_in = _as_input(q, "q", dev)
-        self.k, _ = _as_input(k, "k", dev)
-        self.v, _ = _as_input(v, "v", dev)
+        self.q, np_in = _as_input(q, "q", dev, validate)
+        self.k, _ = _as_input(k, "k", dev, validate)
+        self.v, _ = _as_input(v, "v", dev, validate)
         self.numpy_io = np_in
         for name, t in (("q", self.q), ("k", self.k), ("v", self.v)):
             if t.dim() != 3:
@@ -62,8 +68,16 @@ class AttentionInputs:
         if not (self.q.shape == self.k.shape == self.v.shape):
             raise ValueError(f"q/k/v shapes differ: {tuple(self.q.shape)}, "
                              f"{tuple(self.k.shape)}, {tuple(self.v.shape)}")
+        if not (self.q.device == self.k.device == self.v.device):
+            raise ValueError(f"q/k/v live on different devices: {self.q.device}, "
+                             f"{self.k.device}, {self.v.device}")
         if not (self.q.dtype == self.k.dtype == self.v.dtype):
-            raise ValueError("q/k/v dtypes differ")
+            self.q, self.k, self.v = self.q.float(), self.k.float(), self.v.float()
+        on_dev = [t for x, t in zip((q, k, v), (self.q, self.k, self.v))
+                  if isinstance(x, torch.Tensor) and x.device.type == "cuda"]
+        if validate and on_dev:
+            if not N.all_finite(*on_dev):
+                raise ValueError("q/k/v contain non-finite values")
 
     @property
     def heads(self) -> int:

@@ -31,8 +31,12 @@ _MASK_HEADER_SIZE = struct.calcsize(_MASK_HEADER_FMT)
 # ---------------------------------------------------------------------------
 # input plumbing
 # ---------------------------------------------------------------------------
-def _to_device(x, name: str, allow_bf16: bool = True):
-    """-> (contiguous-last-dim CUDA tensor, came_from_numpy)."""
+def _to_device(x, name: str, allow_bf16: bool = True, validate: bool = True):
+    """-> (contiguous-last-dim CUDA tensor, came_from_numpy).
+
+    validate: reject NaN/inf like the reference's as_f32 (tensorio.py:47-59)
+    for every input, device tensors included (one min/max reduction and one
+    sync per tensor; callers that validated already pass False)."""
     dev = N.require_cuda()
     if isinstance(x, torch.Tensor):
         t = x
@@ -43,9 +47,11 @@ def _to_device(x, name: str, allow_bf16: bool = True):
         if t.dtype not in ((torch.float32, torch.bfloat16) if allow_bf16 else (torch.float32,)):
             t = t.float()
         if t.device.type != "cuda":
-            if not torch.isfinite(t).all():
+            if validate and not torch.isfinite(t).all():
                 raise ValueError(f"{name} contains non-finite values")
             t = t.to(dev)
+        elif validate and not N.all_finite(t):
+            raise ValueError(f"{name} contains non-finite values")
         if t.stride(-1) != 1:
             t = t.contiguous()
         return t, False
@@ -54,7 +60,7 @@ def _to_device(x, name: str, allow_bf16: bool = True):
         raise ValueError(f"{name} must have at least one dimension")
     if min(a.shape) < 1:
         raise ValueError(f"{name} has a zero-sized dimension: {a.shape}")
-    if not np.isfinite(a).all():
+    if validate and not np.isfinite(a).all():
         raise ValueError(f"{name} contains non-finite values")
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev), True
 
@@ -144,9 +150,10 @@ class BlockMask:
         g = self.geometry
         bits = self.device_bits()
         area = torch.empty(self._heads, dtype=torch.int64, device=bits.device)
-        N.check(N.lib().bsa_mask_selected_area(bits.data_ptr(), self._heads, g.patch_tokens,
-                                               g.block_q, g.block_k, area.data_ptr(),
-                                               N.stream_ptr()), "selected_area")
+        with N.on_device(bits.device):
+            N.check(N.lib().bsa_mask_selected_area(bits.data_ptr(), self._heads, g.patch_tokens,
+                                                   g.block_q, g.block_k, area.data_ptr(),
+                                                   N.stream_ptr()), "selected_area")
         return area.cpu().numpy()
 
     def achieved_sparsity(self) -> np.ndarray:
@@ -157,15 +164,24 @@ class BlockMask:
 
     # -- device views --------------------------------------------------------
     def device_bits(self, device=None) -> torch.Tensor:
-        """(heads*nq, ceil(nk/8)) uint8 on the GPU, .bsm row layout."""
+        """(heads*nq, ceil(nk/8)) uint8 on the GPU, .bsm row layout.  With
+        `device`, the bits are moved there (and cached there) if they live
+        on another GPU."""
         if self._bits is None:
             dev = device or N.require_cuda()
             g = self.geometry
             packed = np.packbits(self._blocks.reshape(-1, g.nk_blocks), axis=1, bitorder="little")
             self._bits = torch.from_numpy(np.ascontiguousarray(packed)).to(dev)
+        elif device is not None and self._bits.device != torch.device(device):
+            self._bits = self._bits.to(device)
+            if self._counts is not None:
+                self._counts = self._counts.to(device)
         return self._bits
 
-    def device_counts(self) -> torch.Tensor | None:
+    def device_counts(self, device=None) -> torch.Tensor | None:
+        if device is not None and self._counts is not None and \
+                self._counts.device != torch.device(device):
+            self._counts = self._counts.to(device)
         return self._counts
 
     def csr(self):
@@ -178,33 +194,37 @@ class BlockMask:
         row_ptr = torch.empty(rows + 1, dtype=torch.int32, device=bits.device)
         nnz = int(np.unpackbits(bits.cpu().numpy(), axis=1, bitorder="little")[:, : g.nk_blocks].sum())
         col_idx = torch.empty(max(nnz, 1), dtype=torch.int32, device=bits.device)
-        N.check(L.bsa_mask_to_csr(bits.data_ptr(), self._heads, g.nq_blocks, g.nk_blocks,
-                                  row_ptr.data_ptr(), col_idx.data_ptr(), ws.data_ptr(),
-                                  ws.numel(), N.stream_ptr()), "mask_to_csr")
+        with N.on_device(bits.device):
+            N.check(L.bsa_mask_to_csr(bits.data_ptr(), self._heads, g.nq_blocks, g.nk_blocks,
+                                      row_ptr.data_ptr(), col_idx.data_ptr(), ws.data_ptr(),
+                                      ws.numel(), N.stream_ptr()), "mask_to_csr")
         return row_ptr, col_idx[:nnz]
 
 
 # ---------------------------------------------------------------------------
 # operators
 # ---------------------------------------------------------------------------
-def block_pool(x, block: int):
+def block_pool(x, block: int, *, validate: bool = True):
     """Average-pool (heads, tokens, dim) over token blocks (maskpred.py:104-120)."""
-    t, was_np = _to_device(x, "x")
+    t, was_np = _to_device(x, "x", validate=validate)
     if t.dim() != 3:
         raise ValueError(f"block_pool expects (heads, tokens, dim), got {tuple(t.shape)}")
     if block < 1:
         raise ValueError(f"block size must be >= 1, got {block}")
     h, n, d = t.shape
     out = torch.empty((h, -(-n // block), d), dtype=torch.float32, device=t.device)
-    N.check(N.lib().bsa_block_pool(N.tensor_desc(t), None, int(block), out.data_ptr(),
-                                   N.stream_ptr()), "block_pool")
+    with N.on_device(t.device):
+        N.check(N.lib().bsa_block_pool(N.tensor_desc(t), None, int(block), out.data_ptr(),
+                                       N.stream_ptr()), "block_pool")
     return _out(out, was_np)
 
 
-def pooled_scores(q_pooled, k_pooled, head_dim: int):
+def pooled_scores(q_pooled, k_pooled, head_dim: int, *, validate: bool = True):
     """Softmaxed pooled similarity (heads, nq, nk) (maskpred.py:123-139)."""
-    qp, was_np = _to_device(q_pooled, "q_pooled", allow_bf16=False)
-    kp, _ = _to_device(k_pooled, "k_pooled", allow_bf16=False)
+    qp, was_np = _to_device(q_pooled, "q_pooled", allow_bf16=False, validate=validate)
+    kp, _ = _to_device(k_pooled, "k_pooled", allow_bf16=False, validate=validate)
+    if kp.device != qp.device:
+        raise ValueError(f"q_pooled on {qp.device} but k_pooled on {kp.device}")
     if qp.dim() != 3 or kp.dim() != 3:
         raise ValueError(f"pooled tensors must be 3-D, got {tuple(qp.shape)} and {tuple(kp.shape)}")
     if qp.shape[0] != kp.shape[0] or qp.shape[2] != kp.shape[2]:
@@ -216,17 +236,18 @@ def pooled_scores(q_pooled, k_pooled, head_dim: int):
     out = torch.empty((h, nq, nk), dtype=torch.float32, device=qp.device)
     L = N.lib()
     ws = N.workspace(L.bsa_pooled_scores_workspace(h, nq, nk), qp.device)
-    N.check(L.bsa_pooled_scores(qp.data_ptr(), kp.data_ptr(), h, nq, nk, d, float(scale),
-                                out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
-            "pooled_scores")
+    with N.on_device(qp.device):
+        N.check(L.bsa_pooled_scores(qp.data_ptr(), kp.data_ptr(), h, nq, nk, d, float(scale),
+                                    out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
+                "pooled_scores")
     return _out(out, was_np)
 
 
-def select_blocks(scores, policy: MaskPolicy) -> BlockMask:
+def select_blocks(scores, policy: MaskPolicy, *, validate: bool = True) -> BlockMask:
     """Per (head, q-block) row: rank blocks by probability (ties -> lower
     index), shortest prefix reaching tau, extended to the rho floor
     (maskpred.py:142-174)."""
-    s, _ = _to_device(scores, "scores", allow_bf16=False)
+    s, _ = _to_device(scores, "scores", allow_bf16=False, validate=validate)
     if s.dim() != 3:
         raise ValueError(f"scores must be (heads, nq, nk), got {tuple(s.shape)}")
     g = policy.geometry
@@ -240,23 +261,27 @@ def select_blocks(scores, policy: MaskPolicy) -> BlockMask:
     bits = torch.empty((h * nq, -(-nk // 8)), dtype=torch.uint8, device=s.device)
     counts = torch.empty(h * nq, dtype=torch.int32, device=s.device)
     ws = N.workspace(L.bsa_select_workspace(h, nq, nk), s.device)
-    N.check(L.bsa_select_blocks(s.data_ptr(), h, nq, nk, float(policy.tau), policy.min_blocks,
-                                bits.data_ptr(), counts.data_ptr(), ws.data_ptr(), ws.numel(),
-                                N.stream_ptr()), "select_blocks")
+    with N.on_device(s.device):
+        N.check(L.bsa_select_blocks(s.data_ptr(), h, nq, nk, float(policy.tau),
+                                    policy.min_blocks, bits.data_ptr(), counts.data_ptr(),
+                                    ws.data_ptr(), ws.numel(), N.stream_ptr()), "select_blocks")
     return BlockMask._from_device(bits, counts, h, g)
 
 
 def predict_mask(q_patches, k_patches, policy: MaskPolicy, *, layout: TokenLayout | None = None,
-                 return_probs: bool = False):
+                 return_probs: bool = False, validate: bool = True):
     """Pool, score and select in one device pass (maskpred.py:177-194).
 
     Inputs are (heads, patch_tokens, head_dim) patch-only tensors, exactly as
     the reference.  Extension: with ``layout=`` they may instead be the full
     interleaved sequences; the patch gather is then folded into the kernels'
-    addressing (no copy).
+    addressing (no copy).  ``validate=False`` skips the non-finite scan of
+    the inputs (as_f32, tensorio.py:47-59) for callers that already did it.
     """
-    q, _ = _to_device(q_patches, "q_patches")
-    k, _ = _to_device(k_patches, "k_patches")
+    q, _ = _to_device(q_patches, "q_patches", validate=validate)
+    k, _ = _to_device(k_patches, "k_patches", validate=validate)
+    if k.device != q.device:
+        raise ValueError(f"q on {q.device} but k on {k.device}")
     g = policy.geometry
     expect = layout.total_tokens if layout is not None else g.patch_tokens
     if layout is not None and layout.patch_tokens != g.patch_tokens:
@@ -268,7 +293,8 @@ def predict_mask(q_patches, k_patches, policy: MaskPolicy, *, layout: TokenLayou
     if q.shape != k.shape:
         raise ValueError(f"q/k shapes differ: {tuple(q.shape)} vs {tuple(k.shape)}")
     if q.dtype != k.dtype:
-        k = k.to(q.dtype)
+        # promote like the reference (as_f32 makes both fp32, tensorio.py:47-59)
+        q, k = q.float(), k.float()
     h, _, d = q.shape
     L = N.lib()
     nq, nk = g.nq_blocks, g.nk_blocks
@@ -279,10 +305,11 @@ def predict_mask(q_patches, k_patches, policy: MaskPolicy, *, layout: TokenLayou
                      q.device)
     scale = np.float32(1.0 / float(np.sqrt(d)))
     lay = N.layout_desc(layout) if layout is not None else None
-    N.check(L.bsa_predict_mask(N.tensor_desc(q), N.tensor_desc(k), lay, g.block_q, g.block_k,
-                               float(scale), float(policy.tau), policy.min_blocks, bits.data_ptr(),
-                               counts.data_ptr(), N.ptr(probs), ws.data_ptr(), ws.numel(),
-                               N.stream_ptr()), "predict_mask")
+    with N.on_device(q.device):
+        N.check(L.bsa_predict_mask(N.tensor_desc(q), N.tensor_desc(k), lay, g.block_q, g.block_k,
+                                   float(scale), float(policy.tau), policy.min_blocks,
+                                   bits.data_ptr(), counts.data_ptr(), N.ptr(probs),
+                                   ws.data_ptr(), ws.numel(), N.stream_ptr()), "predict_mask")
     mask = BlockMask._from_device(bits, counts, h, g)
     if return_probs:
         return mask, probs

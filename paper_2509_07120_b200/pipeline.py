@@ -74,10 +74,16 @@ class HostLayerPipeline:
         self.s_out = torch.cuda.Stream(self.device)
 
     def run(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: TokenLayout,
-            policy: MaskPolicy, out: torch.Tensor | None = None, return_masks: bool = False):
+            policy: MaskPolicy, out: torch.Tensor | None = None, return_masks: bool = False,
+            validate: bool = True):
         """q, k, v: host (ideally pinned) (H, T, d) tensors in interleaved
         token order. Returns the host output (and the per-chunk masks).
-        The call is synchronous: the output is complete on return."""
+        The call is synchronous: the output is complete on return.
+
+        validate: reject non-finite inputs like the reference's as_f32
+        (tensorio.py:47-59). The scan runs on the device copy of each chunk,
+        asynchronously, and is checked once at the end (a host scan of the
+        pinned buffers, or a sync per chunk, would stall the pipeline)."""
         for name, t in (("q", q), ("k", k), ("v", v)):
             if tuple(t.shape) != self.shape or t.dtype != self.dtype:
                 raise ValueError(f"{name} must be {self.shape} {self.dtype}, got "
@@ -90,6 +96,7 @@ class HostLayerPipeline:
         dq, dk, dv = self.bufs
         comp = torch.cuda.current_stream(self.device)
         masks = []
+        extrema = []
         done_in, done_comp = [], []
         chunks = self.chunks
         # the copy-in stream must not overwrite buffers a previous call still reads
@@ -107,9 +114,12 @@ class HostLayerPipeline:
                 done_in.append((ev_qk, ev_v))
         for (a, b), (ev_qk, ev_v) in zip(chunks, done_in):
             comp.wait_event(ev_qk)
-            mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout)
+            mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout, validate=False)
             comp.wait_event(ev_v)
-            job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b]), layout, mask)
+            if validate:
+                extrema += [torch.stack(torch.aminmax(x[a:b])).float() for x in (dq, dk, dv)]
+            job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b], validate=False),
+                                     layout, mask)
             sparse_attention(job, out=self.obuf[a:b])
             ev = torch.cuda.Event()
             ev.record(comp)
@@ -121,6 +131,8 @@ class HostLayerPipeline:
                 out[a:b].copy_(self.obuf[a:b], non_blocking=True)
         comp.wait_stream(self.s_out)
         torch.cuda.current_stream(self.device).synchronize()
+        if validate and not bool(torch.isfinite(torch.cat(extrema)).all()):
+            raise ValueError("q/k/v contain non-finite values")
         return (out, masks) if return_masks else out
 
 

@@ -111,8 +111,9 @@ class DeviceOps:
         h, _, d = x.shape
         n = layout.patch_tokens
         out = torch.empty((h, -(-n // block), d), dtype=torch.float32, device=x.device)
-        N.check(N.lib().bsa_block_pool(N.tensor_desc(x), N.layout_desc(layout), int(block),
-                                       out.data_ptr(), N.stream_ptr()), "block_pool")
+        with N.on_device(x.device):
+            N.check(N.lib().bsa_block_pool(N.tensor_desc(x), N.layout_desc(layout), int(block),
+                                           out.data_ptr(), N.stream_ptr()), "block_pool")
         return out
 
     def score_rows(self, qp_rows: torch.Tensor, kp: torch.Tensor, head_dim: int,
@@ -131,14 +132,16 @@ class DeviceOps:
         L = N.lib()
         scale = np.float32(1.0 / float(np.sqrt(head_dim)))
         probs = torch.empty((h, nr, nk), dtype=torch.float32, device=qp_rows.device)
-        ws = N.workspace(L.bsa_pooled_scores_workspace(h, nr, nk), qp_rows.device)
-        N.check(L.bsa_pooled_scores(qp_rows.data_ptr(), kp.data_ptr(), h, nr, nk, d, float(scale),
-                                    probs.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
-                "pooled_scores")
-        ws = N.workspace(L.bsa_select_workspace(h, nr, nk), qp_rows.device)
-        N.check(L.bsa_select_blocks(probs.data_ptr(), h, nr, nk, float(policy.tau),
-                                    policy.min_blocks, bits.data_ptr(), counts.data_ptr(),
-                                    ws.data_ptr(), ws.numel(), N.stream_ptr()), "select_blocks")
+        with N.on_device(qp_rows.device):
+            ws = N.workspace(L.bsa_pooled_scores_workspace(h, nr, nk), qp_rows.device)
+            N.check(L.bsa_pooled_scores(qp_rows.data_ptr(), kp.data_ptr(), h, nr, nk, d,
+                                        float(scale), probs.data_ptr(), ws.data_ptr(), ws.numel(),
+                                        N.stream_ptr()), "pooled_scores")
+            ws = N.workspace(L.bsa_select_workspace(h, nr, nk), qp_rows.device)
+            N.check(L.bsa_select_blocks(probs.data_ptr(), h, nr, nk, float(policy.tau),
+                                        policy.min_blocks, bits.data_ptr(), counts.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), N.stream_ptr()),
+                    "select_blocks")
         return bits, counts
 
     def attend_scatter(self, q, k, v, layout: TokenLayout, mask: BlockMask, shard: int,
@@ -148,7 +151,7 @@ class DeviceOps:
         from .dense import AttentionInputs
 
         g = mask.geometry
-        inp = AttentionInputs(q, k, v)
+        inp = AttentionInputs(q, k, v, validate=False)
         L = N.lib()
         lay = N.layout_desc(layout)
         need = L.bsa_sparse_attention_workspace(lay, q.shape[0], q.shape[2], g.block_q,
@@ -156,12 +159,13 @@ class DeviceOps:
         ws = N.workspace(need, q.device)
         ptrs = target.chunk_ptrs(head0)
         sc = N.BsaScatter(target.world, ptrs.data_ptr(), target.token_begin.data_ptr())
-        counts = mask.device_counts()
-        N.check(L.bsa_sparse_attention_scatter(
-            N.tensor_desc(inp.q), N.tensor_desc(inp.k), N.tensor_desc(inp.v), lay, g.block_q,
-            g.block_k, mask.device_bits(q.device).data_ptr(), N.ptr(counts),
-            float(np.float32(inp.scale)), int(shard), int(num_shards), 0, sc, ws.data_ptr(),
-            ws.numel(), N.stream_ptr()), "sparse_attention_scatter")
+        counts = mask.device_counts(q.device)
+        with N.on_device(q.device):
+            N.check(L.bsa_sparse_attention_scatter(
+                N.tensor_desc(inp.q), N.tensor_desc(inp.k), N.tensor_desc(inp.v), lay, g.block_q,
+                g.block_k, mask.device_bits(q.device).data_ptr(), N.ptr(counts),
+                float(np.float32(inp.scale)), int(shard), int(num_shards), 0, sc, ws.data_ptr(),
+                ws.numel(), N.stream_ptr()), "sparse_attention_scatter")
 
     def attend(self, q, k, v, layout: TokenLayout, mask: BlockMask, shard: int,
                num_shards: int) -> torch.Tensor:
@@ -169,7 +173,8 @@ class DeviceOps:
         from .sparse import SparseAttentionJob, sparse_attention
 
         out = torch.zeros(q.shape, dtype=q.dtype, device=q.device)
-        job = SparseAttentionJob(AttentionInputs(q, k, v), layout, mask)
+        # inputs were validated once by sharded_sparse_attention
+        job = SparseAttentionJob(AttentionInputs(q, k, v, validate=False), layout, mask)
         return sparse_attention(job, shard=shard, num_shards=num_shards, out=out)
 
 
@@ -221,6 +226,22 @@ class ScatterTarget:
         self.local = torch.as_tensor(
             _DevBuf(self._own, (heads, self.rows[rank], head_dim), self.device),
             device=self.device).view(torch.bfloat16)
+
+    def check_matches(self, plan: ShardPlan, heads: int, head_dim: int, rank: int) -> None:
+        """The epilogue computes peer addresses from this target's shape:
+        reusing it for a layer of another shape would write past the peers'
+        buffers, so any mismatch is refused."""
+        rows = [plan.token_range(r)[1] - plan.token_range(r)[0] for r in range(plan.world)]
+        tb = [plan.token_range(r)[0] for r in range(plan.world)] + [plan.layout.total_tokens]
+        if (self.world, self.rank, self.heads, self.head_dim) != (plan.world, rank, heads, head_dim):
+            raise ValueError(
+                f"scatter_target is for world={self.world} rank={self.rank} heads={self.heads} "
+                f"head_dim={self.head_dim}, the call has world={plan.world} rank={rank} "
+                f"heads={heads} head_dim={head_dim}")
+        if rows != self.rows or tb != self.token_begin.tolist():
+            raise ValueError("scatter_target token ranges differ from this layer's ShardPlan")
+        if not self._own:
+            raise ValueError("scatter_target was closed")
 
     def chunk_ptrs(self, head0: int) -> torch.Tensor:
         """Per-rank pointers to head `head0` of each buffer (device u64[world])."""
@@ -326,7 +347,8 @@ def _assemble(parts, plan: ShardPlan) -> torch.Tensor:
 def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, group=None,
                              inputs: str = "sharded", ops=None, return_mask: bool = False,
                              chunk_heads: int | None = None, comm_group=None,
-                             combine: str = "allreduce", scatter_target=None):
+                             combine: str = "allreduce", scatter_target=None,
+                             validate: bool = True):
     """One block-sparse global-attention layer over every rank of `group`.
 
     inputs="sharded":    q/k/v are this rank's frames (ShardPlan.frame_range);
@@ -373,6 +395,17 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
     chunk = chunk_heads or H
     spans = [(a, min(H, a + chunk)) for a in range(0, H, chunk)]
     cgroup = comm_group if comm_group is not None else group
+    if combine == "scatter" and scatter_target is not None:
+        scatter_target.check_matches(plan, H, q.shape[2], rank)
+    if validate:
+        # once per call, on this rank's inputs (as_f32, tensorio.py:47-59);
+        # a rank's verdict is shared so that every rank raises together
+        from . import _native as N
+        ok = torch.tensor([1.0 if N.all_finite(q, k, v) else 0.0], device=q.device)
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() < 1.0:
+            raise ValueError("q/k/v contain non-finite values")
 
     own_target = False
     pending = []

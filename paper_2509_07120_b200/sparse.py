@@ -95,15 +95,33 @@ def _run(q, k, v, out, layout, mask: BlockMask, bits, counts, scale, inputs_perm
     out_code = N.BSA_BF16 if out.dtype == torch.bfloat16 else N.BSA_F32
     need = L.bsa_sparse_attention_workspace(lay, q.shape[0], q.shape[2], g.block_q, g.block_k,
                                             in_code, int(inputs_permuted), _PATHS[path])
-    if ws is None or ws.numel() < need:
+    if ws is None or ws.numel() < need or ws.device != q.device:
         ws = N.workspace(need, q.device)
-    N.check(L.bsa_sparse_attention(
-        N.tensor_desc(q), N.tensor_desc(k), N.tensor_desc(v), out.data_ptr(), out_code, lay,
-        g.block_q, g.block_k, bits.data_ptr(), N.ptr(counts), np.float32(scale).item(),
-        int(inputs_permuted), int(shard), int(num_shards),
-        _PATHS[path] | (N.FLAG_TIMING if timing else 0), ws.data_ptr(), ws.numel(),
-        N.stream_ptr()), "sparse_attention")
+    with N.on_device(q.device):
+        N.check(L.bsa_sparse_attention(
+            N.tensor_desc(q), N.tensor_desc(k), N.tensor_desc(v), out.data_ptr(), out_code, lay,
+            g.block_q, g.block_k, bits.data_ptr(), N.ptr(counts), np.float32(scale).item(),
+            int(inputs_permuted), int(shard), int(num_shards),
+            _PATHS[path] | (N.FLAG_TIMING if timing else 0), ws.data_ptr(), ws.numel(),
+            N.stream_ptr()), "sparse_attention")
     return ws
+
+
+def _check_out(out: torch.Tensor, q: torch.Tensor, out_dtype) -> None:
+    """The kernels write a contiguous (H, T, d) fp32/bf16 buffer on q's
+    device through a raw pointer: anything else is refused up front."""
+    if not isinstance(out, torch.Tensor):
+        raise ValueError(f"out must be a torch tensor, got {type(out).__name__}")
+    if tuple(out.shape) != tuple(q.shape):
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {tuple(q.shape)}")
+    if out.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError(f"out dtype must be float32 or bfloat16, got {out.dtype}")
+    if out_dtype is not None and out_dtype != out.dtype:
+        raise ValueError(f"out_dtype {out_dtype} conflicts with out.dtype {out.dtype}")
+    if out.device != q.device:
+        raise ValueError(f"out is on {out.device}, inputs on {q.device}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
 
 
 def last_kernel_ms() -> float:
@@ -126,13 +144,17 @@ def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PAN
     del panel_blocks, threads
     inp = job.inputs
     q, k, v = inp.q, inp.k, inp.v
-    if out_dtype is None:
-        out_dtype = q.dtype
-    if out is None:
+    if out is not None:
+        _check_out(out, q, out_dtype)
+    else:
+        if out_dtype is None:
+            out_dtype = q.dtype
+        if out_dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError(f"out_dtype must be float32 or bfloat16, got {out_dtype}")
         alloc = torch.zeros if num_shards > 1 else torch.empty
         out = alloc(q.shape, dtype=out_dtype, device=q.device)
     bits = job.mask.device_bits(q.device)
-    _run(q, k, v, out, job.layout, job.mask, bits, job.mask.device_counts(), inp.scale,
+    _run(q, k, v, out, job.layout, job.mask, bits, job.mask.device_counts(q.device), inp.scale,
          inputs_permuted, shard, num_shards, path, workspace, timing)
     if inp.numpy_io:
         return out.float().cpu().numpy()
@@ -169,7 +191,7 @@ def sparse_attention_stats(job: SparseAttentionJob, *,
     g = job.mask.geometry
     out = torch.empty(q.shape, dtype=q.dtype, device=q.device)
     bits = job.mask.device_bits(q.device)
-    counts = job.mask.device_counts()
+    counts = job.mask.device_counts(q.device)
     sparsity = job.mask.achieved_sparsity()
     per_dense, per_sparse = _flops_per_head(job)
     reports = []
@@ -178,10 +200,11 @@ def sparse_attention_stats(job: SparseAttentionJob, *,
         sub = BlockMask._from_device(bits[h * rows:(h + 1) * rows], None, 1, g)
         c = counts[h * rows:(h + 1) * rows] if counts is not None else None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+        stream = torch.cuda.current_stream(q.device)
+        e0.record(stream)
         _run(q[h:h + 1], k[h:h + 1], v[h:h + 1], out[h:h + 1], job.layout, sub, sub._bits, c,
              inp.scale, False, 0, 1, path)
-        e1.record()
+        e1.record(stream)
         e1.synchronize()
         reports.append(HeadReport(
             head=h,
