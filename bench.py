@@ -15,17 +15,22 @@ Arms:
                      bounded sample of the same workload, extrapolated to a
                      full layer.
 
-Multi-GPU (torchrun, NCCL), timing is the max over ranks:
-  --mode replicas (default)  every rank runs its own independent layer (the
-                     per-GPU workload replicated: "scaling": "weak"); no
-                     collective on the data path.
-  --mode sharded     ONE layer of --frames frames split over the ranks
-                     (paper_2509_07120_b200/shard.py): frame-sharded Q/K/V,
-                     NCCL all-gather of Q/K/V, row-split scoring + mask
-                     all-gather, LPT-sharded attention, sum all-reduce
-                     ("scaling": "strong").  --combine scatter replaces the
-                     all-reduce with the attention epilogue storing rows
-                     into the owning rank's buffer over NVLink (CUDA IPC).
+Multi-GPU (one process per GPU, NCCL), timing is the max over ranks.
+`python bench.py --gpus N` with N > 1 re-executes itself under
+`torch.distributed.run` with N ranks (or fails loudly when the box has
+fewer than N GPUs); the driver's own torchrun launch is used as is.
+  --mode sharded (default for N > 1)  ONE layer of --frames frames split
+                     over the ranks (paper_2509_07120_b200/shard.py, the
+                     config-5 split): frame-sharded Q/K/V, NCCL all-gather of
+                     Q/K/V, row-split scoring + mask all-gather, every rank
+                     attends its share of each head's LPT rows ("scaling":
+                     "strong").  --combine scatter (default): the attention
+                     epilogue stores each row into the owning rank's buffer
+                     over NVLink (CUDA IPC); allreduce / reduce_scatter: NCCL.
+  --mode replicas    every rank runs its own independent layer (the per-GPU
+                     workload replicated: "scaling": "weak"); no collective.
+NCCL_DEBUG=INFO is set for N > 1 (unless already set) so the rank/channel
+setup is in the log.
 
 The e2e leg runs the same layer from pinned host memory through
 pipeline.HostLayerPipeline (H2D / kernels / D2H overlapped per head chunk).
@@ -67,18 +72,51 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
+                    help="auto: sharded when N > 1")
     ap.add_argument("--shard-chunk", type=int, default=4,
                     help="heads per pipeline chunk of --mode sharded (comm overlaps kernels)")
-    ap.add_argument("--combine", default="allreduce", choices=["allreduce", "scatter"],
-                    help="--mode sharded output combine: NCCL sum all-reduce, or the kernel "
-                         "epilogue storing rows into the owners' buffers over NVLink (CUDA IPC)")
+    ap.add_argument("--combine", default="scatter",
+                    choices=["scatter", "reduce_scatter", "allreduce"],
+                    help="--mode sharded output combine: the kernel epilogue storing rows into "
+                         "the owners' buffers over NVLink (CUDA IPC), or an NCCL "
+                         "reduce-scatter / sum all-reduce")
     ap.add_argument("--e2e-chunk", default="auto",
                     help="head chunks of the host-memory e2e leg: 'auto' (1,3,4,..,4,3,1), "
                          "heads per chunk, or a comma list of chunk sizes")
     ap.add_argument("--specials", type=int, default=S_PER_FRAME,
                     help="special tokens per frame (VGGT 5; pi3: 4 register tokens, no camera)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.mode == "auto":
+        a.mode = "sharded" if a.gpus > 1 else "replicas"
+    return a
+
+
+def ensure_ranks(a):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run with
+    N ranks on this node; never silently run fewer GPUs than asked for."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != a.gpus:
+            sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world_env}: launch one rank per "
+                     "GPU with matching --gpus")
+        return
+    if a.gpus <= 1:
+        return
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        sys.exit(f"bench.py: --gpus {a.gpus} requested but this node has {have} CUDA "
+                 f"device(s); refusing to report a {a.gpus}-GPU number")
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def workload_config(a, extra=None):
@@ -96,8 +134,9 @@ def workload_config(a, extra=None):
                         if a.mode == "replicas" else
                         f"sharded x{a.gpus} (one layer: frame-sharded inputs, NCCL all-gather "
                         f"of Q/K/V, LPT-sharded rows, " +
-                        ("sum all-reduce)" if a.combine == "allreduce" else
-                         "epilogue scatter into peer buffers over NVLink)")),
+                        {"allreduce": "sum all-reduce)",
+                         "reduce_scatter": "NCCL reduce-scatter)",
+                         "scatter": "epilogue scatter into peer buffers over NVLink)"}[a.combine]),
     }
     if extra:
         cfg.update(extra)
@@ -182,6 +221,7 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
@@ -513,6 +553,7 @@ def main():
     if a.impl == "reference":
         run_reference(a)
     else:
+        ensure_ranks(a)
         run_ours(a)
 
 

@@ -44,6 +44,11 @@ extern "C" {
 #define BSA_PATH_SIMT 1     /* force the CUDA-core kernel (fp32 math)        */
 #define BSA_PATH_TC 2       /* require the tcgen05 kernel (EUNSUPPORTED if not) */
 #define BSA_FLAG_TIMING 16  /* bracket the attention kernel with CUDA events */
+/* key-range split of the tensor-core path (bits 8-15): 0 = auto (split when a
+ * head's K+V outgrows L2, e.g. N=1000 frames), n = n ranges whose partials
+ * are merged by log-sum-exp (results equal within rounding) */
+#define BSA_FLAG_RANGES(n) (((n) & 0xFF) << 8)
+#define BSA_FLAG_RANGES_GET(f) (((f) >> 8) & 0xFF)
 
 /* TokenLayout (layout.py:27-66): F frames of S specials + P patches. */
 typedef struct {

@@ -294,17 +294,20 @@ def masked_attention_f64(q, k, v, frames, patches, specials, mask, block_q, bloc
     out = np.empty((h, src_rows.size, d), dtype=np.float64)
     scale = head_scale(d)
     part = inv[src_rows]
+    # rows sharing a key set (all special rows; the rows of one q-block) are
+    # evaluated together, <= 128 rows per matrix product
+    group = np.where(part < n_spec, -1, (part - n_spec) // block_q)
     for hh in range(h):
-        for i, (sr, pr) in enumerate(zip(src_rows, part)):
-            if pr < n_spec:
-                keys = np.arange(n)
-            else:
-                qb = (pr - n_spec) // block_q
-                keys = _row_keys(mask[hh, qb], n_spec, tp, block_k)
-            s = (kp_[hh, keys] @ q[hh, sr]) * scale
-            w = np.exp(s - s.max())
-            w /= w.sum()
-            out[hh, i] = w @ vp_[hh, keys]
+        for gq in np.unique(group):
+            idx = np.nonzero(group == gq)[0]
+            keys = np.arange(n) if gq < 0 else _row_keys(mask[hh, gq], n_spec, tp, block_k)
+            kk, vv = kp_[hh, keys], vp_[hh, keys]
+            for c0 in range(0, idx.size, 128):
+                sel = idx[c0:c0 + 128]
+                s = (q[hh, src_rows[sel]] @ kk.T) * scale
+                w = np.exp(s - s.max(axis=1, keepdims=True))
+                w /= w.sum(axis=1, keepdims=True)
+                out[hh, sel] = w @ vv
     return out
 
 

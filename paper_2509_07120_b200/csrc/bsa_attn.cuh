@@ -46,15 +46,23 @@ struct KeyChunker {
   int64_t pos, end;     // current contiguous range [pos, end)
   int64_t byte_idx;     // mask iteration
   unsigned int cur;     // remaining bits of the current byte
+  int64_t byte_end;     // mask bytes [.., byte_end) (a key range's slice of the row)
   __device__ KeyChunker(const AttnGeom& G, int64_t qb, const uint8_t* mask_row, int ch)
       : Ts(G.Ts), Tp(G.Tp), T(G.T), bk(G.bk), nk(G.nk), row(qb < 0 ? nullptr : mask_row),
-        CH(ch), phase(0), pos(0), end(qb < 0 ? G.T : G.Ts), byte_idx(-1), cur(0) {}
+        CH(ch), phase(0), pos(0), end(qb < 0 ? G.T : G.Ts), byte_idx(-1), cur(0),
+        byte_end(G.mask_row_bytes) {}
+  // key-range form: contiguous keys [pos0, end0), then the selected blocks
+  // of mask bytes [byte0, byte1)
+  __device__ KeyChunker(const AttnGeom& G, int64_t qb, const uint8_t* mask_row, int ch,
+                        int64_t pos0, int64_t end0, int64_t byte0, int64_t byte1)
+      : Ts(G.Ts), Tp(G.Tp), T(G.T), bk(G.bk), nk(G.nk), row(qb < 0 ? nullptr : mask_row),
+        CH(ch), phase(0), pos(pos0), end(end0), byte_idx(byte0 - 1), cur(0), byte_end(byte1) {}
 
   // next selected key block (>= 0) or -1
   __device__ __forceinline__ int64_t next_block() {
     while (cur == 0) {
       ++byte_idx;
-      if (byte_idx * 8 >= nk) return -1;
+      if (byte_idx * 8 >= nk || byte_idx >= byte_end) return -1;
       cur = row[byte_idx];
     }
     const int b = __ffs(cur) - 1;
@@ -92,7 +100,26 @@ int launch_simt_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_te
                           void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
                           int permuted, float scale, int shard, int num_shards, cudaStream_t st);
 
+// Key-range split (long sequences): the keys of a head are cut into `nr`
+// ranges of `rb` key blocks (rb % 8 == 0, so a range is a byte range of the
+// .bsm mask row).  Work item (head, row tile, range r) streams only range r's
+// keys: the special strip (range 0) or its slice of [0, T) for special rows,
+// then the row's selected blocks inside the range.  Items of one (head,
+// range) run together, so their K/V (1/nr of the head's) stays L2-resident.
+// The ranges of a row are merged afterwards by their log-sum-exp.
+struct KeyRanges {
+  int32_t nr, rb;          // ranges, key blocks per range (nr == 1: rb >= nk)
+  const int32_t* rcounts;  // (H * nq, nr) selected blocks per row and range (nr > 1)
+};
+
 struct TcArgs {
+  // key-range split (bsa_tc_common.cuh KeyRanges); nr > 1: the kernel writes
+  // per-range partials (O / l and log2-sum-exp, rows in partitioned order)
+  // that combine_kernel merges into out
+  KeyRanges kr;
+  void* part_out;             // (nr, H, T, 64) bf16 (part_bf16) or fp32
+  int part_bf16;
+  float* part_lse;            // (nr, H, T): offset + log2(l)
   const __nv_bfloat16* qp;   // packed partitioned (H, T, 64)
   const __nv_bfloat16* kp;
   const void* vp;             // V: bf16, or fp16 scaled by 2^v_shift[h] (v_f16)
@@ -104,8 +131,8 @@ struct TcArgs {
   int permuted_out;          // write rows in partitioned order
   const uint8_t* bits;
   const int32_t* counts;     // per (h, qb) selected blocks
-  const int32_t* items;      // LPT-ordered work items
-  int32_t n_items;
+  const int32_t* items;      // LPT-ordered work items of this shard (schedule_kernel)
+  int32_t n_items;            // capacity of items / ovf_flags (H * nr * M)
   int32_t* work_counter;
   float scale_log2;          // scale * log2(e)
   int shard, num_shards;
@@ -125,7 +152,26 @@ struct TcArgs {
   const int64_t* token_begin;
 };
 
-int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st);
+// merge of the key-range partials (bsa_attn_host.cu combine_kernel): per row
+// L = max_r lse_r, out = sum_r 2^(lse_r - L) O_r / sum_r 2^(lse_r - L) over the
+// ranges the row has keys in, written like the kernel epilogue would
+struct CombineArgs {
+  KeyRanges kr;
+  const void* part_out;
+  int part_bf16;
+  const float* part_lse;
+  const int32_t* row_shard;  // (H, M) shard of each row tile, or null (all rows)
+  int shard;
+  void* out;
+  int out_bf16;
+  int permuted_out;
+  int32_t scatter_world;
+  const unsigned long long* out_ptrs;
+  const int64_t* token_begin;
+};
+int launch_combine(const AttnGeom& G, const CombineArgs& c, cudaStream_t st);
+int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
+                        const CombineArgs* comb);
 cudaEvent_t timing_events(int which);
 size_t tc_smem_bytes();
 // source-order (f32|bf16) Q/K/V -> contiguous bf16 [specials | patches]

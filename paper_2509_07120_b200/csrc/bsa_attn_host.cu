@@ -111,29 +111,59 @@ __global__ void counts_kernel(const uint8_t* __restrict__ bits, int64_t rows, in
   counts[r] = c;
 }
 
-// items per head: nst special tiles (rows of 128) then nq patch q-blocks.
-// Deterministic stable counting sort by descending cost: the histogram is
-// built in parallel, the placement by warp 0 walking the items in index
-// order 32 at a time (__match_any_sync ranks equal costs inside a chunk).
-// Determinism matters: every rank of a multi-GPU run builds this list
-// independently and takes every num_shards-th entry of it.
-__device__ __forceinline__ int64_t item_cost(const int32_t* counts, int64_t h, int64_t nq,
-                                             int64_t nst, int64_t nsc, int64_t spec_cost,
-                                             int64_t max_cost, int64_t i) {
-  const int64_t c = i < nst ? spec_cost : (nsc + counts[h * nq + (i - nst)] + 1) / 2;
-  return min(c, max_cost);
+// ---------------------------------------------------------------------------
+// LPT work list.  Row tiles per head: nst special tiles (rows of 128), then
+// nq patch q-blocks.  Item code = (h * nr + r) * M + li (bsa_tc_common.cuh).
+//
+// Deterministic stable counting sorts by descending cost (histogram in
+// parallel, placement by warp 0 walking the rows in index order, 32 at a
+// time, __match_any_sync ranking equal costs).  Every rank of a multi-GPU run
+// builds the same order independently:
+//   1. (num_shards > 1) rows of a head in LPT order of their total cost are
+//      dealt round-robin to the shards: row_shard[h][li] = position % shards.
+//      All key ranges of a row stay on one shard, so its partials can be
+//      merged locally.
+//   2. per key range r: this shard's rows with keys in range r, LPT by their
+//      range cost, appended to the head's list.
+// Heads stay contiguous, then ranges within a head, so one (head, range)'s
+// K/V stays L2-resident while the SMs drain it.  compact_kernel packs the
+// per-head lists and leaves the item count on the device.
+// ---------------------------------------------------------------------------
+struct SchedGeom {
+  int64_t nq, nst, M, nsc, T, Ts;
+  int32_t nr, rb;
+  int64_t max_cost;
+};
+
+// chunks of row tile li of head h in key range r (0: no keys there)
+__device__ __forceinline__ int64_t range_cost(const SchedGeom& S, const int32_t* counts,
+                                              const int32_t* rcounts, int64_t h, int64_t li,
+                                              int32_t r) {
+  int64_t c;
+  if (li < S.nst) {
+    const int64_t rkeys = (int64_t)S.rb * 64;
+    const int64_t k0 = r == 0 ? 0 : S.Ts + r * rkeys;
+    const int64_t k1 = r == S.nr - 1 ? S.T : S.Ts + (r + 1) * rkeys;
+    c = k1 > k0 ? (k1 - k0 + 63) / 64 : 0;
+  } else {
+    const int64_t row = h * S.nq + (li - S.nst);
+    c = (r == 0 ? S.nsc : 0) + (S.nr == 1 ? counts[row] : rcounts[row * S.nr + r]);
+  }
+  return min(c, S.max_cost);
 }
 
-__global__ void __launch_bounds__(1024)
-    schedule_kernel(const int32_t* __restrict__ counts, int64_t nq, int64_t nst, int64_t nsc,
-                    int64_t spec_cost, int64_t max_cost, int32_t* __restrict__ items) {
-  extern __shared__ int32_t hist[];  // max_cost + 1 bins
-  const int64_t h = blockIdx.x;
-  const int64_t M = nst + nq;
+// stable descending counting sort of the rows with cost(i) >= 0:
+// out[k] = base + i for the k-th longest; returns how many were placed
+template <class CostF>
+__device__ int32_t lpt_place(int64_t M, int64_t max_cost, int32_t* hist, CostF cost,
+                             int32_t* out, int32_t base) {
+  __shared__ int32_t total;
   for (int64_t c = threadIdx.x; c <= max_cost; c += blockDim.x) hist[c] = 0;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x)
-    atomicAdd(&hist[item_cost(counts, h, nq, nst, nsc, spec_cost, max_cost, i)], 1);
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const int64_t c = cost(i);
+    if (c >= 0) atomicAdd(&hist[c], 1);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int32_t run = 0;  // descending cost: longest first
@@ -142,26 +172,167 @@ __global__ void __launch_bounds__(1024)
       hist[c] = run;
       run += n;
     }
+    total = run;
   }
   __syncthreads();
   if (threadIdx.x < 32) {
     const unsigned lane = threadIdx.x;
     for (int64_t i0 = 0; i0 < M; i0 += 32) {
       const int64_t i = i0 + lane;
-      const bool valid = i < M;
+      const int c = i < M ? (int)cost(i) : -1;
+      const bool valid = c >= 0;
       const unsigned active = __ballot_sync(0xffffffffu, valid);
       if (valid) {
-        const int cost = (int)item_cost(counts, h, nq, nst, nsc, spec_cost, max_cost, i);
-        const unsigned same = __match_any_sync(active, cost);
+        const unsigned same = __match_any_sync(active, c);
         const int rank = __popc(same & ((1u << lane) - 1u));
-        const int32_t base = hist[cost];
-        items[h * M + base + rank] = (int32_t)(h * M + i);
+        const int32_t at = hist[c];
+        out[at + rank] = base + (int32_t)i;
         __syncwarp(active);
-        if (rank == 0) hist[cost] = base + __popc(same);
+        if (rank == 0) hist[c] = at + __popc(same);
       }
       __syncwarp();
     }
   }
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(1024)
+    schedule_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ rcounts,
+                    SchedGeom S, int num_shards, int shard, int32_t* __restrict__ row_shard,
+                    int32_t* __restrict__ tmp, int32_t* __restrict__ head_count) {
+  extern __shared__ int32_t hist[];  // max_cost + 1 bins
+  const int64_t h = blockIdx.x;
+  const int64_t cap = (int64_t)S.nr * S.M;
+  int32_t* list = tmp + h * cap;
+  int32_t* rs = row_shard + h * S.M;
+  if (num_shards > 1) {
+    // 1. rows by total cost, dealt round-robin to the shards
+    auto total_cost = [&](int64_t i) -> int64_t {
+      int64_t c = 0;
+      for (int32_t r = 0; r < S.nr; ++r) c += range_cost(S, counts, rcounts, h, i, r);
+      return min(c, S.max_cost);
+    };
+    lpt_place(S.M, S.max_cost, hist, total_cost, list, 0);
+    for (int64_t p = threadIdx.x; p < S.M; p += blockDim.x) rs[list[p]] = (int32_t)(p % num_shards);
+    __syncthreads();
+  }
+  // 2. per key range, this shard's rows with keys there
+  int32_t n = 0;
+  for (int32_t r = 0; r < S.nr; ++r) {
+    auto cost = [&](int64_t i) -> int64_t {
+      if (num_shards > 1 && rs[i] != shard) return -1;
+      const int64_t c = range_cost(S, counts, rcounts, h, i, r);
+      return c > 0 ? c : -1;
+    };
+    n += lpt_place(S.M, S.max_cost, hist, cost, list + n, (int32_t)((h * S.nr + r) * S.M));
+  }
+  if (threadIdx.x == 0) head_count[h] = n;
+}
+
+// pack the per-head lists back to back; the total goes to n_items
+__global__ void compact_kernel(const int32_t* __restrict__ tmp,
+                               const int32_t* __restrict__ head_count, int64_t cap,
+                               int32_t* __restrict__ items, int32_t* __restrict__ n_items) {
+  const int64_t h = blockIdx.x;
+  int64_t off = 0;
+  for (int64_t j = 0; j < h; ++j) off += head_count[j];
+  const int32_t n = head_count[h];
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) items[off + i] = tmp[h * cap + i];
+  if (h == gridDim.x - 1 && threadIdx.x == 0) *n_items = (int32_t)(off + n);
+}
+
+// selected blocks of every (row, key range): popcount of the range's bytes
+__global__ void range_counts_kernel(const uint8_t* __restrict__ bits, int64_t rows,
+                                    int64_t row_bytes, int32_t nr, int32_t rb,
+                                    int32_t* __restrict__ rcounts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * nr) return;
+  const int64_t row = i / nr, r = i - row * nr;
+  const int64_t b0 = r * (rb / 8), b1 = min(row_bytes, (r + 1) * (rb / 8));
+  const uint8_t* b = bits + row * row_bytes;
+  int c = 0;
+  for (int64_t j = b0; j < b1; ++j) c += __popc((unsigned)b[j]);
+  rcounts[i] = c;
+}
+
+// merge of the key-range partials (CombineArgs); one thread per 8 columns
+__global__ void combine_kernel(AttnGeom G, CombineArgs C) {
+  const int64_t nst = ceil_div(G.Ts, 128), M = nst + G.nq;
+  const int nr = C.kr.nr;
+  const int64_t total = G.H * G.T * 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i & 7);
+    const int64_t hr = i >> 3;
+    const int64_t h = hr / G.T, pr = hr - h * G.T;
+    const bool spec = pr < G.Ts;
+    const int64_t qb = spec ? -1 : (pr - G.Ts) / 128;
+    const int64_t li = spec ? pr / 128 : nst + qb;
+    if (C.row_shard && C.row_shard[h * M + li] != C.shard) continue;
+    auto valid = [&](int r) -> bool {
+      if (spec) return true;  // every range holds keys of a special row
+      return (r == 0 && G.Ts > 0) || C.kr.rcounts[(h * G.nq + qb) * nr + r] > 0;
+    };
+    float L = -INFINITY;
+    for (int r = 0; r < nr; ++r)
+      if (valid(r)) L = fmaxf(L, C.part_lse[(r * G.H + h) * G.T + pr]);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, den = 0.f;
+    for (int r = 0; r < nr; ++r) {
+      if (!valid(r)) continue;
+      const int64_t prow = (r * G.H + h) * G.T + pr;
+      const float w = exp2f(C.part_lse[prow] - L);
+      den += w;
+      if (C.part_bf16) {
+        const uint4 u = *reinterpret_cast<const uint4*>((const __nv_bfloat16*)C.part_out + prow * 64 + c8 * 8);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(p2[e]);
+          acc[2 * e] = fmaf(w, f.x, acc[2 * e]);
+          acc[2 * e + 1] = fmaf(w, f.y, acc[2 * e + 1]);
+        }
+      } else {
+        const float4* p4 = reinterpret_cast<const float4*>((const float*)C.part_out + prow * 64 + c8 * 8);
+        const float4 a0 = p4[0], a1 = p4[1];
+        acc[0] = fmaf(w, a0.x, acc[0]); acc[1] = fmaf(w, a0.y, acc[1]);
+        acc[2] = fmaf(w, a0.z, acc[2]); acc[3] = fmaf(w, a0.w, acc[3]);
+        acc[4] = fmaf(w, a1.x, acc[4]); acc[5] = fmaf(w, a1.y, acc[5]);
+        acc[6] = fmaf(w, a1.z, acc[6]); acc[7] = fmaf(w, a1.w, acc[7]);
+      }
+    }
+    const float inv = 1.0f / den;
+    const int64_t dst = C.permuted_out ? pr : G.L.part_src(pr);
+    if (C.out_bf16) {
+      __nv_bfloat16* orow = (__nv_bfloat16*)C.out + (h * G.T + dst) * 64;
+      if (C.scatter_world > 0) {
+        int r = 0;
+        while (r + 1 < C.scatter_world && dst >= C.token_begin[r + 1]) ++r;
+        const int64_t t0 = C.token_begin[r], tr = C.token_begin[r + 1] - t0;
+        orow = (__nv_bfloat16*)C.out_ptrs[r] + (h * tr + (dst - t0)) * 64;
+      }
+      uint4 o;
+      uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+        ow[e] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      *reinterpret_cast<uint4*>(orow + c8 * 8) = o;
+    } else {
+      float4* op = reinterpret_cast<float4*>((float*)C.out + (h * G.T + dst) * 64 + c8 * 8);
+      op[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      op[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    }
+  }
+}
+
+int launch_combine(const AttnGeom& G, const CombineArgs& c, cudaStream_t st) {
+  const int64_t total = G.H * G.T * 8;
+  const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  combine_kernel<<<grid, 256, 0, st>>>(G, c);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
 }
 
 __global__ void area_kernel(const uint8_t* __restrict__ bits, int64_t H, int64_t nq, int64_t nk,
@@ -243,32 +414,73 @@ static int choose_path(const AttnGeom& G, int32_t in_dtype, int32_t flags) {
   return tc_ok ? BSA_PATH_TC : BSA_PATH_SIMT;
 }
 
+// key-range split of the keys of one head (KeyRanges).  requested: 0 = auto:
+// one range while a head's K+V (bf16) fits comfortably in L2, else ranges of
+// about 64 MB of K+V each; else the requested number (capped at nk / 8).
+static KeyRanges choose_ranges(const AttnGeom& G, int requested) {
+  KeyRanges kr;
+  kr.rcounts = nullptr;
+  const int64_t nk8 = ceil_div(G.nk, 8);  // whole mask bytes
+  int64_t nr;
+  if (requested > 0) {
+    nr = requested;
+  } else {
+    const int64_t kv_head = 2 * G.T * G.d * 2;
+    nr = kv_head <= (96ll << 20) ? 1 : ceil_div(kv_head, 64ll << 20);
+  }
+  nr = std::max<int64_t>(1, std::min<int64_t>(nr, nk8));
+  const int64_t rb = 8 * ceil_div(nk8, nr);  // key blocks per range, whole bytes
+  kr.nr = (int32_t)ceil_div(G.nk, rb);
+  kr.rb = (int32_t)rb;
+  return kr;
+}
+
 struct TcWorkspace {
   __nv_bfloat16 *qp, *kp;
   void* vp;
   int32_t *items, *counter, *counts, *vshift;
   int32_t *ovf_flags, *ovf_list, *ovf_count;
+  int32_t *row_shard, *tmp, *head_count, *n_items, *rcounts;
   unsigned int* vamax;
+  void* part_out;
+  float* part_lse;
+  int64_t cap;  // item capacity: H * nr * M
   size_t bytes;
 };
 
-static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G) {
+static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G, const KeyRanges& kr,
+                                bool part_bf16) {
   TcWorkspace w;
   char* p = (char*)base;
   const size_t tens = align_up((size_t)(G.H * G.T * G.d) * 2, 256);
   const int64_t nst = ceil_div(G.Ts, 128);
-  const int64_t n_items = G.H * (nst + G.nq);
+  const int64_t M = nst + G.nq;
+  w.cap = G.H * kr.nr * M;
+  const size_t capb = align_up((size_t)w.cap * 4, 256);
   w.qp = (__nv_bfloat16*)p; p += tens;
   w.kp = (__nv_bfloat16*)p; p += tens;
   w.vp = (void*)p; p += tens;
-  w.items = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
+  w.items = (int32_t*)p; p += capb;
   w.counter = (int32_t*)p; p += 256;
   w.counts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq) * 4, 256);
   w.vshift = (int32_t*)p; p += align_up((size_t)G.H * 4, 256);
   w.vamax = (unsigned int*)p; p += align_up((size_t)G.H * 4, 256);
-  w.ovf_flags = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
-  w.ovf_list = (int32_t*)p; p += align_up((size_t)n_items * 4, 256);
+  w.ovf_flags = (int32_t*)p; p += capb;
+  w.ovf_list = (int32_t*)p; p += capb;
   w.ovf_count = (int32_t*)p; p += 256;
+  w.row_shard = (int32_t*)p; p += align_up((size_t)(G.H * M) * 4, 256);
+  w.tmp = (int32_t*)p; p += capb;
+  w.head_count = (int32_t*)p; p += align_up((size_t)G.H * 4, 256);
+  w.n_items = (int32_t*)p; p += 256;
+  w.rcounts = nullptr;
+  w.part_out = nullptr;
+  w.part_lse = nullptr;
+  if (kr.nr > 1) {
+    w.rcounts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq * kr.nr) * 4, 256);
+    w.part_out = (void*)p;
+    p += align_up((size_t)(kr.nr * G.H * G.T * G.d) * (part_bf16 ? 2 : 4), 256);
+    w.part_lse = (float*)p; p += align_up((size_t)(kr.nr * G.H * G.T) * 4, 256);
+  }
   w.bytes = (size_t)(p - (char*)base);
   return w;
 }
@@ -339,7 +551,8 @@ size_t bsa_sparse_attention_workspace(const bsa_layout* layout, int64_t heads, i
   if (!layout || heads < 1 || dim < 1 || block_q < 1 || block_k < 1) return 0;
   const AttnGeom G = make_geom(to_layout(layout), heads, (int)dim, block_q, block_k);
   if (choose_path(G, in_dtype, flags) != BSA_PATH_TC) return 256;
-  return tc_ws_layout(nullptr, G).bytes + 256;
+  // fp32 partials cover either output dtype
+  return tc_ws_layout(nullptr, G, choose_ranges(G, BSA_FLAG_RANGES_GET(flags)), false).bytes + 256;
 }
 
 static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
@@ -388,7 +601,16 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
 
   // ---------------- tensor-core path ----------------
   if (!ws) return fail(BSA_EINVAL, "sparse_attention: workspace required");
-  TcWorkspace W = tc_ws_layout(ws, G);
+  static int env_ranges = -2;
+  if (env_ranges == -2) {
+    const char* e = getenv("BSA_TC_KEY_RANGES");  // experiments: force a key-range split
+    env_ranges = e ? atoi(e) : -1;
+  }
+  const int req_ranges = BSA_FLAG_RANGES_GET(flags) ? BSA_FLAG_RANGES_GET(flags)
+                                                    : (env_ranges > 0 ? env_ranges : 0);
+  const KeyRanges KR = choose_ranges(G, req_ranges);
+  const bool part_bf16 = out_dtype == BSA_BF16;
+  TcWorkspace W = tc_ws_layout(ws, G, KR, part_bf16);
   if (ws_bytes < W.bytes) return fail(BSA_EINVAL, "sparse_attention: workspace too small");
   // kernel variant: exp2 split between MUFU and the FMA pipe, P/V precision
   static int env_poly = -2, env_f16 = -2;
@@ -416,19 +638,39 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
     BSA_LAUNCH_CHECK();
     counts = W.counts;
   }
-  const int64_t nst = ceil_div(G.Ts, 128);
-  const int64_t nsc = ceil_div(G.Ts, 64);
-  const int64_t spec_cost = (ceil_div(G.T, 64) + 1) / 2;
-  const int64_t max_cost = std::max<int64_t>(spec_cost, (nsc + G.nk + 1) / 2);
-  const size_t hsmem = (size_t)(max_cost + 1) * 4;
+  KeyRanges kr = KR;
+  if (kr.nr > 1) {
+    range_counts_kernel<<<(unsigned)ceil_div(rows * kr.nr, 256), 256, 0, st>>>(
+        mask_bits, rows, G.mask_row_bytes, kr.nr, kr.rb, W.rcounts);
+    BSA_LAUNCH_CHECK();
+    kr.rcounts = W.rcounts;
+  }
+  SchedGeom S;
+  S.nq = G.nq;
+  S.nst = ceil_div(G.Ts, 128);
+  S.M = S.nst + G.nq;
+  S.nsc = ceil_div(G.Ts, 64);
+  S.T = G.T;
+  S.Ts = G.Ts;
+  S.nr = kr.nr;
+  S.rb = kr.rb;
+  S.max_cost = std::max<int64_t>(ceil_div(G.T, 64) + kr.nr, S.nsc + G.nk);
+  const size_t hsmem = (size_t)(S.max_cost + 1) * 4;
   if (hsmem > 200 * 1024) return fail(BSA_EUNSUPPORTED, "sequence too long for the scheduler");
   BSA_CUDA_TRY(cudaFuncSetAttribute(schedule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)hsmem));
-  schedule_kernel<<<(unsigned)G.H, 1024, hsmem, st>>>(counts, G.nq, nst, nsc, spec_cost, max_cost,
-                                                      W.items);
+  schedule_kernel<<<(unsigned)G.H, 1024, hsmem, st>>>(counts, kr.rcounts, S, num_shards, shard,
+                                                      W.row_shard, W.tmp, W.head_count);
+  BSA_LAUNCH_CHECK();
+  compact_kernel<<<(unsigned)G.H, 256, 0, st>>>(W.tmp, W.head_count, (int64_t)kr.nr * S.M, W.items,
+                                                W.n_items);
   BSA_LAUNCH_CHECK();
   BSA_CUDA_TRY(cudaMemsetAsync(W.counter, 0, 8, st));  // main + repair launch counters
   TcArgs a;
+  a.kr = kr;
+  a.part_out = W.part_out;
+  a.part_bf16 = part_bf16;
+  a.part_lse = W.part_lse;
   a.qp = W.qp;
   a.kp = W.kp;
   a.vp = W.vp;
@@ -441,7 +683,8 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   a.bits = mask_bits;
   a.counts = counts;
   a.items = W.items;
-  a.n_items = (int32_t)(G.H * (nst + G.nq));
+  a.n_items = (int32_t)W.cap;
+  a.n_items_dev = W.n_items;
   a.work_counter = W.counter;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.shard = shard;
@@ -450,7 +693,6 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   a.ovf_flags = W.ovf_flags;
   a.ovf_list = W.ovf_list;
   a.ovf_count = W.ovf_count;
-  a.n_items_dev = nullptr;
   a.scatter_world = scatter ? scatter->world : 0;
   a.out_ptrs = scatter ? reinterpret_cast<const unsigned long long*>(scatter->out_ptrs) : nullptr;
   a.token_begin = scatter ? scatter->token_begin : nullptr;
@@ -462,7 +704,20 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
     BSA_CUDA_TRY(cudaMemsetAsync(tbuf, 0, tbytes, st));
     a.trace = tbuf;
   }
-  return launch_tc_attention(G, a, st);
+  CombineArgs c;
+  c.kr = kr;
+  c.part_out = W.part_out;
+  c.part_bf16 = part_bf16;
+  c.part_lse = W.part_lse;
+  c.row_shard = num_shards > 1 ? W.row_shard : nullptr;
+  c.shard = shard;
+  c.out = out;
+  c.out_bf16 = a.out_bf16;
+  c.permuted_out = inputs_permuted;
+  c.scatter_world = a.scatter_world;
+  c.out_ptrs = a.out_ptrs;
+  c.token_begin = a.token_begin;
+  return launch_tc_attention(G, a, st, &c);
 }
 
 int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,

@@ -53,6 +53,15 @@ namespace tc {
 #ifndef BSA_TC_NB
 #define BSA_TC_NB 6
 #endif
+// PAIR: 128-key S tiles.  Two consecutive 64-key chunks of an item's key
+// stream share one K stage (16 KB, contiguous: one N=128 S MMA), one S/P
+// buffer of 128 TMEM columns, one S commit and one PV commit.  The softmax
+// still works per 64-key chunk (group (g + c) % NG takes chunk c, a tile's
+// two chunks go to two groups); the S/PV issuers and the K producer do half
+// as many barrier round trips per key.
+#ifndef BSA_TC_PAIR
+#define BSA_TC_PAIR 0
+#endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
 #endif
@@ -80,7 +89,10 @@ constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 template <bool WIDE>
 struct Cfg {
   static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warp groups (4 warps: the 4 lane quarters)
-  static constexpr int NB = WIDE ? BSA_TC_NB : 2;  // S buffers (64 columns, P over S)
+  static constexpr bool PAIR = WIDE && BSA_TC_PAIR != 0;  // 128-key S tiles
+  static constexpr int TCH = PAIR ? 2 : 1;                // 64-key chunks per S tile
+  static constexpr uint32_t S_COLS = 64 * TCH;            // TMEM columns per S/P buffer
+  static constexpr int NB = PAIR ? 3 : (WIDE ? BSA_TC_NB : 2);  // S buffers (P over S)
   static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
   static constexpr int SM_WARPS = 4 * NG;
   // SPLIT: S MMAs and PV MMAs come from two issuer warps (one warp issuing
@@ -98,18 +110,19 @@ struct Cfg {
   // every 4th warp of the SM's CTAs (8-register granules)
   static constexpr int WARPS_PER_SMSP = (CTAS_PER_SM * NUM_THREADS / 32 + 3) / 4;
   static constexpr int MAX_REGS = (16384 / (32 * WARPS_PER_SMSP)) / 8 * 8;
-  static constexpr int NK = WIDE ? 8 : 5, NV = WIDE ? (LSUM ? 6 : 10) : 4;
+  static constexpr int NK = PAIR ? 4 : (WIDE ? 8 : 5), NV = WIDE ? (LSUM ? 6 : 10) : 4;
+  static constexpr int K_STAGE = TCH * CHUNK_BYTES;  // one S tile of K
   static constexpr int VLAG = 2;  // (one producer warp) K(j) is loaded VLAG tiles before V(j)
   static constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ ones block)
   static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
+  static constexpr int OFF_V = OFF_K + NK * K_STAGE;
   static constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // [3][NG][128] floats
   static constexpr int OFF_QUEUE = OFF_XCH + 3 * NG * BQ * 4;  // (SPLIT) [2][QUEUE] int32
   static constexpr int OFF_BAR = OFF_QUEUE + (SPLIT ? 2 * QUEUE * 4 : 0);
   static constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
   static constexpr uint32_t TMEM_COLS = WIDE ? 512 : 256;
-  // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last)
-  static constexpr uint32_t TM_S = 0, TM_O = NB * 64, TM_Q = TMEM_COLS - 32;
+  // TMEM: S0..S(NB-1) (S_COLS columns each, P over S) | O (80) | Q (32, last)
+  static constexpr uint32_t TM_S = 0, TM_O = NB * S_COLS, TM_Q = TMEM_COLS - 32;
   // barrier slots (8 bytes each) inside the barrier region
   static constexpr int B_QFULL = 0;              // [1]  Q in TMEM (all softmax warps)
   static constexpr int B_KFULL = 1;              // [NK]
@@ -124,7 +137,7 @@ struct Cfg {
   static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
   static constexpr int B_IEMPTY = B_IFULL + 2;   // [2]  softmax warps + MMA warp(s)
   static constexpr int B_COUNT = B_IEMPTY + 2;
-  static_assert(B_COUNT * 8 + 96 <= 1024, "barrier region");
+  static_assert(B_COUNT * 8 + 100 <= 1024, "barrier region (+ item ring, TMEM address)");
   static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
   static_assert(TM_O + O_COLS <= TM_Q, "TMEM columns");
   static_assert(LEAD >= 1 && LEAD < NB, "S(j+LEAD) must only wait for a PV issued earlier");
@@ -207,7 +220,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   constexpr int SM_WARPS = C::SM_WARPS;
   // warps that write one tile's P: one group (stale max, whole tiles), or
   // both groups (exact max, column halves of every tile)
-  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4;
+  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4 * C::TCH;
+  constexpr bool PAIR = C::PAIR;
+  constexpr uint32_t S_COLS = C::S_COLS;
   static_assert(!EXACT || NG == 2, "the exact launch splits tiles into two column halves");
   (void)tm_q;  // Q goes to TMEM from the softmax warps' registers
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -219,17 +234,19 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   // decodes (two dependent global loads) while it waits for the slot, so the
   // other warps start the next item without those loads.
   volatile int32_t* item_ring = (volatile int32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT);
-  uint32_t* tmem_holder = (uint32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT + 80);
+  uint32_t* tmem_holder = (uint32_t*)(smem + C::OFF_BAR + 8 * C::B_COUNT + 96);
   auto ring_put = [&](uint32_t slot, int32_t code, const Item& I) {
-    volatile int32_t* r = item_ring + slot * 9;
+    volatile int32_t* r = item_ring + slot * 11;
     r[0] = code;
     r[1] = I.h; r[2] = I.qb; r[3] = I.row0; r[4] = I.rows;
     r[5] = I.nchunks; r[6] = I.last_len; r[7] = I.nsc; r[8] = I.spec_last;
+    r[9] = I.r; r[10] = I.kstart;
   };
   auto ring_get = [&](uint32_t slot, Item& I) -> int32_t {
-    volatile int32_t* r = item_ring + slot * 9;
+    volatile int32_t* r = item_ring + slot * 11;
     I.h = r[1]; I.qb = r[2]; I.row0 = r[3]; I.rows = r[4];
     I.nchunks = r[5]; I.last_len = r[6]; I.nsc = r[7]; I.spec_last = r[8];
+    I.r = r[9]; I.kstart = r[10];
     return r[0];
   };
   float* xch = (float*)(smem + C::OFF_XCH);  // [3][NG][128]: first-tile max, tile max, l
@@ -284,10 +301,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  int64_t n_work;
-  if (EXACT) n_work = *A.n_items_dev;
-  else n_work = A.num_shards > 1 ? (A.n_items - A.shard + A.num_shards - 1) / A.num_shards
-                                 : A.n_items;
+  // the schedule kernel (main launch) or the overflow list (repair launch)
+  // leaves the item count on the device
+  const int64_t n_work = *A.n_items_dev;
 
   if (C::SPLIT && (warp == C::PRODUCER_WARP || warp == C::VPROD_WARP)) {
     // ======================= K / V producers (SPLIT; one elected lane issues) ===
@@ -297,7 +313,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     // the per-tile cost is one queue read, one barrier wait and one TMA.
     const bool is_k = warp == C::PRODUCER_WARP;
     int32_t* queue = reinterpret_cast<int32_t*>(smem + C::OFF_QUEUE) + (is_k ? 0 : C::QUEUE);
-    uint32_t it = 0, gx = 0;
+    uint32_t it = 0, gx = 0, gt = 0;  // chunks, (PAIR, K) S tiles
     while (true) {
       const uint32_t slot = it & 1;
       int32_t code;
@@ -307,8 +323,8 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         if (lane == 0) w = atomicAdd(A.work_counter, 1);
         w = __shfl_sync(0xffffffffu, w, 0);
         code = -1;
-        if (w < n_work) code = A.items[A.num_shards > 1 ? w * A.num_shards + A.shard : w];
-        if (code >= 0) I = decode(G, code, A.counts, A.bits);
+        if (w < n_work) code = A.items[w];
+        if (code >= 0) I = decode(G, code, A.counts, A.bits, A.kr);
         mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
         if (elect_one()) {
           ring_put(slot, code, I);
@@ -324,9 +340,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       if (code < 0) break;
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
-      const int64_t nbytes = I.qb >= 0 ? G.mask_row_bytes : 0;
-      int64_t pos = 0, bp = 0;
-      const int64_t end = I.qb < 0 ? G.T : G.Ts;
+      // contiguous keys [kstart, end), then the mask bytes [bp, nbytes) of
+      // this item's key range
+      const int64_t rbytes = (int64_t)A.kr.rb / 8;
+      const int64_t nbytes =
+          I.qb >= 0 ? min((int64_t)G.mask_row_bytes, (int64_t)(I.r + 1) * rbytes) : 0;
+      int64_t pos = I.kstart, bp = (int64_t)I.r * rbytes;
+      const int64_t end = contig_end(I);
       int qh = 0, qt = 0;
       for (int j = 0; j < I.nchunks; ++j) {
         if (qh == qt) {
@@ -366,7 +386,20 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           __syncwarp();
         }
         const int32_t s0 = queue[qh++];
-        if (is_k) {
+        if (is_k && PAIR) {
+          // chunk pairs (j, j+1) fill one 16 KB stage: rows 0-63 and 64-127
+          // of the N=128 B operand
+          const uint32_t st = gt % NK;
+          const int half = j & 1;
+          if (half == 0) mbar_wait(BAR(C::B_KEMPTY + st), ((gt / NK) & 1) ^ 1);
+          if (elect_one()) {
+            if (half == 0)
+              mbar_expect_tx(BAR(C::B_KFULL + st), (I.nchunks - j >= 2 ? 2 : 1) * CHUNK_BYTES);
+            tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE + half * CHUNK_BYTES, &tm_k,
+                        BAR(C::B_KFULL + st), 0, s0, I.h);
+          }
+          if (half == 1 || j == I.nchunks - 1) ++gt;
+        } else if (is_k) {
           const uint32_t st = gx % NK;
           if (lane == 0) BSA_TR(9, gx);
           mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
@@ -402,10 +435,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       if (lane == 0) w = atomicAdd(A.work_counter, 1);
       w = __shfl_sync(0xffffffffu, w, 0);
       int32_t code = -1;
-      if (w < n_work)
-        code = A.items[(!EXACT && A.num_shards > 1) ? w * A.num_shards + A.shard : w];
+      if (w < n_work) code = A.items[w];
       Item I;
-      if (code >= 0) I = decode(G, code, A.counts, A.bits);
+      if (code >= 0) I = decode(G, code, A.counts, A.bits, A.kr);
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IEMPTY + slot), ((it >> 1) & 1) ^ 1);
       if (elect_one()) {
@@ -416,7 +448,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       if (code < 0) break;
       const uint8_t* mrow =
           I.qb >= 0 ? A.bits + ((int64_t)I.h * G.nq + I.qb) * G.mask_row_bytes : nullptr;
-      KeyChunker ck(G, I.qb, mrow, CH);
+      const int64_t rbytes = (int64_t)A.kr.rb / 8;
+      KeyChunker ck(G, I.qb, mrow, CH, I.kstart, contig_end(I), (int64_t)I.r * rbytes,
+                    (int64_t)(I.r + 1) * rbytes);
       auto load_v = [&](int32_t s0) {
         const uint32_t st = gv % NV;
         mbar_wait(BAR(C::B_VEMPTY + st), ((gv / NV) & 1) ^ 1);
@@ -465,6 +499,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     uint32_t sk = 0, kph = 0, sb = 0, sph = 0;  // S issue: K stage, S buffer (+ phases)
     uint32_t pb = 0, pph = 0, sv = 0, vph = 0;  // PV issue: P buffer, V stage
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
+    const uint32_t id_s2 = idesc_f16(128, 128, 0, 1);                // (PAIR) two chunks
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
     const uint64_t dk0 = sdesc(sbase + C::OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + C::OFF_V, 8192, 1024);
@@ -542,7 +577,56 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
         if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
       };
-      if constexpr (C::SPLIT) {
+      // PAIR: one S MMA (N = 64 * chunks) per tile of up to two chunks; the
+      // PV of each chunk reads its own V stage, one PFREE commit per tile
+      auto issue_s_pair = [&](int nch) {
+        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR(C::B_PFREE + sb), sph ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dk = dk0 + (uint64_t)(sk * (C::K_STAGE >> 4));
+          const uint32_t ds = tmem + C::TM_S + sb * S_COLS;
+          const uint32_t id = nch == 2 ? id_s2 : id_s;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k)
+            mma_ts(ds, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id, k > 0 ? 1u : 0u);
+          tc_commit(BAR(C::B_SFULL + sb));
+          tc_commit(BAR(C::B_KEMPTY + sk));
+        }
+        __syncwarp();
+        if (++sk == (uint32_t)NK) { sk = 0; kph ^= 1; }
+        if (++sb == (uint32_t)NB) { sb = 0; sph ^= 1; }
+      };
+      auto issue_pv_pair = [&](int jt, int nch) {
+        mbar_wait2(BAR(C::B_PFULL + pb), pph, BAR(C::B_VFULL + sv), vph);
+        if (jt == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
+        tc_fence_after();
+        for (int h = 0; h < nch; ++h) {
+          if (h > 0) {
+            mbar_wait(BAR(C::B_VFULL + sv), vph);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+            const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
+            const uint32_t pa = tmem + C::TM_S + pb * S_COLS + h * 64;
+#pragma unroll
+            for (int k = 0; k < CH / 16; ++k)
+              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv,
+                     (jt > 0 || h > 0 || k > 0) ? 1u : 0u);
+            tc_commit(BAR(C::B_VEMPTY + sv));
+            if (h == nch - 1) tc_commit(BAR(C::B_PFREE + pb));
+          }
+          __syncwarp();
+          if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
+        }
+        if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
+      };
+      if constexpr (PAIR) {
+        for (int jt = 0; 2 * jt < ntiles; ++jt) {
+          const int nch = ntiles - 2 * jt >= 2 ? 2 : 1;
+          if (do_s) issue_s_pair(nch);
+          else issue_pv_pair(jt, nch);
+        }
+      } else if constexpr (C::SPLIT) {
         if (do_s) {
           for (int j = 0; j < ntiles; ++j) issue_s();
         } else {
@@ -577,15 +661,25 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     float* x_first = xch;              // [NG][128]
     float* x_tile = xch + NG * BQ;     // [NG][128] (EXACT)
     float* x_l = xch + 2 * NG * BQ;    // [NG][128] (EXACT)
-    // TMEM column of keys 32*hh..32*hh+31 of tile gg's S
-    auto s_half_col = [&](uint32_t gg, int hh) -> uint32_t {
-      return C::TM_S + (gg % NB) * 64 + hh * 32;
+    // S/P buffer, its phase, and the first TMEM column of chunk j of the
+    // current item (g: the item's first global chunk; PAIR, gt: its first
+    // global 128-key tile, chunk j is half j & 1 of tile gt + j / 2)
+    uint32_t it = 0, g = 0, gt = 0;
+    struct ChunkSlot {
+      uint32_t buf, phase, col;
+    };
+    auto slot_of = [&](int j) -> ChunkSlot {
+      ChunkSlot z;
+      const uint32_t t = PAIR ? gt + (uint32_t)(j >> 1) : g + (uint32_t)j;
+      z.buf = t % NB;
+      z.phase = (t / NB) & 1;
+      z.col = C::TM_S + z.buf * S_COLS + (PAIR ? (uint32_t)(j & 1) * 64 : 0u);
+      return z;
     };
     // the NG warps sharing this TMEM lane quarter
     auto quarter_sync = [&]() {
       asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "n"(32 * NG) : "memory");
     };
-    uint32_t it = 0, g = 0;
     while (true) {
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
@@ -628,15 +722,15 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         const int first_grp = (int)(g % NG);  // group that owns the item's tile 0
         if (grp == first_grp) {
           // tile 0's row max becomes the item's offset
-          const uint32_t sb = g % NB;
-          mbar_wait(BAR(C::B_SFULL + sb), (g / NB) & 1);
+          const ChunkSlot z = slot_of(0);
+          mbar_wait(BAR(C::B_SFULL + z.buf), z.phase);
           tc_fence_after();
           const int len0 = chunk_len(I, 0);
           float mx = NEG_INF;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             uint32_t sr[32];
-            const uint32_t s_col = tmem + lane_off + s_half_col(g, hh);
+            const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
             tmem_ld16(s_col + 16, &sr[16]);
             tmem_wait_ld();
@@ -652,10 +746,12 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         quarter_sync();
         m = x_first[row] * sl2;
         for (int j = (grp - first_grp + NG) % NG; j < ntiles; j += NG) {
-          const uint32_t gg = g + j, sb = gg % NB;
+          const uint32_t gg = g + j;
+          const ChunkSlot z = slot_of(j);
+          const uint32_t sb = z.buf;
           const int len = chunk_len(I, j);
           if (lane == 0 && quarter == 0) BSA_TR(4, gg);
-          mbar_wait(BAR(C::B_SFULL + sb), (gg / NB) & 1);
+          mbar_wait(BAR(C::B_SFULL + sb), z.phase);
           tc_fence_after();
           if (lane == 0 && quarter == 0) BSA_TR(8, gg);
 #pragma unroll
@@ -663,7 +759,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             // 32 keys at a time; their P (16 packed columns) goes over S
             // columns this thread has already read
             uint32_t sr[32];
-            const uint32_t s_col = tmem + lane_off + s_half_col(gg, hh);
+            const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
             tmem_ld16(s_col + 16, &sr[16]);
             tmem_wait_ld();
@@ -677,7 +773,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
-            const uint32_t p_col = tmem + lane_off + C::TM_S + sb * 64 + hh * 16;
+            const uint32_t p_col = tmem + lane_off + z.col + hh * 16;
 #if BSA_TC_EXPERIMENT == 1
             {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
@@ -698,7 +794,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(BAR(C::B_PFULL + sb));
+            // (PAIR) a tile holding one chunk completes with this group alone
+            if (PAIR && (j & 1) == 0 && j == ntiles - 1) mbar_arrive_cnt(BAR(C::B_PFULL + sb), 2);
+            else mbar_arrive(BAR(C::B_PFULL + sb));
             if (quarter == 0) BSA_TR(16, gg);
           }
         }
@@ -790,16 +888,22 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       const bool store = row < I.rows;
       const int32_t pr = I.row0 + row;
       const int64_t dst = A.permuted_out ? pr : G.L.part_src(pr);
-      // output row: local (H, T, d) buffer, or (multi-GPU scatter) the buffer
-      // of the rank owning token dst, (H, T_r, d), written over NVLink
-      __nv_bfloat16* orow_bf16 = (__nv_bfloat16*)A.out + ((int64_t)I.h * G.T + dst) * D;
-      if (A.scatter_world > 0 && store) {
+      // output row: local (H, T, d) buffer; (multi-GPU scatter) the buffer of
+      // the rank owning token dst, (H, T_r, d), written over NVLink; or (key
+      // ranges) this range's partial row, partitioned order, merged later
+      const bool part = A.kr.nr > 1;
+      const bool obf = part ? A.part_bf16 != 0 : A.out_bf16 != 0;
+      const int64_t orow = part ? ((int64_t)I.r * G.H + I.h) * G.T + pr : (int64_t)I.h * G.T + dst;
+      __nv_bfloat16* orow_bf16 = (__nv_bfloat16*)(part ? A.part_out : A.out) + orow * D;
+      float* orow_f32 = (float*)(part ? A.part_out : A.out) + orow * D;
+      if (!part && A.scatter_world > 0 && store) {
         int r = 0;
         while (r + 1 < A.scatter_world && dst >= A.token_begin[r + 1]) ++r;
         const int64_t t0 = A.token_begin[r], tr = A.token_begin[r + 1] - t0;
         orow_bf16 = (__nv_bfloat16*)A.out_ptrs[r] + ((int64_t)I.h * tr + (dst - t0)) * D;
       }
       const float inv = (F16P ? __int_as_float((127 - A.v_shift[I.h]) << 23) : 1.0f) / ltot;
+      if (part && store && grp == 0) A.part_lse[orow] = m + log2f(ltot);
       // 16-column chunks c with c % NG == grp
       for (int c = grp; c < 4; c += NG) {
         const int col0 = c * 16;
@@ -808,7 +912,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         tmem_wait_ld();
         reg_fence16(orr);
         if (store) {
-          if (A.out_bf16) {
+          if (obf) {
             uint4* op = reinterpret_cast<uint4*>(orow_bf16 + col0);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
@@ -820,7 +924,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               op[q] = v;
             }
           } else {
-            float4* op = reinterpret_cast<float4*>((float*)A.out + ((int64_t)I.h * G.T + dst) * D + col0);
+            float4* op = reinterpret_cast<float4*>(orow_f32 + col0);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               op[q] = make_float4(__uint_as_float(orr[4 * q]) * inv, __uint_as_float(orr[4 * q + 1]) * inv,
@@ -840,6 +944,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
       }
       g += ntiles;
+      gt += (ntiles + 1) / 2;
       ++it;
     }
   }
@@ -934,10 +1039,13 @@ static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
   }
 }
 
-// Two launches: the stale-max kernel over the (sharded) LPT list, then the
-// exact-max kernel over the items it listed as overflowed (normally none: the
-// second launch reads a zero count and its CTAs exit at once).
-int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
+// Two launches: the stale-max kernel over this shard's LPT list (its length
+// is on the device, written by the schedule kernel), then the exact-max
+// kernel over the items it listed as overflowed (normally none: the second
+// launch reads a zero count and its CTAs exit at once).  With a key-range
+// split, the combine kernel then merges each row's range partials.
+int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
+                        const CombineArgs* comb) {
   CUtensorMap mk, mv;
   CUtensorMap mq;
   int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);  // unused by the kernel (Q goes via registers)
@@ -949,11 +1057,8 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   int dev = 0, sms = 148;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t n_work = a.num_shards > 1
-                             ? (a.n_items - a.shard + a.num_shards - 1) / a.num_shards
-                             : a.n_items;
-  const int grid =
-      (int)std::min<int64_t>((int64_t)sms * tc::CfgMain::CTAS_PER_SM, std::max<int64_t>(1, n_work));
+  const int grid = (int)std::min<int64_t>((int64_t)sms * tc::CfgMain::CTAS_PER_SM,
+                                          std::max<int64_t>(1, a.n_items));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_flags, 0, (size_t)a.n_items * 4, st));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_count, 0, 4, st));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
@@ -963,10 +1068,12 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st) {
   r.items = a.ovf_list;
   r.n_items_dev = a.ovf_count;
   r.work_counter = a.work_counter + 1;
-  r.num_shards = 1;
-  r.shard = 0;
   rc = launch_pick<true>(mq, mk, mv, G, r, sms, st);
   if (rc) return rc;
+  if (a.kr.nr > 1 && comb) {
+    rc = launch_combine(G, *comb, st);
+    if (rc) return rc;
+  }
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));
   if (a.trace) {
     // debug only: dump the CTA-0 pipeline trace (BSA_TC_TRACE=<file>)

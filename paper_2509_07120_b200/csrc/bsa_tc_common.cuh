@@ -73,6 +73,9 @@ __device__ __forceinline__ void mbar_wait2(uint32_t a, uint32_t pa, uint32_t b, 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
@@ -231,41 +234,60 @@ struct Item {
   int32_t last_len; // length of the final tile (ragged tails)
   int32_t nsc;      // leading contiguous tiles (special strip / all keys)
   int32_t spec_last;  // length of the last contiguous tile
+  int32_t r;        // key range (KeyRanges; 0 when the keys are not split)
+  int32_t kstart;   // first key of the contiguous part of the stream
 };
 
+// item code = (h * nr + r) * M + li, M = ceil(Ts / BQ) + nq; li < ceil(Ts/BQ)
+// is a special-row tile, else patch q-block li - ceil(Ts/BQ).
 // 32-bit fields: the tensor-core path requires T < 2^31 and H < 65536.
 __device__ __forceinline__ Item decode(const AttnGeom& G, int32_t code, const int32_t* counts,
-                                       const uint8_t* bits) {
+                                       const uint8_t* bits, const KeyRanges& KR) {
   Item it;
   const int32_t nst = (int32_t)ceil_div(G.Ts, BQ);
   const int32_t M = nst + (int32_t)G.nq;
   const int32_t T = (int32_t)G.T, Ts = (int32_t)G.Ts, Tp = (int32_t)G.Tp;
-  it.h = code / M;
-  const int32_t li = code - it.h * M;
+  const int32_t hr = code / M;
+  const int32_t li = code - hr * M;
+  it.h = hr / KR.nr;
+  it.r = hr - it.h * KR.nr;
+  const int32_t rkeys = KR.rb * CH;
   if (li < nst) {
     it.qb = -1;
     it.row0 = li * BQ;
     it.rows = min(BQ, Ts - it.row0);
-    it.nsc = (T + CH - 1) / CH;
-    it.spec_last = T - (it.nsc - 1) * CH;
+    // keys [kstart, kend): range 0 also holds the special keys
+    it.kstart = it.r == 0 ? 0 : Ts + it.r * rkeys;
+    const int32_t kend = it.r == KR.nr - 1 ? T : Ts + (it.r + 1) * rkeys;
+    const int32_t len = kend - it.kstart;
+    it.nsc = (len + CH - 1) / CH;
+    it.spec_last = len - (it.nsc - 1) * CH;
     it.nchunks = it.nsc;
     it.last_len = it.spec_last;
   } else {
     it.qb = li - nst;
     it.row0 = Ts + it.qb * BQ;
     it.rows = min(BQ, Tp - it.qb * BQ);
-    it.nsc = (Ts + CH - 1) / CH;
+    it.kstart = 0;
+    it.nsc = it.r == 0 ? (Ts + CH - 1) / CH : 0;
     it.spec_last = it.nsc ? Ts - (it.nsc - 1) * CH : CH;
-    const int32_t cnt = counts[(int64_t)it.h * G.nq + it.qb];
+    const int64_t row = (int64_t)it.h * G.nq + it.qb;
+    const int32_t cnt = KR.nr == 1 ? counts[row] : KR.rcounts[row * KR.nr + it.r];
     it.nchunks = it.nsc + cnt;
-    // the ragged last patch block, if selected, is always the final tile
+    // the ragged last patch block, if selected (and in this range), is
+    // always the final tile
     const int32_t lastb = (int32_t)G.nk - 1;
-    const uint8_t lb = bits[((int64_t)it.h * G.nq + it.qb) * G.mask_row_bytes + (lastb >> 3)];
-    const bool last_sel = (lb >> (lastb & 7)) & 1;
+    const uint8_t lb = bits[row * G.mask_row_bytes + (lastb >> 3)];
+    const bool last_sel = ((lb >> (lastb & 7)) & 1) && lastb / KR.rb == it.r;
     it.last_len = last_sel ? Tp - lastb * CH : CH;
     if (cnt == 0) it.last_len = it.spec_last;
   }
   return it;
+}
+
+// end of the contiguous part of an item's key stream
+__device__ __forceinline__ int32_t contig_end(const Item& it) {
+  return it.nsc ? it.kstart + (it.nsc - 1) * CH + it.spec_last : it.kstart;
 }
 
 __device__ __forceinline__ int chunk_len(const Item& it, int c) {

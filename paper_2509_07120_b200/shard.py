@@ -344,11 +344,49 @@ def _assemble(parts, plan: ShardPlan) -> torch.Tensor:
     return torch.cat(pieces, dim=1)
 
 
+class _Staging:
+    """Local stand-in for ScatterTarget (combine="reduce_scatter"): one zeroed
+    (world, heads, max_rows, d) buffer per head chunk; the epilogue stores
+    every row into slice r = the owning rank's, and one NCCL reduce-scatter
+    (sum of disjoint rows: exact) hands each rank its slice."""
+
+    def __init__(self, plan: ShardPlan, heads: int, head_dim: int, device,
+                 dtype=torch.bfloat16):
+        self.world, self.heads, self.head_dim = plan.world, heads, head_dim
+        self.rows = [plan.token_range(r)[1] - plan.token_range(r)[0] for r in range(plan.world)]
+        self.starts = [plan.token_range(r)[0] for r in range(plan.world)]
+        self.max_rows = max(self.rows)
+        self.buf = torch.zeros((plan.world, heads, self.max_rows, head_dim), dtype=dtype,
+                               device=device)
+        tb = [plan.token_range(r)[0] for r in range(plan.world)] + [plan.layout.total_tokens]
+        self.token_begin = torch.tensor(tb, dtype=torch.int64, device=device)
+        self._ptrs = torch.tensor([self.buf[r].data_ptr() for r in range(plan.world)],
+                                  dtype=torch.int64, device=device)
+
+    def chunk_ptrs(self, head0: int) -> torch.Tensor:
+        del head0  # one staging buffer per chunk
+        return self._ptrs
+
+
+def _reduce_scatter(buf: torch.Tensor, rank: int, group):
+    """Sum-reduce-scatter of (world, ...) along dim 0 -> this rank's slice.
+    Backends without reduce-scatter for these tensors (gloo on CUDA) fall
+    back to an all-reduce of the whole buffer."""
+    recv = torch.empty_like(buf[0])
+    try:
+        work = dist.reduce_scatter_tensor(recv, buf, op=dist.ReduceOp.SUM, group=group,
+                                          async_op=True)
+        return work, recv
+    except (RuntimeError, NotImplementedError):
+        work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True)
+        return work, buf[rank]
+
+
 def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *, group=None,
                              inputs: str = "sharded", ops=None, return_mask: bool = False,
                              chunk_heads: int | None = None, comm_group=None,
-                             combine: str = "allreduce", scatter_target=None,
-                             validate: bool = True):
+                             combine: str = "auto", scatter_target=None,
+                             validate: bool = True, chunk_ready=None, out_host=None):
     """One block-sparse global-attention layer over every rank of `group`.
 
     inputs="sharded":    q/k/v are this rank's frames (ShardPlan.frame_range);
@@ -359,26 +397,44 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
     chunk_heads: pipeline the layer over chunks of heads (heads are
     independent through the whole path). The Q/K/V all-gathers of every
     chunk start at once, asynchronously, on `group`. Each chunk's mask
-    all-gather and output all-reduce go on `comm_group` (default: `group`;
+    all-gather and output combine go on `comm_group` (default: `group`;
     pass a second communicator so they do not queue behind the big
     gathers). So communication overlaps the previous chunks' kernels.
     Results are bit-identical to the unchunked call.
 
-    combine="scatter" (sharded inputs, DeviceOps): the kernel epilogue writes
-    every output row straight into the owning rank's buffer over NVLink
-    (ScatterTarget; pass a persistent one to reuse the IPC mapping across
-    layers). No output all-reduce is needed. Returns this rank's rows.
-    Reusing a target is safe: a peer's next-layer kernel cannot start before
-    its Q/K/V all-gathers, which this rank only joins after it has copied
-    the previous layer's rows out of the buffer (same stream order).
+    combine (how each rank gets its own frames' rows):
+      "scatter" (default for sharded inputs on the device path): the kernel
+        epilogue writes every output row straight into the owning rank's
+        buffer over NVLink (ScatterTarget; pass a persistent one to reuse
+        the IPC mapping across layers). A one-element all-reduce per chunk
+        fences the ranks. Reusing a target is safe: a peer's next-layer
+        kernel cannot start before its Q/K/V all-gathers, which this rank
+        only joins after it has copied the previous layer's rows out of the
+        buffer (same stream order).
+      "reduce_scatter": the epilogue writes rows into a local staging
+        buffer sliced by owner; one NCCL reduce-scatter per chunk.
+      "allreduce": zero-filled full outputs, NCCL sum all-reduce (the only
+        choice for inputs="replicated").
+
+    chunk_ready: one CUDA event per head chunk; the chunk's gathers wait for
+    it (host-to-device copies of the inputs overlapping earlier chunks).
+    out_host: (sharded inputs) a host (ideally pinned) tensor for this
+    rank's rows; each chunk is copied out on a side stream as soon as it is
+    combined. The call then returns out_host after a synchronize.
     """
     if inputs not in ("sharded", "replicated"):
         raise ValueError(f"inputs must be 'sharded' or 'replicated', got {inputs!r}")
-    if combine not in ("allreduce", "scatter"):
-        raise ValueError(f"combine must be 'allreduce' or 'scatter', got {combine!r}")
-    if combine == "scatter" and inputs != "sharded":
-        raise ValueError("combine='scatter' returns this rank's frames: needs inputs='sharded'")
+    if combine not in ("auto", "allreduce", "scatter", "reduce_scatter"):
+        raise ValueError("combine must be 'auto', 'scatter', 'reduce_scatter' or 'allreduce', "
+                         f"got {combine!r}")
     ops = ops or DeviceOps()
+    if combine == "auto":
+        combine = ("scatter" if inputs == "sharded" and hasattr(ops, "attend_scatter")
+                   and q.device.type == "cuda" else "allreduce")
+    if combine in ("scatter", "reduce_scatter") and inputs != "sharded":
+        raise ValueError(f"combine={combine!r} returns this rank's frames: needs inputs='sharded'")
+    if out_host is not None and inputs != "sharded":
+        raise ValueError("out_host holds this rank's frames: needs inputs='sharded'")
     rank, world = _rank_world(group)
     g = policy.geometry
     plan = ShardPlan(layout, world, g.block_q, g.block_k)
@@ -394,13 +450,21 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
             f"inputs have {q.shape[1]} tokens but layout describes {layout.total_tokens}")
     chunk = chunk_heads or H
     spans = [(a, min(H, a + chunk)) for a in range(0, H, chunk)]
+    if chunk_ready is not None and len(chunk_ready) != len(spans):
+        raise ValueError(f"chunk_ready has {len(chunk_ready)} events for {len(spans)} chunks")
+    if out_host is not None and tuple(out_host.shape) != (H, t1 - t0, q.shape[2]):
+        raise ValueError(f"out_host must be {(H, t1 - t0, q.shape[2])}, got {tuple(out_host.shape)}")
     cgroup = comm_group if comm_group is not None else group
     if combine == "scatter" and scatter_target is not None:
         scatter_target.check_matches(plan, H, q.shape[2], rank)
+    cur = torch.cuda.current_stream(q.device) if q.device.type == "cuda" else None
     if validate:
         # once per call, on this rank's inputs (as_f32, tensorio.py:47-59);
         # a rank's verdict is shared so that every rank raises together
         from . import _native as N
+        if chunk_ready is not None and cur is not None:
+            for ev in chunk_ready:
+                cur.wait_event(ev)
         ok = torch.tensor([1.0 if N.all_finite(q, k, v) else 0.0], device=q.device)
         if world > 1:
             dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
@@ -408,13 +472,35 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
             raise ValueError("q/k/v contain non-finite values")
 
     own_target = False
+    if combine == "scatter" and scatter_target is None:
+        scatter_target = ScatterTarget(plan, H, q.shape[2], rank, group, q.device)
+        own_target = True
     pending = []
     if inputs == "sharded" and world > 1:
         # every chunk's Q/K/V gathers start now; chunk c's kernels only wait
         # for chunk c's gathers
-        for a, b in spans:
+        for c, (a, b) in enumerate(spans):
+            if chunk_ready is not None:
+                cur.wait_event(chunk_ready[c])
             pending.append([_gather_async(x[a:b], plan, group) for x in (q, k, v)])
-    outs, masks, reduces = [], [], []
+    elif chunk_ready is not None and cur is not None:
+        for ev in chunk_ready:
+            cur.wait_event(ev)
+    copy_stream = torch.cuda.Stream(q.device) if out_host is not None else None
+    outs, masks, combines = [], [], []
+
+    def emit(c, a, b, work, rows):
+        """Chunk c's rows of this rank are final once `work` completes:
+        keep them, and start their device-to-host copy if asked."""
+        combines.append((work, rows))
+        if out_host is not None:
+            with torch.cuda.stream(copy_stream):
+                if work is not None:
+                    work.wait()
+                else:
+                    copy_stream.wait_stream(cur)
+                out_host[a:b].copy_(rows, non_blocking=True)
+
     for c, (a, b) in enumerate(spans):
         if inputs == "sharded" and world > 1:
             full = []
@@ -426,32 +512,48 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
             qf, kf, vf = q[a:b], k[a:b], v[a:b]
         mask = sharded_predict_mask(qf, kf, layout, policy, plan, rank, cgroup, ops)
         if combine == "scatter":
-            if scatter_target is None:
-                scatter_target = ScatterTarget(plan, H, q.shape[2], rank, group, q.device)
-                own_target = True
             ops.attend_scatter(qf, kf, vf, layout, mask, rank, world, scatter_target, head0=a)
+            # every rank's kernels for this chunk (and so its peer stores into
+            # our buffer) are complete once this tiny all-reduce completes
+            work = (dist.all_reduce(torch.zeros(1, device=q.device), group=cgroup, async_op=True)
+                    if world > 1 else None)
+            emit(c, a, b, work, scatter_target.local[a:b])
+        elif combine == "reduce_scatter":
+            if hasattr(ops, "attend_scatter"):
+                st = _Staging(plan, b - a, q.shape[2], q.device)
+                ops.attend_scatter(qf, kf, vf, layout, mask, rank, world, st, head0=a)
+            else:  # any ops: slice a full local output into the owners' slots
+                out = ops.attend(qf, kf, vf, layout, mask, rank, world)
+                st = _Staging(plan, b - a, q.shape[2], q.device, out.dtype)
+                for r in range(world):
+                    st.buf[r, :, :st.rows[r]] = out[:, st.starts[r]:st.starts[r] + st.rows[r]]
+            if world > 1:
+                work, mine = _reduce_scatter(st.buf, rank, cgroup)
+            else:
+                work, mine = None, st.buf[0]
+            emit(c, a, b, work, mine[:, :t1 - t0])
         else:
             out = ops.attend(qf, kf, vf, layout, mask, rank, world)
-            if world > 1:
-                reduces.append(dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup,
-                                               async_op=True))
-            outs.append(out)
+            work = (dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup, async_op=True)
+                    if world > 1 else None)
+            emit(c, a, b, work, out[:, t0:t1] if inputs == "sharded" else out)
         masks.append(mask)
-    for work in reduces:
-        work.wait()
-    if combine == "scatter":
-        if world > 1:
-            # every rank's kernels (and so its peer stores into our buffer)
-            # are complete once this tiny all-reduce completes
-            dist.all_reduce(torch.zeros(1, device=q.device), group=cgroup)
+    for work, _ in combines:
+        if work is not None:
+            work.wait()
+    if out_host is not None:
+        cur.wait_stream(copy_stream)
+        cur.synchronize()
+        out = out_host
+    elif combine == "scatter":
         out = scatter_target.local.clone()
-        if own_target:
-            torch.cuda.current_stream().synchronize()
-            scatter_target.close(group)
     else:
-        out = outs[0] if len(outs) == 1 else torch.cat(outs, dim=0)
-        if inputs == "sharded":
-            out = out[:, t0:t1].contiguous()
+        rows = [r for _, r in combines]
+        out = rows[0] if len(rows) == 1 else torch.cat(rows, dim=0)
+        out = out.contiguous()
+    if own_target:
+        torch.cuda.current_stream(q.device).synchronize()
+        scatter_target.close(group)
     if not return_mask:
         return out
     if len(masks) == 1:

@@ -86,23 +86,29 @@ def attention_path(job: SparseAttentionJob, path: str = "auto") -> str:
     return "tc" if code == N.PATH_TC else "simt"
 
 
+def _flags(path: str, timing: bool, key_ranges: int) -> int:
+    if not 0 <= int(key_ranges) <= 255:
+        raise ValueError(f"key_ranges must be in [0, 255], got {key_ranges}")
+    return _PATHS[path] | (N.FLAG_TIMING if timing else 0) | (int(key_ranges) << 8)
+
+
 def _run(q, k, v, out, layout, mask: BlockMask, bits, counts, scale, inputs_permuted, shard,
-         num_shards, path, ws=None, timing=False):
+         num_shards, path, ws=None, timing=False, key_ranges=0):
     g = mask.geometry
     L = N.lib()
     lay = N.layout_desc(layout)
     in_code = N.BSA_BF16 if q.dtype == torch.bfloat16 else N.BSA_F32
     out_code = N.BSA_BF16 if out.dtype == torch.bfloat16 else N.BSA_F32
+    flags = _flags(path, timing, key_ranges)
     need = L.bsa_sparse_attention_workspace(lay, q.shape[0], q.shape[2], g.block_q, g.block_k,
-                                            in_code, int(inputs_permuted), _PATHS[path])
+                                            in_code, int(inputs_permuted), flags)
     if ws is None or ws.numel() < need or ws.device != q.device:
         ws = N.workspace(need, q.device)
     with N.on_device(q.device):
         N.check(L.bsa_sparse_attention(
             N.tensor_desc(q), N.tensor_desc(k), N.tensor_desc(v), out.data_ptr(), out_code, lay,
             g.block_q, g.block_k, bits.data_ptr(), N.ptr(counts), np.float32(scale).item(),
-            int(inputs_permuted), int(shard), int(num_shards),
-            _PATHS[path] | (N.FLAG_TIMING if timing else 0), ws.data_ptr(), ws.numel(),
+            int(inputs_permuted), int(shard), int(num_shards), flags, ws.data_ptr(), ws.numel(),
             N.stream_ptr()), "sparse_attention")
     return ws
 
@@ -133,13 +139,16 @@ def last_kernel_ms() -> float:
 def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PANEL_BLOCKS,
                      threads: int = 1, inputs_permuted: bool = False, out_dtype=None,
                      path: str = "auto", shard: int = 0, num_shards: int = 1, out=None,
-                     workspace=None, timing: bool = False):
+                     workspace=None, timing: bool = False, key_ranges: int = 0):
     """Run the block-sparse kernel; returns (heads, tokens, head_dim).
 
     Inputs arrive in interleaved source order and the result comes back in
     that order; with ``inputs_permuted=True`` both are [specials | patches].
-    ``shard``/``num_shards`` compute only that slice of the LPT work list
-    (multi-GPU); other rows of ``out`` are left untouched.
+    ``shard``/``num_shards`` compute only that shard's rows (every
+    num_shards-th row of each head's LPT order; multi-GPU); other rows of
+    ``out`` are left untouched.  ``key_ranges`` (tensor-core path): 0 picks
+    the key-range split automatically (heads whose K/V outgrow L2 are cut
+    into L2-sized key ranges, merged by log-sum-exp), n forces n ranges.
     """
     del panel_blocks, threads
     inp = job.inputs
@@ -155,7 +164,7 @@ def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PAN
         out = alloc(q.shape, dtype=out_dtype, device=q.device)
     bits = job.mask.device_bits(q.device)
     _run(q, k, v, out, job.layout, job.mask, bits, job.mask.device_counts(q.device), inp.scale,
-         inputs_permuted, shard, num_shards, path, workspace, timing)
+         inputs_permuted, shard, num_shards, path, workspace, timing, key_ranges)
     if inp.numpy_io:
         return out.float().cpu().numpy()
     return out

@@ -99,6 +99,54 @@ class GlobalAttentionStack:
 
     __call__ = forward
 
+    def forward_sharded(self, x_local: torch.Tensor, layout: TokenLayout, policy: MaskPolicy, *,
+                        group=None, comm_group=None, combine: str = "auto",
+                        chunk_heads: int | None = None, ops=None) -> torch.Tensor:
+        """The stack with the frames split over the ranks of `group` (config 3
+        at 2/4/8 GPUs): each rank holds the tokens of its frames
+        (ShardPlan.token_range), shape (T_r, C).  LayerNorm, the QKV / output
+        projections, the residual and the MLP act per token and run locally;
+        the global attention is shard.sharded_sparse_attention (NCCL
+        all-gather of Q/K/V, row-split scoring, every rank attends its share
+        of each head's rows, rows returned to their owners).  With the
+        scatter combine one ScatterTarget (CUDA IPC mapping) serves every
+        layer.  Returns this rank's (T_r, C) output; with one rank it equals
+        forward() bit for bit."""
+        from .shard import ScatterTarget, ShardPlan, _rank_world, sharded_sparse_attention
+
+        rank, world = _rank_world(group)
+        plan = ShardPlan(layout, world, policy.geometry.block_q, policy.geometry.block_k)
+        t0, t1 = plan.token_range(rank)
+        if x_local.shape != (t1 - t0, self.dim):
+            raise ValueError(f"rank {rank} must hold ({t1 - t0}, {self.dim}) tokens, "
+                             f"got {tuple(x_local.shape)}")
+        H, d, C = self.heads, self.head_dim, self.dim
+        Tr = t1 - t0
+        target = None
+        if combine in ("auto", "scatter") and ops is None and x_local.device.type == "cuda":
+            combine = "scatter"
+            target = ScatterTarget(plan, H, d, rank, group, x_local.device)
+        x = x_local
+        try:
+            for blk in self.blocks:
+                h = F.layer_norm(x, (C,), blk.ln_w, blk.ln_b)
+                qkv = F.linear(h, blk.qkv_w, blk.qkv_b).view(Tr, 3, H, d).permute(1, 2, 0, 3)
+                o = sharded_sparse_attention(qkv[0], qkv[1], qkv[2], layout, policy, group=group,
+                                             inputs="sharded", ops=ops, chunk_heads=chunk_heads,
+                                             comm_group=comm_group, combine=combine,
+                                             scatter_target=target)
+                o = o.permute(1, 0, 2).reshape(Tr, C)
+                x = x + F.linear(o, blk.proj_w, blk.proj_b)
+                if blk.mlp is not None:
+                    lw, lb, w1, b1, w2, b2 = blk.mlp
+                    hm = F.layer_norm(x, (C,), lw, lb)
+                    x = x + F.linear(F.gelu(F.linear(hm, w1, b1)), w2, b2)
+        finally:
+            if target is not None:
+                torch.cuda.current_stream(x_local.device).synchronize()
+                target.close(group)
+        return x
+
     def layer_statistics(self, x: torch.Tensor, layout: TokenLayout,
                          policy: MaskPolicy | None = None, mode: str = "sparse") -> list[dict]:
         """The paper's per-layer attention analysis (§4.x "Visualizing

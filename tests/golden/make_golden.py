@@ -26,6 +26,8 @@ sys.path.insert(0, os.path.dirname(HERE))  # tests/
 
 from golden_inputs import (  # noqa: E402
     CASES_ATTN,
+    CASES_FULL,
+    FULL_POLICIES,
     CASES_MAP,
     CASES_SCORE,
     SCORE_POLICIES,
@@ -77,6 +79,31 @@ def score_case(name, frames, patches, specials, heads, d, seed, block_q, block_k
         out[f"mask{i}_tau_rho"] = np.array([tau, rho])
     np.savez_compressed(os.path.join(HERE, f"score_{name}.npz"), **out)
     print(f"score_{name}: nq={g.nq_blocks} nk={g.nk_blocks} ({time.time() - t0:.1f}s)")
+
+
+def full_case(name, frames, patches, specials, heads, d, seed, bf16):
+    """Headline size: digests of the reference's pooled Q/K, probabilities and
+    masks (two policies) plus the per-row selected-block counts."""
+    t0 = time.time()
+    lay = TokenLayout(frames, patches, specials)
+    q, k, _ = make_qkv(heads, lay.total_tokens, d, seed)
+    if bf16:
+        q, k = bf16_round(q), bf16_round(k)
+    pidx = patch_token_indices(lay)
+    qp_in, kp_in = np.ascontiguousarray(q[:, pidx]), np.ascontiguousarray(k[:, pidx])
+    g = BlockGeometry(lay.patch_tokens, 128, 64)
+    qp, kp = block_pool(qp_in, 128), block_pool(kp_in, 64)
+    probs = pooled_scores(qp, kp, d)
+    out = dict(frames=frames, patches=patches, specials=specials, heads=heads, d=d, seed=seed,
+               bf16=bf16, qp_sha=sha(qp), kp_sha=sha(kp), probs_sha=sha(probs))
+    for i, (tau, rho) in enumerate(FULL_POLICIES):
+        m = predict_mask(qp_in, kp_in, MaskPolicy(tau, rho, g)).blocks
+        bits = np.packbits(m.reshape(-1, m.shape[2]), axis=1, bitorder="little")
+        out[f"mask{i}_sha"] = sha(bits)
+        out[f"mask{i}_counts"] = m.sum(axis=2).astype(np.uint16)
+        out[f"mask{i}_tau_rho"] = np.array([tau, rho])
+    np.savez_compressed(os.path.join(HERE, f"full_{name}.npz"), **out)
+    print(f"full_{name}: nq={g.nq_blocks} nk={g.nk_blocks} ({time.time() - t0:.1f}s)")
 
 
 def attn_case(name, frames, patches, specials, heads, d, seed, block_q, block_k, tau, rho,
@@ -147,6 +174,9 @@ def main():
     for c in CASES_MAP:
         if not only or c["name"] in only:
             map_case(**c)
+    for c in CASES_FULL:
+        if not only or c["name"] in only:
+            full_case(**c)
 
 
 if __name__ == "__main__":

@@ -33,6 +33,18 @@ CASES_SCORE = [
          block_q=64, block_k=32),
 ]
 
+# the headline size (BASELINE metric: N=200 frames, VGGT tokens), 2 heads: the
+# reference's masks and probabilities are stored as SHA-256 digests plus the
+# per-row counts (the bits themselves are 2.3 MB of incompressible noise).
+# bf16=True: inputs rounded to bf16 first (what the bf16 device path reads).
+CASES_FULL = [
+    dict(name="n200h2", frames=200, patches=1369, specials=5, heads=2, d=64, seed=5,
+         bf16=False),
+    dict(name="n200h2_bf16", frames=200, patches=1369, specials=5, heads=2, d=64, seed=6,
+         bf16=True),
+]
+FULL_POLICIES = [(0.0, 0.75), (0.4, 0.8)]
+
 CASES_ATTN = [
     dict(name="small_spec", frames=2, patches=300, specials=5, heads=2, d=64, seed=21,
          block_q=128, block_k=64, tau=0.4, rho=0.8),

@@ -44,8 +44,16 @@ def _sample_rows(lay, bq=128):
     return sorted(set(int(perm[p]) for p in part))
 
 
-def _check_rows(bsa, lay, q, k, v, mask, out, heads):
-    rows = _sample_rows(lay)
+def _row_rel(got, ref):
+    """max over rows of ||o - ref|| / ||ref||: a row with small outputs cannot
+    hide behind the tensor's global max."""
+    num = np.linalg.norm((got - ref).reshape(-1, got.shape[-1]), axis=1)
+    den = np.linalg.norm(ref.reshape(-1, ref.shape[-1]), axis=1)
+    return float((num / np.maximum(den, 1e-30)).max())
+
+
+def _check_rows(bsa, lay, q, k, v, mask, out, heads, rows=None):
+    rows = _sample_rows(lay) if rows is None else rows
     for h in heads:
         qh, kh, vh = (t[h:h + 1].float().cpu().numpy() for t in (q, k, v))
         ref = oracle.masked_attention_f64(qh, kh, vh, lay.frames, lay.patches_per_frame,
@@ -54,6 +62,7 @@ def _check_rows(bsa, lay, q, k, v, mask, out, heads):
         got = out[h:h + 1, rows].float().cpu().numpy()
         err = np.abs(got - ref).max() / np.abs(ref).max()
         assert err <= BF16_REL_TOL, f"head {h}: rel err {err}"
+        assert _row_rel(got, ref) <= BF16_REL_TOL, f"head {h}: per-row rel err"
 
 
 def test_bench_workload_n200(bsa):
@@ -135,3 +144,66 @@ def test_host_pipeline_full_size_equals_device_path(bsa):
     hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
     out = HostLayerPipeline(16, lay.total_tokens, 64).run(hq, hk, hv, lay, pol)
     assert torch.equal(out, ref.cpu())
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["n200h2", "n200h2_bf16"])
+def test_headline_masks_match_reference_fixture(bsa, name):
+    """N=200 frames (the headline size), 2 heads: pooled Q/K, probabilities
+    and masks for tau=0/rho=0.75 and tau=0.4/rho=0.8 equal the REFERENCE's
+    own (tests/golden/make_golden.py ran bsattn.predict_mask at this size;
+    maskpred.py:104-194), digest for digest; fp32 inputs and bf16 inputs."""
+    import os
+
+    import torch
+    from golden_inputs import FULL_POLICIES, bf16_round, make_qkv
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", f"full_{name}.npz"))
+    lay = bsa.TokenLayout(int(z["frames"]), int(z["patches"]), int(z["specials"]))
+    q, k, _ = make_qkv(int(z["heads"]), lay.total_tokens, int(z["d"]), int(z["seed"]))
+    dt = torch.float32
+    if bool(z["bf16"]):
+        q, k, dt = bf16_round(q), bf16_round(k), torch.bfloat16
+    qd, kd = (torch.from_numpy(x).to("cuda", dt) for x in (q, k))
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    pidx = torch.from_numpy(bsa.patch_token_indices(lay)).cuda()
+    assert _sha(bsa.block_pool(qd[:, pidx], 128).cpu().numpy()) == str(z["qp_sha"])
+    assert _sha(bsa.block_pool(kd[:, pidx], 64).cpu().numpy()) == str(z["kp_sha"])
+    for i, (tau, rho) in enumerate(FULL_POLICIES):
+        mask, probs = bsa.predict_mask(qd, kd, bsa.MaskPolicy(tau, rho, g), layout=lay,
+                                       return_probs=True)
+        if i == 0:
+            assert _sha(probs.cpu().numpy()) == str(z["probs_sha"])
+        assert np.array_equal(mask.device_counts().cpu().numpy().reshape(z[f"mask{i}_counts"].shape),
+                              z[f"mask{i}_counts"])
+        assert _sha(mask.device_bits().cpu().numpy()) == str(z[f"mask{i}_sha"]), (tau, rho)
+
+
+def test_bench_workload_all_heads(bsa):
+    """The bench workload itself (N=200, 16 heads, tau=0, rho=0.75, bf16):
+    all 16 heads' masks bit-exact against the C restatement; per head one
+    whole q-block (128 rows) and, for heads 0 and 1, all 1000 special rows
+    against the float64 oracle, per row and globally."""
+    import torch
+    lay, q, k, v = _inputs(bsa, 200, 16, 0)
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    mask = bsa.predict_mask(q, k, bsa.MaskPolicy(0.0, 0.75, g), layout=lay)
+    pidx = torch.from_numpy(bsa.patch_token_indices(lay)).cuda()
+    qp, kp = (t[:, pidx].float().cpu().numpy() for t in (q, k))
+    om, _ = oracle.predict_mask(qp, kp, 128, 64, 0.0, 0.75)
+    assert np.array_equal(om, mask.blocks), "N=200 16-head mask differs from the oracle"
+    out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask))
+    perm, _ = oracle.partition_perm(lay.frames, lay.patches_per_frame, lay.specials_per_frame)
+    ns = lay.special_tokens
+    rng = np.random.default_rng(0)
+    for h in range(16):
+        qb = int(rng.integers(g.nq_blocks))
+        part = list(range(ns + qb * 128, ns + min((qb + 1) * 128, lay.patch_tokens)))
+        if h < 2:
+            part += list(range(ns))
+        _check_rows(bsa, lay, q, k, v, mask, out, heads=(h,),
+                    rows=sorted(int(perm[p]) for p in part))

@@ -182,3 +182,64 @@ def test_world1_scatter_combine(bsa):
             sharded_sparse_attention(q, k, v, lay, pol, combine="scatter", inputs="replicated")
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("combine", ["allreduce", "scatter"])
+def test_emulated_8_ranks_config5(bsa, combine):
+    """BASELINE config 5's split at its size: N=1000 frames, rho=0.75, 2 heads,
+    8 emulated ranks on one GPU. Each rank scores its q-block rows and
+    attends its share of every head's LPT rows (the automatic key-range
+    split engages at this size); the combined output and the gathered mask
+    must be bit-identical to the single-GPU call."""
+    import torch
+    from paper_2509_07120_b200.shard import DeviceOps, ShardPlan
+
+    world = 8
+    lay = bsa.TokenLayout(1000, 1369, 5)
+    H, T, d = 2, lay.total_tokens, 64
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v = (torch.randn((H, T, d), generator=gen, device="cuda").to(torch.bfloat16)
+               for _ in range(3))
+    pol = bsa.MaskPolicy(0.0, 0.75, bsa.BlockGeometry(lay.patch_tokens, 128, 64))
+    ref_mask = bsa.predict_mask(q, k, pol, layout=lay)
+    ref = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, ref_mask))
+
+    ops = DeviceOps()
+    plan = ShardPlan(lay, world)
+    qp, kp = ops.pool(q, lay, 128), ops.pool(k, lay, 64)
+    bits, counts = [], []
+    for r in range(world):
+        qb0, qb1 = plan.qblock_range(r)
+        b, c = ops.score_rows(qp[:, qb0:qb1], kp, d, pol)
+        bits.append(b)
+        counts.append(c)
+    bits = torch.cat(bits, dim=1).reshape(-1, bits[0].shape[2])
+    counts = torch.cat(counts, dim=1).reshape(-1)
+    assert torch.equal(bits, ref_mask.device_bits()), "row-split scoring changed the mask"
+    assert torch.equal(counts, ref_mask.device_counts())
+    mask = bsa.BlockMask._from_device(bits, counts, H, pol.geometry)
+
+    if combine == "allreduce":
+        acc = torch.zeros_like(ref)
+        for r in range(world):
+            acc += ops.attend(q, k, v, lay, mask, r, world)  # the sum all-reduce
+        assert torch.equal(acc, ref)
+    else:
+        bufs = [torch.full((H, plan.token_range(r)[1] - plan.token_range(r)[0], d), float("nan"),
+                           dtype=torch.bfloat16, device="cuda") for r in range(world)]
+
+        class Target:  # ScatterTarget's pointer table, minus the IPC
+            pass
+        t = Target()
+        t.world = world
+        t.token_begin = torch.tensor([plan.token_range(r)[0] for r in range(world)] + [T],
+                                     dtype=torch.int64, device="cuda")
+        t.chunk_ptrs = lambda head0: torch.tensor(
+            [b.data_ptr() + head0 * b.shape[1] * d * 2 for b in bufs], dtype=torch.int64,
+            device="cuda")
+        for r in range(world):
+            ops.attend_scatter(q, k, v, lay, mask, r, world, t)
+        torch.cuda.synchronize()
+        for r in range(world):
+            t0, t1 = plan.token_range(r)
+            assert torch.equal(bufs[r], ref[:, t0:t1]), f"rank {r} rows differ"

@@ -65,3 +65,36 @@ def test_layer_statistics_match_materialised_maps():
             np.testing.assert_allclose(r["maxes"][quad], ref.maxes[quad], rtol=2e-3)
         assert 0.0 < r["recall"] <= 1.0
         x = x + st.attention(x, blk, lay, None, "dense")
+
+
+def test_stack_forward_sharded_world1_equals_forward():
+    """Config 3's multi-GPU form (frames split over the ranks) through a real
+    NCCL group of one rank: bit-identical to the single-GPU stack, for the
+    scatter (persistent IPC target) and reduce-scatter combines."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_07120_b200 import TokenLayout
+    from paper_2509_07120_b200.stack import GlobalAttentionStack, policy_for
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        lay = TokenLayout(3, 700, 5)
+        stack = GlobalAttentionStack(layers=3, seed=2, mlp=True)
+        g = torch.Generator(device="cuda").manual_seed(5)
+        x = torch.randn((lay.total_tokens, stack.dim), generator=g, device="cuda").to(torch.bfloat16)
+        pol = policy_for(lay, 0.4, 0.8)
+        ref = stack(x, lay, pol, "sparse")
+        for combine, chunk in (("auto", None), ("reduce_scatter", 4), ("allreduce", None)):
+            y = stack.forward_sharded(x, lay, pol, combine=combine, chunk_heads=chunk)
+            assert torch.equal(y, ref), combine
+        with pytest.raises(ValueError):
+            stack.forward_sharded(x[:-1], lay, pol)
+    finally:
+        dist.destroy_process_group()

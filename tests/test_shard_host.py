@@ -81,7 +81,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, inputs, result_q, chunk=None):
+def _worker(rank, world, port, inputs, result_q, chunk=None, combine="auto"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -97,17 +97,18 @@ def _worker(rank, world, port, inputs, result_q, chunk=None):
         else:
             xs = [torch.from_numpy(x) for x in (q, k, v)]
         out, mask = sharded_sparse_attention(*xs, lay, pol, inputs=inputs, ops=OracleOps(),
-                                             return_mask=True, chunk_heads=chunk)
+                                             return_mask=True, chunk_heads=chunk,
+                                             combine=combine)
         result_q.put((rank, out.numpy(), mask.blocks.copy()))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, inputs, chunk=None):
+def _run(world, inputs, chunk=None, combine="auto"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, inputs, q, chunk))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, inputs, q, chunk, combine))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -150,6 +151,20 @@ def test_head_chunked_pipeline_matches(single_process):
     for r, (out, blocks) in res.items():
         assert np.array_equal(blocks, mask)
         t0, t1 = plan.token_range(r)
+        np.testing.assert_allclose(out, ref[:, t0:t1], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("world,chunk", [(2, None), (3, 1)])
+def test_reduce_scatter_combine(world, chunk, single_process):
+    """combine="reduce_scatter": rows staged by owner, one NCCL-style
+    reduce-scatter (sum of disjoint rows) per head chunk."""
+    lay, mask, ref = single_process
+    res = _run(world, "sharded", chunk=chunk, combine="reduce_scatter")
+    plan = ShardPlan(lay, world, BQ, BK)
+    for r, (out, blocks) in res.items():
+        assert np.array_equal(blocks, mask)
+        t0, t1 = plan.token_range(r)
+        assert out.shape == (H, t1 - t0, D)
         np.testing.assert_allclose(out, ref[:, t0:t1], rtol=0, atol=1e-12)
 
 
