@@ -84,6 +84,13 @@ def parse():
     ap.add_argument("--e2e-chunk", default="auto",
                     help="head chunks of the host-memory e2e leg: 'auto' (1,3,4,..,4,3,1), "
                          "heads per chunk, or a comma list of chunk sizes")
+    ap.add_argument("--mask", default="predicted", choices=["predicted", "ragged"],
+                    help="predicted: predict_mask + sparse_attention per step (the headline); "
+                         "ragged: a fixed random mask with per-row block counts uniform in "
+                         "[0.5, 2] x k_floor, attention only (the LPT schedule's case; the "
+                         "reference's bench_sweep does not time scoring either)")
+    ap.add_argument("--schedule", default="lpt", choices=["lpt", "natural"],
+                    help="work-item order of the tensor-core kernel (natural = row order)")
     ap.add_argument("--specials", type=int, default=S_PER_FRAME,
                     help="special tokens per frame (VGGT 5; pi3: 4 register tokens, no camera)")
     a = ap.parse_args()
@@ -209,6 +216,27 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def ragged_mask(bsa, heads, g, k_floor, seed, dev):
+    """Per (head, q-block) row a random set of c key blocks, c uniform in
+    [0.5, 2] x k_floor (clamped to [1, nk]): ragged rows for the LPT
+    schedule, built on the device (random scores, per-row k-th value)."""
+    import torch
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed + 77)
+    rows, nk = heads * g.nq_blocks, g.nk_blocks
+    c = torch.randint(max(1, k_floor // 2), min(nk, 2 * k_floor) + 1, (rows,), generator=gen,
+                      device=dev)
+    r = torch.rand((rows, nk), generator=gen, device=dev)
+    kth = torch.sort(r, dim=1, descending=True).values.gather(1, (c - 1)[:, None])
+    sel = r >= kth
+    pad = (-nk) % 8
+    if pad:
+        sel = torch.cat([sel, sel.new_zeros((rows, pad))], dim=1)
+    w = (1 << torch.arange(8, device=dev, dtype=torch.int32))
+    bits = (sel.view(rows, -1, 8).to(torch.int32) * w).sum(dim=2).to(torch.uint8)
+    return bsa.BlockMask._from_device(bits.contiguous(), sel.sum(dim=1).to(torch.int32), heads, g)
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -250,15 +278,17 @@ def run_ours(a):
     else:
         q_in, k_in, v_in = q, k, v
 
+    fixed_mask = ragged_mask(bsa, H, g, pol.min_blocks, a.seed, dev) if a.mask == "ragged" else None
+
     def step(qq, kk, vv, timing=False):
         if sharded:
             return sharded_sparse_attention(qq, kk, vv, lay, pol, inputs="sharded",
                                             return_mask=True, chunk_heads=a.shard_chunk,
                                             comm_group=comm, combine=a.combine,
                                             scatter_target=target)
-        mask = bsa.predict_mask(qq, kk, pol, layout=lay)
+        mask = fixed_mask or bsa.predict_mask(qq, kk, pol, layout=lay)
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
-        return bsa.sparse_attention(job, timing=timing), mask
+        return bsa.sparse_attention(job, timing=timing, schedule=a.schedule), mask
 
     def barrier():
         if world > 1:
@@ -290,15 +320,19 @@ def run_ours(a):
     for _ in range(a.steps if not sharded else 0):
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        mask = bsa.predict_mask(q, k, pol, layout=lay)
+        mask = fixed_mask or bsa.predict_mask(q, k, pol, layout=lay)
         s1.record(stream)
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask)
-        bsa.sparse_attention(job, timing=True)
+        bsa.sparse_attention(job, timing=True, schedule=a.schedule)
         kern_ms.append(sp.last_kernel_ms())
         score_ms.append(s0.elapsed_time(s1))
     # sharded mode: per-GPU share of the layer's work over the whole step
     kernel_ms = float(np.mean(kern_ms)) if kern_ms else ms_step * world
     area = mask.selected_area().astype(np.int64)
+    row_blocks = None
+    if a.mask == "ragged":
+        cnt = mask.device_counts().float()
+        row_blocks = {"min": int(cnt.min()), "max": int(cnt.max()), "mean": float(cnt.mean())}
     Ts, Tp = lay.special_tokens, lay.patch_tokens
     # algorithmic work: 2 GEMMs (QK^T, PV) x 2 flop/MAC over allowed entries
     flops = int(sum(4 * d * (Ts * T + Tp * Ts + int(ar)) for ar in area))
@@ -418,7 +452,13 @@ def run_ours(a):
             "higher_is_better": True, "scaling": "strong" if sharded else "weak",
             "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded Gaussian Q/K/V, VGGT token layout)",
-            "config": workload_config(a, {"block_density": density}),
+            "config": workload_config(a, dict({"block_density": density},
+                                              **({"mask": "ragged rows, [0.5, 2] x k_floor "
+                                                  "random blocks (attention only)",
+                                                  "row_blocks": row_blocks}
+                                                 if a.mask == "ragged" else {}),
+                                              **({"schedule": a.schedule}
+                                                 if a.schedule != "lpt" else {}))),
             "stages_ms": ({"predict_mask": float(np.mean(score_ms)),
                            "attention_kernel": kernel_ms} if not sharded else None),
             "dense_baseline": {"ms_per_layer": dense_ms, "backend": dense_backend,

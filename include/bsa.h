@@ -48,6 +48,9 @@ extern "C" {
  * head's K+V outgrows L2, e.g. N=1000 frames), n = n ranges whose partials
  * are merged by log-sum-exp (results equal within rounding) */
 #define BSA_FLAG_RANGES(n) (((n) & 0xFF) << 8)
+/* tensor-core path: keep each head's work items in row order instead of the
+ * LPT (longest-first) order -- for measuring what the LPT order buys */
+#define BSA_FLAG_NATURAL_ORDER 32
 #define BSA_FLAG_RANGES_GET(f) (((f) >> 8) & 0xFF)
 
 /* TokenLayout (layout.py:27-66): F frames of S specials + P patches. */

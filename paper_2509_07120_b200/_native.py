@@ -22,6 +22,7 @@ BSA_OK, BSA_EINVAL, BSA_EUNSUPPORTED, BSA_ECUDA = 0, 1, 2, 3
 BSA_F32, BSA_BF16 = 0, 1
 PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
 FLAG_TIMING = 16
+FLAG_NATURAL_ORDER = 32
 
 _DTYPE_CODE = {torch.float32: BSA_F32, torch.bfloat16: BSA_BF16}
 

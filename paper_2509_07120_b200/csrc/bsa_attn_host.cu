@@ -133,6 +133,7 @@ struct SchedGeom {
   int64_t nq, nst, M, nsc, T, Ts;
   int32_t nr, rb;
   int64_t max_cost;
+  int32_t lpt;  // 0: every row costs the same (row order; BSA_FLAG_NATURAL_ORDER)
 };
 
 // chunks of row tile li of head h in key range r (0: no keys there)
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(1024)
     auto cost = [&](int64_t i) -> int64_t {
       if (num_shards > 1 && rs[i] != shard) return -1;
       const int64_t c = range_cost(S, counts, rcounts, h, i, r);
-      return c > 0 ? c : -1;
+      return c > 0 ? (S.lpt ? c : 1) : -1;
     };
     n += lpt_place(S.M, S.max_cost, hist, cost, list + n, (int32_t)((h * S.nr + r) * S.M));
   }
@@ -655,6 +656,7 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   S.nr = kr.nr;
   S.rb = kr.rb;
   S.max_cost = std::max<int64_t>(ceil_div(G.T, 64) + kr.nr, S.nsc + G.nk);
+  S.lpt = (flags & BSA_FLAG_NATURAL_ORDER) ? 0 : 1;
   const size_t hsmem = (size_t)(S.max_cost + 1) * 4;
   if (hsmem > 200 * 1024) return fail(BSA_EUNSUPPORTED, "sequence too long for the scheduler");
   BSA_CUDA_TRY(cudaFuncSetAttribute(schedule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -45,7 +45,8 @@ namespace bsa {
 namespace tc {
 
 #ifndef BSA_TC_EXPERIMENT
-#define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs
+#define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs, 3 = no
+                             // exp-argument FFMA2, 4 = no poly clamp
 #endif
 #ifndef BSA_TC_WIDE
 #define BSA_TC_WIDE 1
@@ -61,6 +62,12 @@ namespace tc {
 // as many barrier round trips per key.
 #ifndef BSA_TC_PAIR
 #define BSA_TC_PAIR 0
+#endif
+// HALFPV: the softmax group publishes P per 32-key half (one more barrier
+// per half) and the PV issuer runs keys 0-31 as soon as the first half is
+// written, so the PV of a tile overlaps the exps of its second half
+#ifndef BSA_TC_HALFPV
+#define BSA_TC_HALFPV 0
 #endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
@@ -131,7 +138,9 @@ struct Cfg {
   static constexpr int B_VEMPTY = B_VFULL + NV;  // [NV]
   static constexpr int B_SFULL = B_VEMPTY + NV;  // [NB]
   static constexpr int B_PFULL = B_SFULL + NB;   // [NB] the warps of the tile
-  static constexpr int B_PFREE = B_PFULL + NB;   // [NB] PV done: S/P buffer reusable
+  static constexpr bool HALFPV = WIDE && !PAIR && BSA_TC_HALFPV != 0;
+  static constexpr int B_PFULL0 = B_PFULL + NB;  // [NB] (HALFPV) first half of P written
+  static constexpr int B_PFREE = B_PFULL0 + (HALFPV ? NB : 0);  // [NB] PV done: buffer reusable
   static constexpr int B_OFULL = B_PFREE + NB;   // [1]
   static constexpr int B_OEMPTY = B_OFULL + 1;   // [1]
   static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
@@ -177,7 +186,9 @@ __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float
   uint32_t r[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
+    // (timing experiment 3: the argument straight from S, no scale / offset)
+    const float2 x = BSA_TC_EXPERIMENT == 3 ? make_float2(s[2 * e], s[2 * e + 1])
+                                            : __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
     float2 p;
     if (poly_pair<POLY>(e)) p = exp2_poly2<F16P ? 3 : BSA_TC_POLY_DEG>(x);
     else p = make_float2(ex2(x.x), ex2(x.y));
@@ -258,6 +269,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     for (int i = 0; i < NB; ++i) {
       mbar_init(BAR(C::B_SFULL + i), 1);
       mbar_init(BAR(C::B_PFULL + i), TILE_WARPS);
+      if (C::HALFPV) mbar_init(BAR(C::B_PFULL0 + i), TILE_WARPS);
       mbar_init(BAR(C::B_PFREE + i), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -554,11 +566,31 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         mbar_wait(BAR(C::B_VFULL + sv), vph);
         if (lane == 0) BSA_TR(5, gp);
 #else
-        mbar_wait2(BAR(C::B_PFULL + pb), pph, BAR(C::B_VFULL + sv), vph);
+        mbar_wait2(BAR((C::HALFPV ? C::B_PFULL0 : C::B_PFULL) + pb), pph, BAR(C::B_VFULL + sv), vph);
 #endif
         if (jj == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
-        if (elect_one()) {
+        if (C::HALFPV) {
+          // keys 0-31 now (P half 0), keys 32-63 once half 1 is written
+          const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
+          const uint32_t pa = tmem + C::TM_S + pb * 64;
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv,
+                     (jj > 0 || k > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+          mbar_wait(BAR(C::B_PFULL + pb), pph);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 2; k < 4; ++k)
+              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv, 1u);
+            tc_commit(BAR(C::B_PFREE + pb));
+            tc_commit(BAR(C::B_VEMPTY + sv));
+          }
+        } else if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
           const uint32_t pa = tmem + C::TM_S + pb * 64;
           // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
@@ -788,6 +820,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               l += lt;
             }
 #endif
+            if (C::HALFPV && hh == 0) {
+              // publish P half 0: the PV issuer starts keys 0-31
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR(C::B_PFULL0 + sb));
+            }
           }
           if (lane == 0 && quarter == 0) BSA_TR(12, gg);
           tmem_wait_st();

@@ -302,8 +302,10 @@ __device__ __forceinline__ int chunk_len(const Item& it, int c) {
 // below the 2^-9 rounding of a bf16 P, one f32x2 FMA cheaper.
 template <int DEG>
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
+#if !defined(BSA_TC_EXPERIMENT) || BSA_TC_EXPERIMENT != 4
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
+#endif
   const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
   const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));

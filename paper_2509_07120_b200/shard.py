@@ -373,9 +373,9 @@ def _reduce_scatter(buf: torch.Tensor, rank: int, group):
     Backends without reduce-scatter for these tensors (gloo on CUDA) fall
     back to an all-reduce of the whole buffer."""
     recv = torch.empty_like(buf[0])
-    try:
-        work = dist.reduce_scatter_tensor(recv, buf, op=dist.ReduceOp.SUM, group=group,
-                                          async_op=True)
+    try:  # flat views: every backend splits the input's dim 0 into world parts
+        work = dist.reduce_scatter_tensor(recv.view(-1), buf.view(-1), op=dist.ReduceOp.SUM,
+                                          group=group, async_op=True)
         return work, recv
     except (RuntimeError, NotImplementedError):
         work = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True)
@@ -519,19 +519,24 @@ def sharded_sparse_attention(q, k, v, layout: TokenLayout, policy: MaskPolicy, *
                     if world > 1 else None)
             emit(c, a, b, work, scatter_target.local[a:b])
         elif combine == "reduce_scatter":
+            # slot r holds rank r's rows as a contiguous (heads, rows_r, d)
+            # block at its start (the epilogue's per-rank addressing)
             if hasattr(ops, "attend_scatter"):
                 st = _Staging(plan, b - a, q.shape[2], q.device)
                 ops.attend_scatter(qf, kf, vf, layout, mask, rank, world, st, head0=a)
-            else:  # any ops: slice a full local output into the owners' slots
+            else:  # any ops: copy a full local output into the owners' slots
                 out = ops.attend(qf, kf, vf, layout, mask, rank, world)
                 st = _Staging(plan, b - a, q.shape[2], q.device, out.dtype)
                 for r in range(world):
-                    st.buf[r, :, :st.rows[r]] = out[:, st.starts[r]:st.starts[r] + st.rows[r]]
+                    n_r = (b - a) * st.rows[r] * q.shape[2]
+                    st.buf[r].view(-1)[:n_r] = \
+                        out[:, st.starts[r]:st.starts[r] + st.rows[r]].reshape(-1)
             if world > 1:
                 work, mine = _reduce_scatter(st.buf, rank, cgroup)
             else:
                 work, mine = None, st.buf[0]
-            emit(c, a, b, work, mine[:, :t1 - t0])
+            n_me = (b - a) * (t1 - t0) * q.shape[2]
+            emit(c, a, b, work, mine.reshape(-1)[:n_me].view(b - a, t1 - t0, q.shape[2]))
         else:
             out = ops.attend(qf, kf, vf, layout, mask, rank, world)
             work = (dist.all_reduce(out, op=dist.ReduceOp.SUM, group=cgroup, async_op=True)

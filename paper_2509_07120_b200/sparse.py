@@ -86,20 +86,23 @@ def attention_path(job: SparseAttentionJob, path: str = "auto") -> str:
     return "tc" if code == N.PATH_TC else "simt"
 
 
-def _flags(path: str, timing: bool, key_ranges: int) -> int:
+def _flags(path: str, timing: bool, key_ranges: int, schedule: str = "lpt") -> int:
     if not 0 <= int(key_ranges) <= 255:
         raise ValueError(f"key_ranges must be in [0, 255], got {key_ranges}")
-    return _PATHS[path] | (N.FLAG_TIMING if timing else 0) | (int(key_ranges) << 8)
+    if schedule not in ("lpt", "natural"):
+        raise ValueError(f"schedule must be 'lpt' or 'natural', got {schedule!r}")
+    return (_PATHS[path] | (N.FLAG_TIMING if timing else 0) | (int(key_ranges) << 8)
+            | (N.FLAG_NATURAL_ORDER if schedule == "natural" else 0))
 
 
 def _run(q, k, v, out, layout, mask: BlockMask, bits, counts, scale, inputs_permuted, shard,
-         num_shards, path, ws=None, timing=False, key_ranges=0):
+         num_shards, path, ws=None, timing=False, key_ranges=0, schedule="lpt"):
     g = mask.geometry
     L = N.lib()
     lay = N.layout_desc(layout)
     in_code = N.BSA_BF16 if q.dtype == torch.bfloat16 else N.BSA_F32
     out_code = N.BSA_BF16 if out.dtype == torch.bfloat16 else N.BSA_F32
-    flags = _flags(path, timing, key_ranges)
+    flags = _flags(path, timing, key_ranges, schedule)
     need = L.bsa_sparse_attention_workspace(lay, q.shape[0], q.shape[2], g.block_q, g.block_k,
                                             in_code, int(inputs_permuted), flags)
     if ws is None or ws.numel() < need or ws.device != q.device:
@@ -139,7 +142,8 @@ def last_kernel_ms() -> float:
 def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PANEL_BLOCKS,
                      threads: int = 1, inputs_permuted: bool = False, out_dtype=None,
                      path: str = "auto", shard: int = 0, num_shards: int = 1, out=None,
-                     workspace=None, timing: bool = False, key_ranges: int = 0):
+                     workspace=None, timing: bool = False, key_ranges: int = 0,
+                     schedule: str = "lpt"):
     """Run the block-sparse kernel; returns (heads, tokens, head_dim).
 
     Inputs arrive in interleaved source order and the result comes back in
@@ -149,6 +153,8 @@ def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PAN
     ``out`` are left untouched.  ``key_ranges`` (tensor-core path): 0 picks
     the key-range split automatically (heads whose K/V outgrow L2 are cut
     into L2-sized key ranges, merged by log-sum-exp), n forces n ranges.
+    ``schedule="natural"`` keeps each head's rows in index order instead of
+    longest-first (to measure what the LPT order buys; same results).
     """
     del panel_blocks, threads
     inp = job.inputs
@@ -164,7 +170,7 @@ def sparse_attention(job: SparseAttentionJob, *, panel_blocks: int = DEFAULT_PAN
         out = alloc(q.shape, dtype=out_dtype, device=q.device)
     bits = job.mask.device_bits(q.device)
     _run(q, k, v, out, job.layout, job.mask, bits, job.mask.device_counts(q.device), inp.scale,
-         inputs_permuted, shard, num_shards, path, workspace, timing, key_ranges)
+         inputs_permuted, shard, num_shards, path, workspace, timing, key_ranges, schedule)
     if inp.numpy_io:
         return out.float().cpu().numpy()
     return out

@@ -25,6 +25,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))  # tests/
 
 from golden_inputs import (  # noqa: E402
+    C6_RHOS,
+    C6_SCENE,
     CASES_ATTN,
     CASES_FULL,
     FULL_POLICIES,
@@ -33,6 +35,7 @@ from golden_inputs import (  # noqa: E402
     SCORE_POLICIES,
     bf16_round,
     make_qkv,
+    c6_inputs,
     sample_rows,
 )
 
@@ -162,6 +165,42 @@ def map_case(name, frames, patches, specials, heads, d, seed):
     print(f"{name}: T={lay.total_tokens} ({time.time() - t0:.1f}s)")
 
 
+def c6_case():
+    """Acceptance C6 scene through the reference itself: its q/k/v digests
+    (pinning tests/golden_inputs.py's restatement of synth.py), its masks and
+    the mean relative error against dense at each rho."""
+    from bsattn.dense import dense_attention
+    from bsattn.synth import SynthScene, full_shift_matches, synth_scene
+
+    t0 = time.time()
+    s = C6_SCENE
+    matches, groups = full_shift_matches(s["frames"], s["patches"], seed=s["match_seed"],
+                                         group_length=s["group_length"],
+                                         shift_quantum=s["shift_quantum"])
+    scene = SynthScene(frames=s["frames"], patches_per_frame=s["patches"], head_dim=s["d"],
+                       matches=matches, c=s["c"], direction_groups=groups)
+    res = synth_scene(scene, seed=s["seed"])
+    q, k, v = res.inputs.q, res.inputs.k, res.inputs.v
+    mq, mk, mv = c6_inputs()
+    assert sha(q) == sha(mq) and sha(k) == sha(mk) and sha(v) == sha(mv), "restatement drifted"
+    dense = dense_attention(res.inputs)
+    g = BlockGeometry(s["frames"] * s["patches"], 128, 64)
+    out = dict(q_sha=sha(q), k_sha=sha(k), v_sha=sha(v), dense_sha=sha(dense))
+    for i, rho in enumerate(C6_RHOS):
+        policy = MaskPolicy(tau=0.0, rho=rho, geometry=g)
+        mask = predict_mask(q, k, policy)
+        o = sparse_attention(SparseAttentionJob(res.inputs, scene.layout, mask, policy))
+        rel = np.linalg.norm(o - dense, axis=2) / np.linalg.norm(dense, axis=2)
+        out[f"mask{i}_bits"] = np.packbits(mask.blocks.reshape(-1, g.nk_blocks), axis=1,
+                                           bitorder="little")
+        out[f"err{i}"] = np.float64(rel.mean())
+    # a CDF policy on the same scene: ragged per-row counts (the LPT case)
+    mask = predict_mask(q, k, MaskPolicy(tau=0.9, rho=0.5, geometry=g))
+    out["cdf_bits"] = np.packbits(mask.blocks.reshape(-1, g.nk_blocks), axis=1, bitorder="little")
+    np.savez_compressed(os.path.join(HERE, "c6_scene.npz"), **out)
+    print(f"c6_scene: errors {[float(out[f'err{i}']) for i in range(3)]} ({time.time() - t0:.1f}s)")
+
+
 def main():
     print("reference bsattn", bsattn.__version__, "numpy", np.__version__)
     only = sys.argv[1:]  # optional case names
@@ -177,6 +216,8 @@ def main():
     for c in CASES_FULL:
         if not only or c["name"] in only:
             full_case(**c)
+    if not only or "c6" in only:
+        c6_case()
 
 
 if __name__ == "__main__":

@@ -93,3 +93,69 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
     u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
     return u.astype(np.uint32).view(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# planted-match scenes (structured, ragged masks): a restatement of the
+# reference's INPUT GENERATOR /root/reference/pkg/src/bsattn/synth.py:149-202
+# (full_shift_matches + synth_scene), test infrastructure only.  The golden
+# fixture stores the SHA-256 of the reference's own q/k/v for the scene, and
+# tests assert this restatement reproduces them bit for bit.
+# ---------------------------------------------------------------------------
+def full_shift_matches(frames: int, patches: int, seed: int, group_length: int = 64,
+                       shift_quantum: int = 1):
+    """Every token of frame f matched to a cyclically shifted token of frame
+    (f+1) mod frames; direction groups of `group_length` matches
+    (synth.py:149-176, same rng call order)."""
+    rng = np.random.default_rng(seed)
+    matches, groups, run_id = [], [], 0
+    for f in range(frames):
+        g = (f + 1) % frames
+        if g == f:
+            continue
+        shift = int(rng.integers(patches // shift_quantum)) * shift_quantum
+        for i in range(patches):
+            matches.append((f, i, g, (i + shift) % patches))
+            groups.append(run_id + i // group_length)
+        run_id = groups[-1] + 1
+    return matches, groups
+
+
+def synth_scene_qkv(frames: int, patches: int, specials: int, heads: int, d: int, matches,
+                    groups, c: float, seed: int):
+    """q, k, v (H, T, d) float32 of a planted-match scene (synth.py:179-202):
+    Gaussian noise, then c * u added to the matched query/key rows, one unit
+    direction u per group drawn in first-use order."""
+    rng = np.random.default_rng(seed)
+    n = frames * (patches + specials)
+    q = rng.standard_normal((heads, n, d)).astype(np.float32)
+    k = rng.standard_normal((heads, n, d)).astype(np.float32)
+    v = rng.standard_normal((heads, n, d)).astype(np.float32)
+    per = patches + specials
+    cf = np.float32(c)
+    dirs = {}
+    for m, (fa, i, fb, j) in enumerate(matches):
+        grp = groups[m] if groups is not None else m
+        u = dirs.get(grp)
+        if u is None:
+            u = rng.standard_normal(d).astype(np.float32)
+            u /= np.float32(np.linalg.norm(u))
+            dirs[grp] = u
+        q[:, fa * per + specials + i] += cf * u
+        k[:, fb * per + specials + j] += cf * u
+    return q, k, v
+
+
+# acceptance C6 (/root/reference/pkg/tests/test_acceptance.py:188-206): a 4-frame
+# planted-match scene, rho in {0.25, 0.5, 0.75} at tau = 0
+C6_SCENE = dict(frames=4, patches=1024, specials=0, heads=1, d=64, c=8.0, match_seed=5,
+                group_length=64, shift_quantum=32, seed=6)
+C6_RHOS = (0.25, 0.5, 0.75)
+
+
+def c6_inputs():
+    s = C6_SCENE
+    matches, groups = full_shift_matches(s["frames"], s["patches"], s["match_seed"],
+                                         s["group_length"], s["shift_quantum"])
+    return synth_scene_qkv(s["frames"], s["patches"], s["specials"], s["heads"], s["d"],
+                           matches, groups, s["c"], s["seed"])

@@ -39,3 +39,21 @@ def test_reference_arm_nonzero_rank_exits_quietly():
         cwd=ROOT, env=env)
     assert out.returncode == 0
     assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+
+
+def test_multi_gpu_request_never_silently_runs_one_gpu():
+    """`bench.py --gpus 2` outside torchrun re-executes itself with 2 ranks; on
+    a box with fewer GPUs (here: none) it must fail loudly instead of
+    reporting a one-GPU number. A WORLD_SIZE that contradicts --gpus fails too."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0
+    assert "--gpus 2" in out.stderr and "refusing" in out.stderr
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]
+    env2 = dict(env, WORLD_SIZE="4", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT, env=env2)
+    assert out.returncode != 0 and "WORLD_SIZE=4" in out.stderr

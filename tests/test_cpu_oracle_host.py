@@ -239,3 +239,30 @@ def test_path_selection_without_gpu():
     assert L.bsa_sparse_attention_path(lay, 32, 64, 32, N.BSA_BF16, 2) < 0
     ws = L.bsa_sparse_attention_workspace(lay, 16, 64, 128, 64, N.BSA_BF16, 0, 0)
     assert ws >= 3 * 16 * 274800 * 64 * 2
+
+
+def test_synth_restatement_matches_reference_digests():
+    """tests/golden_inputs.py's restatement of the reference's planted-match
+    generator (synth.py:149-202) reproduces the reference's q/k/v bit for bit
+    (digests written by make_golden.py from the reference itself)."""
+    import hashlib
+
+    from golden_inputs import c6_inputs
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "c6_scene.npz"))
+    for x, key in zip(c6_inputs(), ("q_sha", "k_sha", "v_sha")):
+        assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == str(z[key])
+
+
+def test_c6_masks_oracle_vs_reference(oracle):
+    """The C restatement of the scoring stage gives the reference's C6 masks."""
+    from golden_inputs import C6_RHOS, c6_inputs
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "c6_scene.npz"))
+    q, k, _ = c6_inputs()
+    for i, rho in enumerate(C6_RHOS):
+        m, _ = oracle.predict_mask(q, k, 128, 64, 0.0, rho)
+        assert np.array_equal(oracle.pack_bits(m).reshape(z[f"mask{i}_bits"].shape),
+                              z[f"mask{i}_bits"])
+    m, _ = oracle.predict_mask(q, k, 128, 64, 0.9, 0.5)
+    assert np.array_equal(oracle.pack_bits(m).reshape(z["cdf_bits"].shape), z["cdf_bits"])
