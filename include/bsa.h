@@ -76,6 +76,11 @@ const char* bsa_last_error(void);
 /* Number of SMs of the current device (for persistent grids / sharding). */
 int bsa_device_sm_count(void);
 
+/* Input validation of the reference's as_f32 (tensorio.py:47-59), on the
+ * device: sets *flag (device int32, caller-zeroed) to 1 if x holds a NaN or
+ * an infinity.  Asynchronous; several tensors may share one flag. */
+int bsa_check_finite(const bsa_tensor* x, int32_t* flag, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Scoring stage                                                      */
 /* ------------------------------------------------------------------ */

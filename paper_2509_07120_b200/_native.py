@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import torch
 
@@ -97,6 +98,7 @@ def _declare(L):
         "bsa_attention_stats_workspace": ([pl, i64], sz),
         "bsa_attention_row_stats": ([pt, pt, pl, f32, vp, vp, sz, vp], ctypes.c_int),
         "bsa_block_attention_map": ([pt, pt, pl, f32, vp, vp, vp, sz, vp], ctypes.c_int),
+        "bsa_check_finite": ([pt, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -116,7 +118,7 @@ def exported_symbols():
         "bsa_sparse_attention_path", "bsa_last_kernel_ms", "bsa_mask_selected_area", "bsa_mask_to_csr_workspace",
         "bsa_mask_to_csr", "bsa_sparse_attention_scatter", "bsa_ipc_alloc", "bsa_ipc_open",
         "bsa_ipc_close", "bsa_ipc_free", "bsa_attention_stats_workspace",
-        "bsa_attention_row_stats", "bsa_block_attention_map",
+        "bsa_attention_row_stats", "bsa_block_attention_map", "bsa_check_finite",
     ]
 
 
@@ -161,12 +163,61 @@ def on_device(device):
     return torch.cuda.device(device)
 
 
+_FINITE_SEEN: dict = {}  # id(tensor) -> (weakref, version) of tensors found finite
+
+
+def _known_finite(t: torch.Tensor) -> bool:
+    e = _FINITE_SEEN.get(id(t))
+    return e is not None and e[0]() is t and e[1] == t._version
+
+
+def _mark_finite(t: torch.Tensor) -> None:
+    if len(_FINITE_SEEN) > 256:
+        for key in [k for k, (r, _) in _FINITE_SEEN.items() if r() is None]:
+            del _FINITE_SEEN[key]
+        if len(_FINITE_SEEN) > 256:
+            _FINITE_SEEN.clear()
+    try:
+        _FINITE_SEEN[id(t)] = (weakref.ref(t), t._version)
+    except TypeError:  # not weak-referenceable: just do not cache
+        pass
+
+
 def all_finite(*tensors: torch.Tensor) -> bool:
-    """True when no element of the (device) tensors is NaN or +-inf: one
-    min/max reduction per tensor (no full-size temporaries), one sync.  The
-    reference's as_f32 rejects non-finite inputs (tensorio.py:47-59)."""
-    ext = [torch.stack(torch.aminmax(t.detach())).float() for t in tensors]
-    return bool(torch.isfinite(torch.cat(ext)).all())
+    """True when no element of the tensors is NaN or +-inf. The reference's
+    as_f32 rejects non-finite inputs (tensorio.py:47-59). CUDA (H, T, d)
+    fp32/bf16 tensors (any head/token strides) are scanned by one HBM-bound
+    kernel each (bsa_check_finite, no temporaries) into a shared flag, read
+    back with ONE sync; anything else falls back to torch. A tensor object
+    already found finite whose version counter (bumped by every in-place
+    write) has not moved since is not rescanned."""
+    todo = [t for t in tensors if not _known_finite(t)]
+    cuda = [t for t in todo if t.device.type == "cuda"]
+    dev = [t for t in cuda if t.dim() == 3 and t.dtype in _DTYPE_CODE and t.stride(2) == 1
+           and t.device == cuda[0].device]
+    rest = [t for t in todo if not any(t is x for x in dev)]
+    ok = True
+    if dev:
+        flag = torch.zeros(1, dtype=torch.int32, device=dev[0].device)
+        with on_device(dev[0].device):
+            for t in dev:
+                check(lib().bsa_check_finite(tensor_desc(t), flag.data_ptr(), stream_ptr()),
+                      "check_finite")
+        ok = int(flag.item()) == 0
+    for t in rest:
+        ok = ok and bool(torch.isfinite(t).all())
+    if ok:
+        for t in todo:
+            _mark_finite(t)
+    return ok
+
+
+def finite_scan(t: torch.Tensor, flag: torch.Tensor) -> None:
+    """Asynchronous part of all_finite: OR "t has a NaN/inf" into the device
+    int32 `flag` (same device) without synchronising."""
+    with on_device(t.device):
+        check(lib().bsa_check_finite(tensor_desc(t), flag.data_ptr(), stream_ptr()),
+              "check_finite")
 
 
 def ptr(t) -> int | None:

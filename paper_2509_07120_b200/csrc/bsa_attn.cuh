@@ -120,7 +120,11 @@ struct TcArgs {
   void* part_out;             // (nr, H, T, 64) bf16 (part_bf16) or fp32
   int part_bf16;
   float* part_lse;            // (nr, H, T): offset + log2(l)
-  const __nv_bfloat16* qp;   // packed partitioned (H, T, 64)
+  const __nv_bfloat16* qp;   // Q: packed partitioned (H, T, 64), or (q_src) the caller's
+                             // bf16 q in its own token order and strides
+  int q_src;                 // 1: qp is the caller's q; row = permuted ? pr : part_src(pr)
+  int64_t q_sH, q_sT;        // element strides of qp (packed: T*64, 64)
+  int64_t kv_sH, kv_sT;      // element strides of kp / vp (packed: T*64, 64)
   const __nv_bfloat16* kp;
   const void* vp;             // V: bf16, or fp16 scaled by 2^v_shift[h] (v_f16)
   const int32_t* v_shift;

@@ -626,11 +626,28 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   // on MUFU: the kernel is MUFU-bound at d=64 (profiles/r01_summary.md);
   // measured 0: 90.0 ms, 2: 85.4, 3: 84.5, 4: 90.9
   const int exp_poly = env_poly >= 0 ? env_poly : 3;
-  rc = launch_pack(q, G, inputs_permuted, W.qp, st);
-  if (!rc) rc = launch_pack(k, G, inputs_permuted, W.kp, st);
-  if (!rc)
-    rc = v_f16 ? launch_pack_v(v, G, inputs_permuted, W.vamax, W.vshift, (__half*)W.vp, st)
-               : launch_pack(v, G, inputs_permuted, (__nv_bfloat16*)W.vp, st);
+  // Pack passes only where the kernel cannot read the caller's tensors:
+  //  * Q (read row by row by the softmax warps) is used in place whenever it
+  //    is bf16 with 16-byte aligned rows: the partitioned-order gather is the
+  //    row address part_src(pr);
+  //  * K and V are TMA-loaded in 64-key boxes of the partitioned order, which
+  //    straddle frames in source order: used in place only when the inputs
+  //    are already partitioned (inputs_permuted), bf16, aligned and share
+  //    strides; otherwise packed (3 bytes moved per 2 read, ~0.4 ms at N=200).
+  auto aligned16 = [](const bsa_tensor* t) {
+    return t->dtype == BSA_BF16 && (uintptr_t)t->data % 16 == 0 && (t->stride_token * 2) % 16 == 0 &&
+           (t->stride_head * 2) % 16 == 0;
+  };
+  const bool q_direct = aligned16(q);
+  const bool kv_direct = !v_f16 && inputs_permuted && aligned16(k) && aligned16(v) &&
+                         k->stride_token == v->stride_token && k->stride_head == v->stride_head;
+  if (!q_direct) rc = launch_pack(q, G, inputs_permuted, W.qp, st);
+  if (!rc && !kv_direct) {
+    rc = launch_pack(k, G, inputs_permuted, W.kp, st);
+    if (!rc)
+      rc = v_f16 ? launch_pack_v(v, G, inputs_permuted, W.vamax, W.vshift, (__half*)W.vp, st)
+                 : launch_pack(v, G, inputs_permuted, (__nv_bfloat16*)W.vp, st);
+  }
   if (rc) return rc;
   const int64_t rows = G.H * G.nq;
   if (!counts) {
@@ -673,9 +690,14 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   a.part_out = W.part_out;
   a.part_bf16 = part_bf16;
   a.part_lse = W.part_lse;
-  a.qp = W.qp;
-  a.kp = W.kp;
-  a.vp = W.vp;
+  a.qp = q_direct ? (const __nv_bfloat16*)q->data : W.qp;
+  a.q_src = q_direct ? 1 : 0;
+  a.q_sH = q_direct ? q->stride_head : G.T * G.d;
+  a.q_sT = q_direct ? q->stride_token : G.d;
+  a.kp = kv_direct ? (const __nv_bfloat16*)k->data : W.kp;
+  a.vp = kv_direct ? v->data : W.vp;
+  a.kv_sH = kv_direct ? k->stride_head : G.T * G.d;
+  a.kv_sT = kv_direct ? k->stride_token : G.d;
   a.v_shift = W.vshift;
   a.v_f16 = v_f16;
   a.exp_poly = exp_poly;

@@ -54,20 +54,21 @@ namespace tc {
 #ifndef BSA_TC_NB
 #define BSA_TC_NB 6
 #endif
-// PAIR: 128-key S tiles.  Two consecutive 64-key chunks of an item's key
-// stream share one K stage (16 KB, contiguous: one N=128 S MMA), one S/P
-// buffer of 128 TMEM columns, one S commit and one PV commit.  The softmax
-// still works per 64-key chunk (group (g + c) % NG takes chunk c, a tile's
-// two chunks go to two groups); the S/PV issuers and the K producer do half
-// as many barrier round trips per key.
-#ifndef BSA_TC_PAIR
-#define BSA_TC_PAIR 0
+// SEP: P in its own TMEM buffers (NP of 32 packed columns) instead of over
+// its S buffer.  An S buffer is then free as soon as its group has READ S
+// (SFREE), not when the PV that read P completes: the chain P(j) -> PV(j) ->
+// S(j + NB) leaves the S pipeline.  TMEM: S 3 x 64 | P 6 x 32 | O 80 | Q 32.
+#ifndef BSA_TC_SEP
+#define BSA_TC_SEP 0
 #endif
-// HALFPV: the softmax group publishes P per 32-key half (one more barrier
-// per half) and the PV issuer runs keys 0-31 as soon as the first half is
-// written, so the PV of a tile overlaps the exps of its second half
-#ifndef BSA_TC_HALFPV
-#define BSA_TC_HALFPV 0
+#ifndef BSA_TC_NBS
+#define BSA_TC_NBS 3  // (SEP) S buffers
+#endif
+#ifndef BSA_TC_NP
+#define BSA_TC_NP 6   // (SEP) P buffers
+#endif
+#ifndef BSA_TC_LOAD64
+#define BSA_TC_LOAD64 0  // stale-max softmax: load a tile's 64 S columns at once
 #endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
@@ -96,10 +97,9 @@ constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 template <bool WIDE>
 struct Cfg {
   static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warp groups (4 warps: the 4 lane quarters)
-  static constexpr bool PAIR = WIDE && BSA_TC_PAIR != 0;  // 128-key S tiles
-  static constexpr int TCH = PAIR ? 2 : 1;                // 64-key chunks per S tile
-  static constexpr uint32_t S_COLS = 64 * TCH;            // TMEM columns per S/P buffer
-  static constexpr int NB = PAIR ? 3 : (WIDE ? BSA_TC_NB : 2);  // S buffers (P over S)
+  static constexpr bool SEP = WIDE && BSA_TC_SEP != 0;  // P in its own buffers
+  static constexpr int NB = SEP ? BSA_TC_NBS : (WIDE ? BSA_TC_NB : 2);  // S buffers (64 columns)
+  static constexpr int NP = SEP ? BSA_TC_NP : NB;  // P buffers (SEP: 32 columns; else P over S)
   static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
   static constexpr int SM_WARPS = 4 * NG;
   // SPLIT: S MMAs and PV MMAs come from two issuer warps (one warp issuing
@@ -117,19 +117,20 @@ struct Cfg {
   // every 4th warp of the SM's CTAs (8-register granules)
   static constexpr int WARPS_PER_SMSP = (CTAS_PER_SM * NUM_THREADS / 32 + 3) / 4;
   static constexpr int MAX_REGS = (16384 / (32 * WARPS_PER_SMSP)) / 8 * 8;
-  static constexpr int NK = PAIR ? 4 : (WIDE ? 8 : 5), NV = WIDE ? (LSUM ? 6 : 10) : 4;
-  static constexpr int K_STAGE = TCH * CHUNK_BYTES;  // one S tile of K
+  static constexpr int NK = WIDE ? 8 : 5, NV = WIDE ? (LSUM ? 6 : 10) : 4;
   static constexpr int VLAG = 2;  // (one producer warp) K(j) is loaded VLAG tiles before V(j)
   static constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ ones block)
   static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + NK * K_STAGE;
+  static constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
   static constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // [3][NG][128] floats
   static constexpr int OFF_QUEUE = OFF_XCH + 3 * NG * BQ * 4;  // (SPLIT) [2][QUEUE] int32
   static constexpr int OFF_BAR = OFF_QUEUE + (SPLIT ? 2 * QUEUE * 4 : 0);
   static constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
   static constexpr uint32_t TMEM_COLS = WIDE ? 512 : 256;
-  // TMEM: S0..S(NB-1) (S_COLS columns each, P over S) | O (80) | Q (32, last)
-  static constexpr uint32_t TM_S = 0, TM_O = NB * S_COLS, TM_Q = TMEM_COLS - 32;
+  // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last);
+  // SEP: S0..S(NB-1) | P0..P(NP-1) (32 columns each) | O | Q
+  static constexpr uint32_t TM_S = 0, TM_P = SEP ? NB * 64 : 0, P_STRIDE = SEP ? 32 : 64;
+  static constexpr uint32_t TM_O = SEP ? TM_P + NP * 32 : NB * 64, TM_Q = TMEM_COLS - 32;
   // barrier slots (8 bytes each) inside the barrier region
   static constexpr int B_QFULL = 0;              // [1]  Q in TMEM (all softmax warps)
   static constexpr int B_KFULL = 1;              // [NK]
@@ -137,11 +138,10 @@ struct Cfg {
   static constexpr int B_VFULL = B_KEMPTY + NK;  // [NV]
   static constexpr int B_VEMPTY = B_VFULL + NV;  // [NV]
   static constexpr int B_SFULL = B_VEMPTY + NV;  // [NB]
-  static constexpr int B_PFULL = B_SFULL + NB;   // [NB] the warps of the tile
-  static constexpr bool HALFPV = WIDE && !PAIR && BSA_TC_HALFPV != 0;
-  static constexpr int B_PFULL0 = B_PFULL + NB;  // [NB] (HALFPV) first half of P written
-  static constexpr int B_PFREE = B_PFULL0 + (HALFPV ? NB : 0);  // [NB] PV done: buffer reusable
-  static constexpr int B_OFULL = B_PFREE + NB;   // [1]
+  static constexpr int B_SFREE = B_SFULL + NB;   // [NB] (SEP) S read: S buffer reusable
+  static constexpr int B_PFULL = B_SFREE + (SEP ? NB : 0);  // [NP] the warps of the tile
+  static constexpr int B_PFREE = B_PFULL + NP;   // [NP] PV done: P (and, not SEP, S) buffer reusable
+  static constexpr int B_OFULL = B_PFREE + NP;   // [1]
   static constexpr int B_OEMPTY = B_OFULL + 1;   // [1]
   static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
   static constexpr int B_IEMPTY = B_IFULL + 2;   // [2]  softmax warps + MMA warp(s)
@@ -231,9 +231,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   constexpr int SM_WARPS = C::SM_WARPS;
   // warps that write one tile's P: one group (stale max, whole tiles), or
   // both groups (exact max, column halves of every tile)
-  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4 * C::TCH;
-  constexpr bool PAIR = C::PAIR;
-  constexpr uint32_t S_COLS = C::S_COLS;
+  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4;
   static_assert(!EXACT || NG == 2, "the exact launch splits tiles into two column halves");
   (void)tm_q;  // Q goes to TMEM from the softmax warps' registers
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -268,8 +266,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     mbar_init(BAR(C::B_QFULL), SM_WARPS);
     for (int i = 0; i < NB; ++i) {
       mbar_init(BAR(C::B_SFULL + i), 1);
+      if (C::SEP) mbar_init(BAR(C::B_SFREE + i), TILE_WARPS);
+    }
+    for (int i = 0; i < C::NP; ++i) {
       mbar_init(BAR(C::B_PFULL + i), TILE_WARPS);
-      if (C::HALFPV) mbar_init(BAR(C::B_PFULL0 + i), TILE_WARPS);
       mbar_init(BAR(C::B_PFREE + i), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -325,7 +325,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     // the per-tile cost is one queue read, one barrier wait and one TMA.
     const bool is_k = warp == C::PRODUCER_WARP;
     int32_t* queue = reinterpret_cast<int32_t*>(smem + C::OFF_QUEUE) + (is_k ? 0 : C::QUEUE);
-    uint32_t it = 0, gx = 0, gt = 0;  // chunks, (PAIR, K) S tiles
+    uint32_t it = 0, gx = 0;
     while (true) {
       const uint32_t slot = it & 1;
       int32_t code;
@@ -398,20 +398,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           __syncwarp();
         }
         const int32_t s0 = queue[qh++];
-        if (is_k && PAIR) {
-          // chunk pairs (j, j+1) fill one 16 KB stage: rows 0-63 and 64-127
-          // of the N=128 B operand
-          const uint32_t st = gt % NK;
-          const int half = j & 1;
-          if (half == 0) mbar_wait(BAR(C::B_KEMPTY + st), ((gt / NK) & 1) ^ 1);
-          if (elect_one()) {
-            if (half == 0)
-              mbar_expect_tx(BAR(C::B_KFULL + st), (I.nchunks - j >= 2 ? 2 : 1) * CHUNK_BYTES);
-            tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE + half * CHUNK_BYTES, &tm_k,
-                        BAR(C::B_KFULL + st), 0, s0, I.h);
-          }
-          if (half == 1 || j == I.nchunks - 1) ++gt;
-        } else if (is_k) {
+        if (is_k) {        } else if (is_k) {
           const uint32_t st = gx % NK;
           if (lane == 0) BSA_TR(9, gx);
           mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
@@ -511,7 +498,6 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     uint32_t sk = 0, kph = 0, sb = 0, sph = 0;  // S issue: K stage, S buffer (+ phases)
     uint32_t pb = 0, pph = 0, sv = 0, vph = 0;  // PV issue: P buffer, V stage
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
-    const uint32_t id_s2 = idesc_f16(128, 128, 0, 1);                // (PAIR) two chunks
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
     const uint64_t dk0 = sdesc(sbase + C::OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + C::OFF_V, 8192, 1024);
@@ -535,10 +521,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
 #ifdef BSA_TC_TRACE_BUILD
         mbar_wait(BAR(C::B_KFULL + sk), kph);
         if (lane == 0) BSA_TR(3, gs);
-        mbar_wait(BAR(C::B_PFREE + sb), sph ^ 1);
+        mbar_wait(BAR((C::SEP ? C::B_SFREE : C::B_PFREE) + sb), sph ^ 1);
         if (lane == 0) BSA_TR(13, gs);
 #else
-        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR(C::B_PFREE + sb), sph ^ 1);
+        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR((C::SEP ? C::B_SFREE : C::B_PFREE) + sb), sph ^ 1);
 #endif
         tc_fence_after();
         if (elect_one()) {
@@ -566,33 +552,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         mbar_wait(BAR(C::B_VFULL + sv), vph);
         if (lane == 0) BSA_TR(5, gp);
 #else
-        mbar_wait2(BAR((C::HALFPV ? C::B_PFULL0 : C::B_PFULL) + pb), pph, BAR(C::B_VFULL + sv), vph);
+        mbar_wait2(BAR(C::B_PFULL + pb), pph, BAR(C::B_VFULL + sv), vph);
 #endif
         if (jj == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
         tc_fence_after();
-        if (C::HALFPV) {
-          // keys 0-31 now (P half 0), keys 32-63 once half 1 is written
+        if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
-          const uint32_t pa = tmem + C::TM_S + pb * 64;
-          if (elect_one()) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv,
-                     (jj > 0 || k > 0) ? 1u : 0u);
-          }
-          __syncwarp();
-          mbar_wait(BAR(C::B_PFULL + pb), pph);
-          tc_fence_after();
-          if (elect_one()) {
-#pragma unroll
-            for (int k = 2; k < 4; ++k)
-              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv, 1u);
-            tc_commit(BAR(C::B_PFREE + pb));
-            tc_commit(BAR(C::B_VEMPTY + sv));
-          }
-        } else if (elect_one()) {
-          const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
-          const uint32_t pa = tmem + C::TM_S + pb * 64;
+          const uint32_t pa = tmem + C::TM_P + pb * C::P_STRIDE;
           // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
           // column halves: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
@@ -606,59 +572,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
         __syncwarp();
         ++gp;
-        if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
+        if (++pb == (uint32_t)C::NP) { pb = 0; pph ^= 1; }
         if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
       };
-      // PAIR: one S MMA (N = 64 * chunks) per tile of up to two chunks; the
-      // PV of each chunk reads its own V stage, one PFREE commit per tile
-      auto issue_s_pair = [&](int nch) {
-        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR(C::B_PFREE + sb), sph ^ 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint64_t dk = dk0 + (uint64_t)(sk * (C::K_STAGE >> 4));
-          const uint32_t ds = tmem + C::TM_S + sb * S_COLS;
-          const uint32_t id = nch == 2 ? id_s2 : id_s;
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k)
-            mma_ts(ds, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id, k > 0 ? 1u : 0u);
-          tc_commit(BAR(C::B_SFULL + sb));
-          tc_commit(BAR(C::B_KEMPTY + sk));
-        }
-        __syncwarp();
-        if (++sk == (uint32_t)NK) { sk = 0; kph ^= 1; }
-        if (++sb == (uint32_t)NB) { sb = 0; sph ^= 1; }
-      };
-      auto issue_pv_pair = [&](int jt, int nch) {
-        mbar_wait2(BAR(C::B_PFULL + pb), pph, BAR(C::B_VFULL + sv), vph);
-        if (jt == 0) mbar_wait(BAR(C::B_OEMPTY), (it & 1) ^ 1);
-        tc_fence_after();
-        for (int h = 0; h < nch; ++h) {
-          if (h > 0) {
-            mbar_wait(BAR(C::B_VFULL + sv), vph);
-            tc_fence_after();
-          }
-          if (elect_one()) {
-            const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
-            const uint32_t pa = tmem + C::TM_S + pb * S_COLS + h * 64;
-#pragma unroll
-            for (int k = 0; k < CH / 16; ++k)
-              mma_ts(tmem + C::TM_O, pa + k * 8, dv + (uint64_t)(k * (2048 >> 4)), id_pv,
-                     (jt > 0 || h > 0 || k > 0) ? 1u : 0u);
-            tc_commit(BAR(C::B_VEMPTY + sv));
-            if (h == nch - 1) tc_commit(BAR(C::B_PFREE + pb));
-          }
-          __syncwarp();
-          if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
-        }
-        if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
-      };
-      if constexpr (PAIR) {
-        for (int jt = 0; 2 * jt < ntiles; ++jt) {
-          const int nch = ntiles - 2 * jt >= 2 ? 2 : 1;
-          if (do_s) issue_s_pair(nch);
-          else issue_pv_pair(jt, nch);
-        }
-      } else if constexpr (C::SPLIT) {
+      if constexpr (C::SPLIT) {
         if (do_s) {
           for (int j = 0; j < ntiles; ++j) issue_s();
         } else {
@@ -693,19 +610,22 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     float* x_first = xch;              // [NG][128]
     float* x_tile = xch + NG * BQ;     // [NG][128] (EXACT)
     float* x_l = xch + 2 * NG * BQ;    // [NG][128] (EXACT)
-    // S/P buffer, its phase, and the first TMEM column of chunk j of the
-    // current item (g: the item's first global chunk; PAIR, gt: its first
-    // global 128-key tile, chunk j is half j & 1 of tile gt + j / 2)
-    uint32_t it = 0, g = 0, gt = 0;
+    // S buffer, its phase and first TMEM column for tile j of the current
+    // item (g: the item's first global tile), and the P buffer (SEP: its own
+    // ring; else P over S)
+    uint32_t it = 0, g = 0;
     struct ChunkSlot {
-      uint32_t buf, phase, col;
+      uint32_t buf, phase, col, pbuf, pphase, pcol;
     };
     auto slot_of = [&](int j) -> ChunkSlot {
       ChunkSlot z;
-      const uint32_t t = PAIR ? gt + (uint32_t)(j >> 1) : g + (uint32_t)j;
+      const uint32_t t = g + (uint32_t)j;
       z.buf = t % NB;
       z.phase = (t / NB) & 1;
-      z.col = C::TM_S + z.buf * S_COLS + (PAIR ? (uint32_t)(j & 1) * 64 : 0u);
+      z.col = C::TM_S + z.buf * 64;
+      z.pbuf = t % C::NP;
+      z.pphase = (t / C::NP) & 1;
+      z.pcol = C::SEP ? C::TM_P + z.pbuf * 32 : z.col;
       return z;
     };
     // the NG warps sharing this TMEM lane quarter
@@ -728,11 +648,14 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         // previous item's S MMAs are complete: its epilogue waited for O.
         // 16-dimension chunks c (8 packed columns) with c % NG == grp
         const int32_t pr = I.row0 + row;
+        // Q straight from the caller's bf16 tensor (no pack pass): the
+        // partitioned row's source token; else the packed copy
+        const int64_t qrow = pr < (int32_t)G.T && A.q_src && !A.permuted_out ? G.L.part_src(pr) : pr;
         for (int c = grp; c < 4; c += NG) {
           uint32_t qr[8];
           if (pr < (int32_t)G.T) {
-            const uint4* src =
-                reinterpret_cast<const uint4*>(A.qp + ((int64_t)I.h * G.T + pr) * D + c * 16);
+            const uint4* src = reinterpret_cast<const uint4*>(
+                A.qp + (int64_t)I.h * A.q_sH + qrow * A.q_sT + c * 16);
             const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
             qr[0] = v0.x; qr[1] = v0.y; qr[2] = v0.z; qr[3] = v0.w;
             qr[4] = v1.x; qr[5] = v1.y; qr[6] = v1.z; qr[7] = v1.w;
@@ -786,10 +709,37 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           mbar_wait(BAR(C::B_SFULL + sb), z.phase);
           tc_fence_after();
           if (lane == 0 && quarter == 0) BSA_TR(8, gg);
+#if BSA_TC_LOAD64
+          // (variant) all 64 S columns in one round trip: one TMEM-load
+          // latency per tile instead of one per 32-key half
+          uint32_t sr64[64];
+          tmem_ld32(tmem + lane_off + z.col, &sr64[0]);
+          tmem_ld32(tmem + lane_off + z.col + 32, &sr64[32]);
+          tmem_wait_ld();
+          reg_fence16(&sr64[0]);
+          reg_fence16(&sr64[16]);
+          reg_fence16(&sr64[32]);
+          reg_fence16(&sr64[48]);
+          if (C::SEP) {  // S read: the S issuer may refill this buffer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(C::B_SFREE + sb));
+          }
+#endif
+          if (C::SEP) {
+            // our P buffer: the PV that read it NP tiles ago has completed
+            mbar_wait(BAR(C::B_PFREE + z.pbuf), z.pphase ^ 1);
+            tc_fence_after();
+          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             // 32 keys at a time; their P (16 packed columns) goes over S
             // columns this thread has already read
+#if BSA_TC_LOAD64
+            float s[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr64[hh * 32 + e]);
+#else
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
@@ -797,15 +747,21 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             tmem_wait_ld();
             reg_fence16(&sr[0]);
             reg_fence16(&sr[16]);
+            if (C::SEP && hh == 1) {  // S read: the S issuer may refill this buffer
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(BAR(C::B_SFREE + sb));
+            }
             float s[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
+#endif
             if (len - hh * 32 < 32) {
 #pragma unroll
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
-            const uint32_t p_col = tmem + lane_off + z.col + hh * 16;
+            const uint32_t p_col = tmem + lane_off + z.pcol + hh * 16;
 #if BSA_TC_EXPERIMENT == 1
             {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
@@ -820,22 +776,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               l += lt;
             }
 #endif
-            if (C::HALFPV && hh == 0) {
-              // publish P half 0: the PV issuer starts keys 0-31
-              tmem_wait_st();
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(BAR(C::B_PFULL0 + sb));
-            }
           }
           if (lane == 0 && quarter == 0) BSA_TR(12, gg);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            // (PAIR) a tile holding one chunk completes with this group alone
-            if (PAIR && (j & 1) == 0 && j == ntiles - 1) mbar_arrive_cnt(BAR(C::B_PFULL + sb), 2);
-            else mbar_arrive(BAR(C::B_PFULL + sb));
+            mbar_arrive(BAR(C::B_PFULL + z.pbuf));
             if (quarter == 0) BSA_TR(16, gg);
           }
         }
@@ -983,7 +930,6 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
       }
       g += ntiles;
-      gt += (ntiles + 1) / 2;
       ++it;
     }
   }
@@ -1021,12 +967,14 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
+// 3-D (d, T, H) map of a 16-bit (H, T, 64) tensor with element strides sT, sH
 static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, int box_rows,
+                    int64_t sT, int64_t sH,
                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)tc::D, (cuuint64_t)T, (cuuint64_t)H};
-  cuuint64_t strides[2] = {(cuuint64_t)tc::D * 2, (cuuint64_t)T * tc::D * 2};
+  cuuint64_t strides[2] = {(cuuint64_t)sT * 2, (cuuint64_t)sH * 2};
   cuuint32_t box[3] = {(cuuint32_t)tc::D, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, dt, 3, const_cast<void*>(base), dims,
@@ -1086,13 +1034,12 @@ static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
                         const CombineArgs* comb) {
   CUtensorMap mk, mv;
-  CUtensorMap mq;
-  int rc = make_map(&mq, a.qp, G.H, G.T, tc::BQ);  // unused by the kernel (Q goes via registers)
-  if (!rc) rc = make_map(&mk, a.kp, G.H, G.T, tc::CH);
+  int rc = make_map(&mk, a.kp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH);
   if (!rc)
-    rc = make_map(&mv, a.vp, G.H, G.T, tc::CH,
+    rc = make_map(&mv, a.vp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH,
                   a.v_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   if (rc) return rc;
+  const CUtensorMap& mq = mk;  // the kernel's Q map parameter is unused (Q goes via registers)
   int dev = 0, sms = 148;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

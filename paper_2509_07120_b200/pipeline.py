@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import torch
 
+from . import _native as N
 from .dense import AttentionInputs
 from .layout import TokenLayout
 from .maskpred import BlockMask, MaskPolicy, predict_mask
@@ -96,7 +97,7 @@ class HostLayerPipeline:
         dq, dk, dv = self.bufs
         comp = torch.cuda.current_stream(self.device)
         masks = []
-        extrema = []
+        bad = torch.zeros(1, dtype=torch.int32, device=self.device) if validate else None
         done_in, done_comp = [], []
         chunks = self.chunks
         # the copy-in stream must not overwrite buffers a previous call still reads
@@ -116,8 +117,9 @@ class HostLayerPipeline:
             comp.wait_event(ev_qk)
             mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout, validate=False)
             comp.wait_event(ev_v)
-            if validate:
-                extrema += [torch.stack(torch.aminmax(x[a:b])).float() for x in (dq, dk, dv)]
+            if validate:  # device scan into one flag, read once at the end
+                for x in (dq, dk, dv):
+                    N.finite_scan(x[a:b], bad)
             job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b], validate=False),
                                      layout, mask)
             sparse_attention(job, out=self.obuf[a:b])
@@ -131,7 +133,7 @@ class HostLayerPipeline:
                 out[a:b].copy_(self.obuf[a:b], non_blocking=True)
         comp.wait_stream(self.s_out)
         torch.cuda.current_stream(self.device).synchronize()
-        if validate and not bool(torch.isfinite(torch.cat(extrema)).all()):
+        if validate and int(bad.item()) != 0:
             raise ValueError("q/k/v contain non-finite values")
         return (out, masks) if return_masks else out
 
