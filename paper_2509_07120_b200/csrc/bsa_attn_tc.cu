@@ -398,7 +398,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           __syncwarp();
         }
         const int32_t s0 = queue[qh++];
-        if (is_k) {        } else if (is_k) {
+        if (is_k) {
           const uint32_t st = gx % NK;
           if (lane == 0) BSA_TR(9, gx);
           mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
