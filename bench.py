@@ -344,9 +344,19 @@ def run_ours(a):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
-    peak_tf = float(peaks.get("bf16_tflops", 1590.0))
-    peak_src = "measured burst cuBLAS bf16 (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks else \
-        "fallback 1.59 PF/s (B200_PROFILING.md)"
+    # the kernel is timed inside a multi-second loop of back-to-back ~85 ms
+    # launches under the board's power cap: the measured SUSTAINED cuBLAS
+    # bf16 figure (4 s back to back, same cap) is the matching denominator;
+    # the burst figure (a short run at full clock) is reported beside it
+    burst_tf = float(peaks.get("bf16_tflops", 1590.0))
+    if "bf16_tflops_sustained" in peaks:
+        peak_tf = float(peaks["bf16_tflops_sustained"])
+        peak_src = ("measured SUSTAINED cuBLAS bf16, 4 s back to back (MEASURED_PEAKS.json): "
+                    "the kernel is timed inside a long loop of back-to-back launches")
+    else:
+        peak_tf = burst_tf
+        peak_src = ("measured burst cuBLAS bf16 (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks
+                    else "fallback 1.59 PF/s (B200_PROFILING.md)")
     achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
     traffic = None
     if not sharded:
@@ -358,6 +368,22 @@ def run_ours(a):
                 traffic = tr["dram_bytes_per_launch"]
         except (OSError, ValueError, KeyError):
             pass
+
+    # scoring roofline (predict_mask): HBM bytes it must move -- the bf16
+    # patch rows of Q and K read once, the mask bits and counts written --
+    # and the exact fp32 pooled dot products on the FMA pipe
+    scoring = None
+    if score_ms and a.mask == "predicted":
+        sc_ms = float(np.mean(score_ms))
+        nq_, nk_ = g.nq_blocks, g.nk_blocks
+        sc_bytes = 2 * H * Tp * d * 2 + H * nq_ * (-(-nk_ // 8)) + 4 * H * nq_
+        fma = H * nq_ * nk_ * d
+        fma_peak = 148 * 128 * 1.965e9  # fp32 FMA/s at the maximum SM clock
+        hbm = float(peaks.get("hbm_gbs", 6544.0))
+        scoring = {"bound": "hbm", "ms": sc_ms, "bytes": sc_bytes,
+                   "achieved_gbs": sc_bytes / (sc_ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                   "frac": sc_bytes / (sc_ms * 1e-3) / 1e9 / hbm,
+                   "fma": fma, "fma_frac": fma / (sc_ms * 1e-3) / fma_peak}
 
     # dense baseline on the same GPU: library SDPA (cuDNN / flash) in bf16
     dense_ms = None
@@ -467,15 +493,14 @@ def run_ours(a):
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": traffic,
                          "kernel": "bsa_tc_kernel", "algorithmic_flops_per_launch": flops,
                          "dense_flops": dense_flops, "peak_source": peak_src,
-                         # the same kernel against the measured SUSTAINED cuBLAS bf16
-                         # figure (power-capped clocks, like this multi-second loop)
-                         "frac_of_sustained": (achieved_tf / float(peaks["bf16_tflops_sustained"])
-                                               if "bf16_tflops_sustained" in peaks else None)},
+                         "peak_burst": burst_tf, "frac_of_burst": achieved_tf / burst_tf},
+            "scoring": scoring,
             "e2e": e2e,
-            # per step: 2 pool8, scores, pw_plan, softsel, fallback, 3 pack,
-            # schedule, bsa_tc_kernel + its exact-repair launch (ncu launch
-            # list, profiles/r01/launches_v3.csv)
-            "gpu_launches": 12 * a.steps,
+            # per step: 2 pool8a, scores, pw_plan, softsel, fallback; pack K,
+            # pack V, schedule, compact, bsa_tc_kernel + its exact-repair
+            # launch (Q is read in place; the non-finite scans of unchanged
+            # inputs are cached). ncu launch list: profiles/r02/launches.csv
+            "gpu_launches": (12 if a.mask == "predicted" else 6) * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -54,22 +54,6 @@ namespace tc {
 #ifndef BSA_TC_NB
 #define BSA_TC_NB 6
 #endif
-// SEP: P in its own TMEM buffers (NP of 32 packed columns) instead of over
-// its S buffer.  An S buffer is then free as soon as its group has READ S
-// (SFREE), not when the PV that read P completes: the chain P(j) -> PV(j) ->
-// S(j + NB) leaves the S pipeline.  TMEM: S 3 x 64 | P 6 x 32 | O 80 | Q 32.
-#ifndef BSA_TC_SEP
-#define BSA_TC_SEP 0
-#endif
-#ifndef BSA_TC_NBS
-#define BSA_TC_NBS 3  // (SEP) S buffers
-#endif
-#ifndef BSA_TC_NP
-#define BSA_TC_NP 6   // (SEP) P buffers
-#endif
-#ifndef BSA_TC_LOAD64
-#define BSA_TC_LOAD64 0  // stale-max softmax: load a tile's 64 S columns at once
-#endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
 #endif
@@ -97,9 +81,7 @@ constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 template <bool WIDE>
 struct Cfg {
   static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warp groups (4 warps: the 4 lane quarters)
-  static constexpr bool SEP = WIDE && BSA_TC_SEP != 0;  // P in its own buffers
-  static constexpr int NB = SEP ? BSA_TC_NBS : (WIDE ? BSA_TC_NB : 2);  // S buffers (64 columns)
-  static constexpr int NP = SEP ? BSA_TC_NP : NB;  // P buffers (SEP: 32 columns; else P over S)
+  static constexpr int NB = WIDE ? BSA_TC_NB : 2;  // S buffers (64 columns, P over S)
   static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
   static constexpr int SM_WARPS = 4 * NG;
   // SPLIT: S MMAs and PV MMAs come from two issuer warps (one warp issuing
@@ -127,10 +109,8 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_QUEUE + (SPLIT ? 2 * QUEUE * 4 : 0);
   static constexpr int SMEM_BYTES = OFF_BAR + 1024 + 1024;  // barriers/ring + alignment slack
   static constexpr uint32_t TMEM_COLS = WIDE ? 512 : 256;
-  // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last);
-  // SEP: S0..S(NB-1) | P0..P(NP-1) (32 columns each) | O | Q
-  static constexpr uint32_t TM_S = 0, TM_P = SEP ? NB * 64 : 0, P_STRIDE = SEP ? 32 : 64;
-  static constexpr uint32_t TM_O = SEP ? TM_P + NP * 32 : NB * 64, TM_Q = TMEM_COLS - 32;
+  // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last)
+  static constexpr uint32_t TM_S = 0, TM_O = NB * 64, TM_Q = TMEM_COLS - 32;
   // barrier slots (8 bytes each) inside the barrier region
   static constexpr int B_QFULL = 0;              // [1]  Q in TMEM (all softmax warps)
   static constexpr int B_KFULL = 1;              // [NK]
@@ -138,10 +118,9 @@ struct Cfg {
   static constexpr int B_VFULL = B_KEMPTY + NK;  // [NV]
   static constexpr int B_VEMPTY = B_VFULL + NV;  // [NV]
   static constexpr int B_SFULL = B_VEMPTY + NV;  // [NB]
-  static constexpr int B_SFREE = B_SFULL + NB;   // [NB] (SEP) S read: S buffer reusable
-  static constexpr int B_PFULL = B_SFREE + (SEP ? NB : 0);  // [NP] the warps of the tile
-  static constexpr int B_PFREE = B_PFULL + NP;   // [NP] PV done: P (and, not SEP, S) buffer reusable
-  static constexpr int B_OFULL = B_PFREE + NP;   // [1]
+  static constexpr int B_PFULL = B_SFULL + NB;   // [NB] the warps of the tile
+  static constexpr int B_PFREE = B_PFULL + NB;   // [NB] PV done: S/P buffer reusable
+  static constexpr int B_OFULL = B_PFREE + NB;   // [1]
   static constexpr int B_OEMPTY = B_OFULL + 1;   // [1]
   static constexpr int B_IFULL = B_OEMPTY + 1;   // [2]
   static constexpr int B_IEMPTY = B_IFULL + 2;   // [2]  softmax warps + MMA warp(s)
@@ -266,9 +245,6 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     mbar_init(BAR(C::B_QFULL), SM_WARPS);
     for (int i = 0; i < NB; ++i) {
       mbar_init(BAR(C::B_SFULL + i), 1);
-      if (C::SEP) mbar_init(BAR(C::B_SFREE + i), TILE_WARPS);
-    }
-    for (int i = 0; i < C::NP; ++i) {
       mbar_init(BAR(C::B_PFULL + i), TILE_WARPS);
       mbar_init(BAR(C::B_PFREE + i), 1);
     }
@@ -521,10 +497,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
 #ifdef BSA_TC_TRACE_BUILD
         mbar_wait(BAR(C::B_KFULL + sk), kph);
         if (lane == 0) BSA_TR(3, gs);
-        mbar_wait(BAR((C::SEP ? C::B_SFREE : C::B_PFREE) + sb), sph ^ 1);
+        mbar_wait(BAR(C::B_PFREE + sb), sph ^ 1);
         if (lane == 0) BSA_TR(13, gs);
 #else
-        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR((C::SEP ? C::B_SFREE : C::B_PFREE) + sb), sph ^ 1);
+        mbar_wait2(BAR(C::B_KFULL + sk), kph, BAR(C::B_PFREE + sb), sph ^ 1);
 #endif
         tc_fence_after();
         if (elect_one()) {
@@ -558,7 +534,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
-          const uint32_t pa = tmem + C::TM_P + pb * C::P_STRIDE;
+          const uint32_t pa = tmem + C::TM_S + pb * 64;
           // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
           // column halves: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
@@ -572,7 +548,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         }
         __syncwarp();
         ++gp;
-        if (++pb == (uint32_t)C::NP) { pb = 0; pph ^= 1; }
+        if (++pb == (uint32_t)NB) { pb = 0; pph ^= 1; }
         if (++sv == (uint32_t)NV) { sv = 0; vph ^= 1; }
       };
       if constexpr (C::SPLIT) {
@@ -610,12 +586,11 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     float* x_first = xch;              // [NG][128]
     float* x_tile = xch + NG * BQ;     // [NG][128] (EXACT)
     float* x_l = xch + 2 * NG * BQ;    // [NG][128] (EXACT)
-    // S buffer, its phase and first TMEM column for tile j of the current
-    // item (g: the item's first global tile), and the P buffer (SEP: its own
-    // ring; else P over S)
+    // S/P buffer, its phase and first TMEM column for tile j of the
+    // current item (g: the item's first global tile)
     uint32_t it = 0, g = 0;
     struct ChunkSlot {
-      uint32_t buf, phase, col, pbuf, pphase, pcol;
+      uint32_t buf, phase, col;
     };
     auto slot_of = [&](int j) -> ChunkSlot {
       ChunkSlot z;
@@ -623,9 +598,6 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       z.buf = t % NB;
       z.phase = (t / NB) & 1;
       z.col = C::TM_S + z.buf * 64;
-      z.pbuf = t % C::NP;
-      z.pphase = (t / C::NP) & 1;
-      z.pcol = C::SEP ? C::TM_P + z.pbuf * 32 : z.col;
       return z;
     };
     // the NG warps sharing this TMEM lane quarter
@@ -709,37 +681,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           mbar_wait(BAR(C::B_SFULL + sb), z.phase);
           tc_fence_after();
           if (lane == 0 && quarter == 0) BSA_TR(8, gg);
-#if BSA_TC_LOAD64
-          // (variant) all 64 S columns in one round trip: one TMEM-load
-          // latency per tile instead of one per 32-key half
-          uint32_t sr64[64];
-          tmem_ld32(tmem + lane_off + z.col, &sr64[0]);
-          tmem_ld32(tmem + lane_off + z.col + 32, &sr64[32]);
-          tmem_wait_ld();
-          reg_fence16(&sr64[0]);
-          reg_fence16(&sr64[16]);
-          reg_fence16(&sr64[32]);
-          reg_fence16(&sr64[48]);
-          if (C::SEP) {  // S read: the S issuer may refill this buffer
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR(C::B_SFREE + sb));
-          }
-#endif
-          if (C::SEP) {
-            // our P buffer: the PV that read it NP tiles ago has completed
-            mbar_wait(BAR(C::B_PFREE + z.pbuf), z.pphase ^ 1);
-            tc_fence_after();
-          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             // 32 keys at a time; their P (16 packed columns) goes over S
             // columns this thread has already read
-#if BSA_TC_LOAD64
-            float s[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr64[hh * 32 + e]);
-#else
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
@@ -747,21 +692,15 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             tmem_wait_ld();
             reg_fence16(&sr[0]);
             reg_fence16(&sr[16]);
-            if (C::SEP && hh == 1) {  // S read: the S issuer may refill this buffer
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(BAR(C::B_SFREE + sb));
-            }
             float s[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(sr[e]);
-#endif
             if (len - hh * 32 < 32) {
 #pragma unroll
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
-            const uint32_t p_col = tmem + lane_off + z.pcol + hh * 16;
+            const uint32_t p_col = tmem + lane_off + z.col + hh * 16;
 #if BSA_TC_EXPERIMENT == 1
             {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
@@ -782,7 +721,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(BAR(C::B_PFULL + z.pbuf));
+            mbar_arrive(BAR(C::B_PFULL + sb));
             if (quarter == 0) BSA_TR(16, gg);
           }
         }
