@@ -540,6 +540,107 @@ __global__ void __launch_bounds__(256) scores_kernel(const float* __restrict__ q
   }
 }
 
+// Wide-tile form: 128 q-rows x 256 k-columns per CTA, one CTA per SM.  Warp
+// w owns rows 16w..16w+15 and lane l columns 8l..8l+7 (16 x 8 outputs per
+// thread, 128 accumulators).  All lanes of a warp read the same 16 q values
+// per k step (shared-memory broadcasts), so a k step costs 4 broadcast + 2
+// vector loads for 64 FFMA2: the FMA pipe, not shared-memory bandwidth, is
+// the limit.  Each output is still one sequential fmaf chain over k.
+constexpr int SW_TQ = 128, SW_TK = 256, SW_KC = 16;
+
+__global__ void __launch_bounds__(256, 1) scores_wide_kernel(const float* __restrict__ qp,
+                                                             const float* __restrict__ kp,
+                                                             int64_t nq, int64_t nk, int d,
+                                                             float scale, float* __restrict__ z,
+                                                             int64_t ldz) {
+  __shared__ __align__(16) float qs[2][SW_KC][SW_TQ];
+  __shared__ __align__(16) float ks[2][SW_KC][SW_TK];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int64_t h = blockIdx.z;
+  const int64_t i0 = (int64_t)blockIdx.y * SW_TQ, j0 = (int64_t)blockIdx.x * SW_TK;
+  const float* qh = qp + h * nq * d;
+  const float* kh = kp + h * nk * d;
+  float2 acc[16][4];
+#pragma unroll
+  for (int a = 0; a < 16; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_float2(0.0f, 0.0f);
+  // chunk c0 -> registers (thread t: 8 values of q row t/2, 16 of k row t),
+  // then into stage st transposed to [k][row]: the next chunk's global
+  // loads are in flight while the current chunk is multiplied
+  float rq[8], rk[SW_KC];
+  auto load = [&](int c0) {
+    const int kc = min(SW_KC, d - c0);
+    const int i = tid >> 1, half = tid & 1;
+    const bool qok = i0 + i < nq, kok = j0 + tid < nk;
+    const float* qsrc = qh + (i0 + i) * d + c0 + half * 8;
+    const float* ksrc = kh + (j0 + tid) * d + c0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) rq[u] = (qok && half * 8 + u < kc) ? __ldg(qsrc + u) : 0.0f;
+#pragma unroll
+    for (int u = 0; u < SW_KC; ++u) rk[u] = (kok && u < kc) ? __ldg(ksrc + u) : 0.0f;
+  };
+  auto store = [&](int st) {
+    const int i = tid >> 1, half = tid & 1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) qs[st][half * 8 + u][i] = rq[u];
+#pragma unroll
+    for (int u = 0; u < SW_KC; ++u) ks[st][u][tid] = rk[u];
+  };
+  const int nch = (d + SW_KC - 1) / SW_KC;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch & 1;
+    if (ch + 1 < nch) load((ch + 1) * SW_KC);
+    const int kc = min(SW_KC, d - ch * SW_KC);
+#pragma unroll 4
+    for (int c = 0; c < kc; ++c) {
+      float qv[16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 t = *reinterpret_cast<const float4*>(&qs[st][c][w * 16 + 4 * u]);
+        qv[4 * u] = t.x; qv[4 * u + 1] = t.y; qv[4 * u + 2] = t.z; qv[4 * u + 3] = t.w;
+      }
+      const float4 ka = *reinterpret_cast<const float4*>(&ks[st][c][lane * 8]);
+      const float4 kb = *reinterpret_cast<const float4*>(&ks[st][c][lane * 8 + 4]);
+      const float2 kv[4] = {make_float2(ka.x, ka.y), make_float2(ka.z, ka.w),
+                            make_float2(kb.x, kb.y), make_float2(kb.z, kb.w)};
+#pragma unroll
+      for (int a = 0; a < 16; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          acc[a][b] = __ffma2_rn(make_float2(qv[a], qv[a]), kv[b], acc[a][b]);
+    }
+    // stage st ^ 1 was last read in the previous chunk (behind its barrier)
+    if (ch + 1 < nch) store(st ^ 1);
+    __syncthreads();
+  }
+  const bool vst = (ldz % 4) == 0 && ((uintptr_t)z % 16) == 0;
+  const int64_t jb = j0 + lane * 8;
+#pragma unroll
+  for (int a = 0; a < 16; ++a) {
+    const int64_t i = i0 + w * 16 + a;
+    if (i >= nq) continue;
+    float* zr = z + (h * nq + i) * ldz;
+    float o[8];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      o[2 * b] = __fmul_rn(acc[a][b].x, scale);
+      o[2 * b + 1] = __fmul_rn(acc[a][b].y, scale);
+    }
+    if (vst && jb + 8 <= nk) {
+      reinterpret_cast<float4*>(zr + jb)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(zr + jb)[1] = make_float4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (jb + b < nk) zr[jb + b] = o[b];
+    }
+  }
+}
+
 // ===========================================================================
 // block-level reductions (256 threads)
 // ===========================================================================
@@ -1366,8 +1467,16 @@ static int launch_scores(const float* qp, const float* kp, int64_t H, int64_t nq
   if (nq > 65535LL * SC_TQ || H > 65535)
     return fail(BSA_EUNSUPPORTED, "pooled_scores: grid too large (nq=%lld, heads=%lld)",
                 (long long)nq, (long long)H);
-  dim3 grid((unsigned)ceil_div(nk, SC_TK), (unsigned)ceil_div(nq, SC_TQ), (unsigned)H);
-  scores_kernel<<<grid, 256, 0, st>>>(qp, kp, nq, nk, (int)d, scale, z, ldz);
+#ifndef BSA_SCORES_WIDE
+#define BSA_SCORES_WIDE 1
+#endif
+  if (BSA_SCORES_WIDE) {
+    dim3 grid((unsigned)ceil_div(nk, SW_TK), (unsigned)ceil_div(nq, SW_TQ), (unsigned)H);
+    scores_wide_kernel<<<grid, 256, 0, st>>>(qp, kp, nq, nk, (int)d, scale, z, ldz);
+  } else {
+    dim3 grid((unsigned)ceil_div(nk, SC_TK), (unsigned)ceil_div(nq, SC_TQ), (unsigned)H);
+    scores_kernel<<<grid, 256, 0, st>>>(qp, kp, nq, nk, (int)d, scale, z, ldz);
+  }
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
