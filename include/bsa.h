@@ -129,6 +129,16 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
                      int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* Which scoring kernel predict_mask runs for nk key blocks of head_dim
+ * dim: the fused score+softmax+select kernel's rows per CTA (8 or 4), or 0
+ * for the three-kernel path (rows longer than shared memory holds, head_dim
+ * not a multiple of 32, or BSA_SCORESEL=0 in the environment). */
+int bsa_scoring_rows_per_cta(int64_t nk, int64_t dim);
+/* Diagnostics: with BSA_SCORESEL_DEBUG=2 the fused scoring kernel records
+ * clock64 per K stage of its first CTA (issue, ready, consumed; 512 each);
+ * copies them (synchronously) to host.  Returns 0, or -1 if none recorded. */
+int bsa_debug_scoring_trace(void* host, size_t bytes);
+
 /* ------------------------------------------------------------------ */
 /* Attention stage                                                    */
 /* ------------------------------------------------------------------ */

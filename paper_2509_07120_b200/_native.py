@@ -99,6 +99,8 @@ def _declare(L):
         "bsa_attention_row_stats": ([pt, pt, pl, f32, vp, vp, sz, vp], ctypes.c_int),
         "bsa_block_attention_map": ([pt, pt, pl, f32, vp, vp, vp, sz, vp], ctypes.c_int),
         "bsa_check_finite": ([pt, vp, vp], ctypes.c_int),
+        "bsa_scoring_rows_per_cta": ([i64, i64], ctypes.c_int),
+        "bsa_debug_scoring_trace": ([vp, sz], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -119,6 +121,7 @@ def exported_symbols():
         "bsa_mask_to_csr", "bsa_sparse_attention_scatter", "bsa_ipc_alloc", "bsa_ipc_open",
         "bsa_ipc_close", "bsa_ipc_free", "bsa_attention_stats_workspace",
         "bsa_attention_row_stats", "bsa_block_attention_map", "bsa_check_finite",
+        "bsa_scoring_rows_per_cta", "bsa_debug_scoring_trace",
     ]
 
 

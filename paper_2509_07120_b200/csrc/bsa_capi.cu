@@ -26,7 +26,12 @@ int fail(int code, const char* fmt, ...) {
 
 }  // namespace bsa
 
+namespace bsa { extern unsigned long long* g_scoresel_trace; }
 extern "C" {
+int bsa_debug_scoring_trace(void* host, size_t bytes) {
+  if (!bsa::g_scoresel_trace) return -1;
+  return cudaMemcpy(host, bsa::g_scoresel_trace, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
 
 int bsa_version(void) { return 100; }
 

@@ -26,7 +26,7 @@
 #include <cstring>
 #include <algorithm>
 
-#include "bsa_common.cuh"
+#include "bsa_select.cuh"
 
 namespace bsa {
 
@@ -716,19 +716,6 @@ __device__ __forceinline__ void block_minmax_u(unsigned int& mn, unsigned int& m
   }
 }
 
-// value of a non-negative finite float < 2 in units of 2^-52, exact for
-// p >= 2^-29 (the fp32 ulp is then >= 2^-52), truncated below that.
-__device__ __forceinline__ unsigned long long fx52(unsigned int key) {
-  const unsigned int E = key >> 23;
-  if (E == 0) return 0ull;
-  const unsigned long long m = (unsigned long long)((key & 0x7fffffu) | 0x800000u);
-  const int sh = (int)E - 98;
-  if (sh >= 0) return m << sh;
-  return sh > -40 ? (m >> (-sh)) : 0ull;
-}
-
-constexpr unsigned int KEY_TINY = 98u << 23;   // bits of 2^-29
-constexpr unsigned int KEY_TWO = 128u << 23;   // bits of 2.0f
 
 // mass (2^-52 units) and count of keys >= t, plus count of keys == t
 __device__ __forceinline__ void mass_at_or_above(const unsigned int* keys, int64_t nk,
@@ -1164,26 +1151,6 @@ __global__ void pw_plan_kernel(int64_t n, int32_t* plan) {
   if (threadIdx.x == 0 && blockIdx.x == 0) pw_plan_walk(n, plan, nullptr, nullptr);
 }
 
-// numpy pairwise_sum leaf (n <= 128) over contiguous smem values
-__device__ __forceinline__ float pw_leaf_smem(const float* a, int n) {
-  if (n < 8) {
-    float r = 0.0f;
-    for (int i = 0; i < n; ++i) r = __fadd_rn(r, a[i]);
-    return r;
-  }
-  float r[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = a[j];
-  int i = 8;
-  for (; i < n - (n % 8); i += 8)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], a[i + j]);
-  float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __fadd_rn(res, a[i]);
-  return res;
-}
-
 template <bool SOFTMAX, bool SELECT>
 __global__ void __launch_bounds__(SS_THREADS)
     softsel_kernel(float* __restrict__ src, int64_t ld, int64_t rows, int64_t nk, double tau,
@@ -1592,12 +1559,17 @@ int bsa_select_blocks(const float* probs, int64_t heads, int64_t nq, int64_t nk,
                                      nullptr, mask_bits, counts, ws, (cudaStream_t)stream);
 }
 
+int bsa_scoring_rows_per_cta(int64_t nk, int64_t dim) { return fs_rows_per_cta(nk, dim); }
+
 size_t bsa_predict_mask_workspace(int64_t heads, int64_t patch_tokens, int64_t dim,
                                   int32_t block_q, int32_t block_k) {
   if (heads < 1 || patch_tokens < 1 || dim < 1 || block_q < 1 || block_k < 1) return 0;
   const int64_t nq = ceil_div(patch_tokens, block_q), nk = ceil_div(patch_tokens, block_k);
+  // pooled Q, pooled K, the score matrix (three-kernel path; fused path:
+  // probabilities of fallback rows only), selection workspace, blocked K
   return align_up((size_t)(heads * nq * dim) * 4, 256) + align_up((size_t)(heads * nk * dim) * 4, 256) +
-         align_up((size_t)(heads * nq * nk) * 4, 256) + select_ws_bytes(heads * nq, nk);
+         align_up((size_t)(heads * nq * nk) * 4, 256) + align_up(select_ws_bytes(heads * nq, nk), 256) +
+         align_up(fs_kblock_bytes(heads, nk, dim), 256);
 }
 
 int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* patch_gather,
@@ -1632,7 +1604,31 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
   int64_t n1 = 0, n2 = 0;
   rc = launch_pool(q, patch_gather, block_q, qp, st, &n1);
   if (!rc) rc = launch_pool(k, patch_gather, block_k, kp, st, &n2);
-  if (!rc) rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
+  if (rc) return rc;
+  if (fs_rows_per_cta(nk, d) > 0) {
+    // fused: scores, softmax and selection in one kernel (bsa_scoresel.cu);
+    // z only receives the probability rows of rows handed to the fallback
+    char* sw = w;
+    float* kb = (float*)(w + align_up(select_ws_bytes(H * nq, nk), 256));
+    int32_t* fb_count = (int32_t*)sw;
+    sw += 256;
+    sw += align_up((size_t)plan_ints_for(nk) * 4, 256);
+    int32_t* fb_list = (int32_t*)sw;
+    sw += align_up((size_t)(H * nq) * 4, 256);
+    unsigned long long* scratch = (unsigned long long*)sw;
+    BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
+    rc = launch_scoresel(qp, kp, H, nq, nk, d, scale, tau, k_floor, kb, mask_bits, counts,
+                         probs_out, z, fb_list, fb_count, st);
+    if (rc) return rc;
+    const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
+    BSA_CUDA_TRY(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(fsmem, 16)));
+    fallback_kernel<<<FB_GRID, SS_THREADS, std::max<size_t>(fsmem, 16), st>>>(
+        z, nk, nk, tau, k_floor, mask_bits, counts, fb_list, fb_count, scratch, next_pow2(nk));
+    BSA_LAUNCH_CHECK();
+    return BSA_OK;
+  }
+  rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
   if (!rc)
     rc = launch_softsel<true, true>(z, nk, H * nq, nk, tau, k_floor, probs_out, mask_bits, counts,
                                     w, st);
