@@ -4,11 +4,12 @@ fallback_kernel), which the golden-fixture tests pin to the reference.
 
 Bar: bit-identical masks, per-row counts and probabilities.  The path is
 chosen once per process (BSA_SCORESEL, read at the first call), so each arm
-runs in its own subprocess.  Cases cover both kernel shapes (8 rows per CTA
-at N <= 215 frames, 4 rows beyond), bf16 and fp32 inputs, the top-k floor
-and the CDF branch, rho 0 / 1, tau 1, head_dim 32, the shape the fused
-kernel declines (head_dim 16) and rows handed to the exact fallback
-(constant scores: every probability equal).
+runs in its own subprocess.  Cases cover the launch shapes (two CTAs of 4
+rows per SM up to N ~ 230 frames, one CTA per SM beyond; the one-CTA shapes
+also forced at every size via BSA_SCORESEL_SHAPE=1), bf16 and fp32 inputs,
+the top-k floor and the CDF branch, rho 0 / 1, tau 1, head_dim 32, the shape
+the fused kernel declines (head_dim 16) and rows handed to the exact
+fallback (constant scores: every probability equal).
 """
 
 import os
@@ -60,16 +61,17 @@ np.savez({path!r}, **out)
 """
 
 
-def _run(tmp_path, fused):
-    path = str(tmp_path / f"arm{int(fused)}.npz")
+def _run(tmp_path, fused, shape="0"):
+    path = str(tmp_path / f"arm{int(fused)}_{shape}.npz")
     code = ARM.format(root=ROOT, cases=CASES, path=path)
-    env = dict(os.environ, BSA_SCORESEL="1" if fused else "0")
+    env = dict(os.environ, BSA_SCORESEL="1" if fused else "0", BSA_SCORESEL_SHAPE=shape)
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
     return np.load(path)
 
 
-def test_fused_scoring_bit_identical_to_three_kernel_path(tmp_path):
-    legacy, fused = _run(tmp_path, False), _run(tmp_path, True)
+@pytest.mark.parametrize("shape", ["0", "1"])
+def test_fused_scoring_bit_identical_to_three_kernel_path(tmp_path, shape):
+    legacy, fused = _run(tmp_path, False), _run(tmp_path, True, shape)
     for name, *_ in CASES:
         for part in ("bits", "counts", "probs"):
             a, b = legacy[f"{name}/{part}"], fused[f"{name}/{part}"]
@@ -80,7 +82,7 @@ def test_fused_scoring_engaged_at_the_bench_shape():
     """The C ABI reports the fused kernel's rows per CTA (0: three-kernel path)."""
     from paper_2509_07120_b200 import _native as N
     L = N.lib()
-    assert L.bsa_scoring_rows_per_cta(4280, 64) == 8    # N=200 (bench)
+    assert L.bsa_scoring_rows_per_cta(4280, 64) == 4    # N=200 (bench): two CTAs per SM
     assert L.bsa_scoring_rows_per_cta(6418, 64) == 4    # N=300 (pi3)
     assert L.bsa_scoring_rows_per_cta(21390, 64) == 0   # N=1000: rows exceed shared memory
     assert L.bsa_scoring_rows_per_cta(4280, 16) == 0    # head_dim not a multiple of 32
