@@ -369,6 +369,11 @@ def run_ours(a):
         except (OSError, ValueError, KeyError):
             pass
 
+    scoring_launches = 0
+    if a.mask == "predicted":
+        from paper_2509_07120_b200 import _native as N
+        fused = N.lib().bsa_scoring_rows_per_cta(g.nk_blocks, d) > 0
+        scoring_launches = 5 if fused else 6
     # scoring roofline (predict_mask): HBM bytes it must move -- the bf16
     # patch rows of Q and K read once, the mask bits and counts written --
     # and the exact fp32 pooled dot products on the FMA pipe
@@ -496,11 +501,13 @@ def run_ours(a):
                          "peak_burst": burst_tf, "frac_of_burst": achieved_tf / burst_tf},
             "scoring": scoring,
             "e2e": e2e,
-            # per step: 2 pool8a, scores, pw_plan, softsel, fallback; pack K,
-            # pack V, schedule, compact, bsa_tc_kernel + its exact-repair
-            # launch (Q is read in place; the non-finite scans of unchanged
-            # inputs are cached). ncu launch list: profiles/r02/launches.csv
-            "gpu_launches": (12 if a.mask == "predicted" else 6) * a.steps,
+            # per step: scoring = 2 pool8a, kblock, scoresel (fused scores +
+            # softmax + select), fallback (three-kernel path: 2 pool8a,
+            # scores, pw_plan, softsel, fallback); attention = pack K, pack V,
+            # schedule, compact, bsa_tc_kernel + its exact-repair launch (Q is
+            # read in place; the non-finite scans of unchanged inputs are
+            # cached). ncu launch list: profiles/r02b/launches.csv
+            "gpu_launches": (scoring_launches + 6) * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
