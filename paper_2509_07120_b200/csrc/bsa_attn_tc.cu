@@ -54,6 +54,9 @@ namespace tc {
 #ifndef BSA_TC_NB
 #define BSA_TC_NB 6
 #endif
+#ifndef BSA_TC_COLH
+#define BSA_TC_COLH 0  // stale-max launch: tiles split into key halves (2 tile groups of 8 warps)
+#endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
 #endif
@@ -80,7 +83,11 @@ constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 // producer and one MMA warp.
 template <bool WIDE>
 struct Cfg {
-  static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warp groups (4 warps: the 4 lane quarters)
+  static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warps per TMEM lane quarter
+  // key halves per tile (2: each of a tile's two 32-key halves has its own
+  // four warps) and tile groups (tile j goes to group j % NTG)
+  static constexpr int HALVES = WIDE ? (BSA_TC_COLH ? 2 : 1) : 2;
+  static constexpr int NTG = NG / HALVES;
   static constexpr int NB = WIDE ? BSA_TC_NB : 2;  // S buffers (64 columns, P over S)
   static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
   static constexpr int SM_WARPS = 4 * NG;
@@ -210,8 +217,9 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   constexpr int SM_WARPS = C::SM_WARPS;
   // warps that write one tile's P: one group (stale max, whole tiles), or
   // both groups (exact max, column halves of every tile)
-  constexpr int TILE_WARPS = EXACT ? SM_WARPS : 4;
-  static_assert(!EXACT || NG == 2, "the exact launch splits tiles into two column halves");
+  constexpr int HALVES = C::HALVES, NTG = C::NTG;
+  constexpr int TILE_WARPS = 4 * HALVES;
+  static_assert(!EXACT || (NG == 2 && HALVES == 2), "the exact launch splits tiles into two column halves");
   (void)tm_q;  // Q goes to TMEM from the softmax warps' registers
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -540,7 +548,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k)
             if (BSA_TC_EXPERIMENT != 2)
-              mma_ts(tmem + C::TM_O, pa + (EXACT ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
+              mma_ts(tmem + C::TM_O, pa + (HALVES == 2 ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
                      dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
           tc_commit(BAR(C::B_PFREE + pb));
           tc_commit(BAR(C::B_VEMPTY + sv));
@@ -645,9 +653,11 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       float m = NEG_INF, l = 0.0f;
       bool ovf = false;
       if constexpr (!EXACT) {
-        // ---- stale max: group grp takes tiles j with (g + j) % NG == grp ----
-        const int first_grp = (int)(g % NG);  // group that owns the item's tile 0
-        if (grp == first_grp) {
+        // ---- stale max: tile group tg takes tiles j with (g + j) % NTG == tg;
+        // with HALVES == 2 its warps split every tile into key halves ----
+        const int half = HALVES == 2 ? (grp & 1) : 0, tg = grp / HALVES;
+        const int first_tg = (int)(g % NTG);  // tile group that owns the item's tile 0
+        if (tg == first_tg) {
           // tile 0's row max becomes the item's offset
           const ChunkSlot z = slot_of(0);
           mbar_wait(BAR(C::B_SFULL + z.buf), z.phase);
@@ -655,7 +665,8 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           const int len0 = chunk_len(I, 0);
           float mx = NEG_INF;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int h2 = 0; h2 < 3 - HALVES; ++h2) {
+            const int hh = HALVES == 2 ? half : h2;
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
@@ -668,23 +679,25 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             for (int e = 0; e < 32; ++e) s[e] = e + hh * 32 < len0 ? __uint_as_float(sr[e]) : NEG_INF;
             mx = fmaxf(mx, max32(s));
           }
-          x_first[row] = mx;
+          x_first[half * BQ + row] = mx;
         }
         quarter_sync();
-        m = x_first[row] * sl2;
-        for (int j = (grp - first_grp + NG) % NG; j < ntiles; j += NG) {
+        m = (HALVES == 2 ? fmaxf(x_first[row], x_first[BQ + row]) : x_first[row]) * sl2;
+        for (int j = (tg - first_tg + NTG) % NTG; j < ntiles; j += NTG) {
           const uint32_t gg = g + j;
           const ChunkSlot z = slot_of(j);
           const uint32_t sb = z.buf;
           const int len = chunk_len(I, j);
-          if (lane == 0 && quarter == 0) BSA_TR(4, gg);
+          if (lane == 0 && quarter == 0 && half == 0) BSA_TR(4, gg);
           mbar_wait(BAR(C::B_SFULL + sb), z.phase);
           tc_fence_after();
-          if (lane == 0 && quarter == 0) BSA_TR(8, gg);
+          if (lane == 0 && quarter == 0 && half == 0) BSA_TR(8, gg);
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int h2 = 0; h2 < 3 - HALVES; ++h2) {
+            const int hh = HALVES == 2 ? half : h2;
             // 32 keys at a time; their P (16 packed columns) goes over S
-            // columns this thread has already read
+            // columns this thread has already read (whole tiles: columns
+            // 16hh..; key halves: each half's own columns 32hh..)
             uint32_t sr[32];
             const uint32_t s_col = tmem + lane_off + z.col + hh * 32;
             tmem_ld16(s_col, &sr[0]);
@@ -700,7 +713,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
-            const uint32_t p_col = tmem + lane_off + z.col + hh * 16;
+            const uint32_t p_col = tmem + lane_off + z.col + hh * (HALVES == 2 ? 32 : 16);
 #if BSA_TC_EXPERIMENT == 1
             {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
@@ -716,13 +729,13 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             }
 #endif
           }
-          if (lane == 0 && quarter == 0) BSA_TR(12, gg);
+          if (lane == 0 && quarter == 0 && half == 0) BSA_TR(12, gg);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
             mbar_arrive(BAR(C::B_PFULL + sb));
-            if (quarter == 0) BSA_TR(16, gg);
+            if (quarter == 0 && half == 0) BSA_TR(16, gg);
           }
         }
       } else {
