@@ -99,6 +99,24 @@ struct KeyChunker {
 int launch_simt_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
                           void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
                           int permuted, float scale, int shard, int num_shards, cudaStream_t st);
+// SIMT recomputation of listed tensor-core work items (whole rows, exact
+// online softmax): list[0..*count) of item codes (h * nr + r) * M + li,
+// li < nst special-row tiles, else patch q-block li - nst; 128-row items.
+struct SimtList {
+  const int32_t* list;
+  const int32_t* count;
+  int64_t M, nst;
+  int32_t nr;
+  int64_t cap;
+};
+// the caller's fp32 inputs, for the X3 launch's SIMT repair of overflowed items
+struct SimtRepair {
+  const bsa_tensor *q, *k, *v;
+  float scale;
+};
+int launch_simt_attention_list(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                               void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
+                               int permuted, float scale, const SimtList& sl, cudaStream_t st);
 
 // Key-range split (long sequences): the keys of a head are cut into `nr`
 // ranges of `rb` key blocks (rb % 8 == 0, so a range is a byte range of the
@@ -122,6 +140,10 @@ struct TcArgs {
   float* part_lse;            // (nr, H, T): offset + log2(l)
   const __nv_bfloat16* qp;   // Q: packed partitioned (H, T, 64), or (q_src) the caller's
                              // bf16 q in its own token order and strides
+  const __nv_bfloat16* qp_lo; // (x3) Q lo, packed beside qp (fp32 inputs split into bf16 hi + lo)
+  int x3;                    // fp32 inputs: three-MMA split-bf16 products (kp/vp hi, kp_lo/vp_lo lo)
+  const __nv_bfloat16* kp_lo;
+  const __nv_bfloat16* vp_lo;
   int q_src;                 // 1: qp is the caller's q; row = permuted ? pr : part_src(pr)
   int64_t q_sH, q_sT;        // element strides of qp (packed: T*64, 64)
   int64_t kv_sH, kv_sT;      // element strides of kp / vp (packed: T*64, 64)
@@ -174,13 +196,15 @@ struct CombineArgs {
   const int64_t* token_begin;
 };
 int launch_combine(const AttnGeom& G, const CombineArgs& c, cudaStream_t st);
+struct SimtRepair;
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
-                        const CombineArgs* comb);
+                        const CombineArgs* comb, const SimtRepair* rep = nullptr);
 cudaEvent_t timing_events(int which);
 size_t tc_smem_bytes();
 // source-order (f32|bf16) Q/K/V -> contiguous bf16 [specials | patches]
 // (bsa_attn_host.cu; also used by the dense-statistics kernels)
+// (fp32 x, lo != null: also the residual x - bf16(x) rounded to bf16)
 int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
-                cudaStream_t st);
+                cudaStream_t st, __nv_bfloat16* lo = nullptr);
 
 }  // namespace bsa

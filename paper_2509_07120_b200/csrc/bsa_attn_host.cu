@@ -23,7 +23,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 template <typename T>
 __global__ void pack_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int64_t H,
                             int64_t ntok, int d, Layout L, int permuted,
-                            __nv_bfloat16* __restrict__ out) {
+                            __nv_bfloat16* __restrict__ out, __nv_bfloat16* __restrict__ lo) {
   // one thread per 8 output elements (d % 8 == 0)
   const int64_t per_row = d / 8;
   const int64_t total = H * ntok * per_row;
@@ -47,6 +47,19 @@ __global__ void pack_kernel(const T* __restrict__ x, int64_t sH, int64_t sT, int
       t = __floats2bfloat162_rn(v[4], v[5]); o.z = *reinterpret_cast<uint32_t*>(&t);
       t = __floats2bfloat162_rn(v[6], v[7]); o.w = *reinterpret_cast<uint32_t*>(&t);
       *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = o;
+      if (lo) {
+        // the residual x - bf16(x) (exact in fp32), rounded to bf16: hi + lo
+        // carries ~16 significant bits (the X3 tensor-core path)
+        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+        uint32_t r[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+          t = __floats2bfloat162_rn(v[2 * e] - h.x, v[2 * e + 1] - h.y);
+          r[e] = *reinterpret_cast<uint32_t*>(&t);
+        }
+        *reinterpret_cast<uint4*>(lo + hr * d + c8 * 8) = make_uint4(r[0], r[1], r[2], r[3]);
+      }
     } else {
       *reinterpret_cast<uint4*>(out + hr * d + c8 * 8) = *reinterpret_cast<const uint4*>(p);
     }
@@ -408,8 +421,10 @@ static int check_qkv(const bsa_tensor* t, const char* name) {
 
 static int choose_path(const AttnGeom& G, int32_t in_dtype, int32_t flags) {
   flags &= 0xF;  // path bits; BSA_FLAG_* live above
-  const bool tc_ok = in_dtype == BSA_BF16 && G.d == 64 && G.bq == 128 && G.bk == 64 &&
-                     G.T < (1LL << 31) && G.H < 65536;
+  // bf16: the tcgen05 kernel; fp32: its X3 form (split-bf16 hi + lo
+  // operands, three MMAs per product, fp32-level accuracy)
+  const bool tc_ok = (in_dtype == BSA_BF16 || in_dtype == BSA_F32) && G.d == 64 && G.bq == 128 &&
+                     G.bk == 64 && G.T < (1LL << 31) && G.H < 65536;
   if (flags == BSA_PATH_SIMT) return BSA_PATH_SIMT;
   if (flags == BSA_PATH_TC) return tc_ok ? BSA_PATH_TC : -BSA_EUNSUPPORTED;
   return tc_ok ? BSA_PATH_TC : BSA_PATH_SIMT;
@@ -418,7 +433,7 @@ static int choose_path(const AttnGeom& G, int32_t in_dtype, int32_t flags) {
 // key-range split of the keys of one head (KeyRanges).  requested: 0 = auto:
 // one range while a head's K+V (bf16) fits comfortably in L2, else ranges of
 // about 64 MB of K+V each; else the requested number (capped at nk / 8).
-static KeyRanges choose_ranges(const AttnGeom& G, int requested) {
+static KeyRanges choose_ranges(const AttnGeom& G, int requested, bool x3) {
   KeyRanges kr;
   kr.rcounts = nullptr;
   const int64_t nk8 = ceil_div(G.nk, 8);  // whole mask bytes
@@ -426,7 +441,7 @@ static KeyRanges choose_ranges(const AttnGeom& G, int requested) {
   if (requested > 0) {
     nr = requested;
   } else {
-    const int64_t kv_head = 2 * G.T * G.d * 2;
+    const int64_t kv_head = 2 * G.T * G.d * 2 * (x3 ? 2 : 1);  // (X3: hi + lo)
     nr = kv_head <= (96ll << 20) ? 1 : ceil_div(kv_head, 64ll << 20);
   }
   nr = std::max<int64_t>(1, std::min<int64_t>(nr, nk8));
@@ -439,6 +454,7 @@ static KeyRanges choose_ranges(const AttnGeom& G, int requested) {
 struct TcWorkspace {
   __nv_bfloat16 *qp, *kp;
   void* vp;
+  __nv_bfloat16 *qp_lo, *kp_lo, *vp_lo;  // (X3) lo parts
   int32_t *items, *counter, *counts, *vshift;
   int32_t *ovf_flags, *ovf_list, *ovf_count;
   int32_t *row_shard, *tmp, *head_count, *n_items, *rcounts;
@@ -450,7 +466,7 @@ struct TcWorkspace {
 };
 
 static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G, const KeyRanges& kr,
-                                bool part_bf16) {
+                                bool part_bf16, bool x3) {
   TcWorkspace w;
   char* p = (char*)base;
   const size_t tens = align_up((size_t)(G.H * G.T * G.d) * 2, 256);
@@ -461,6 +477,12 @@ static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G, const KeyRanges& 
   w.qp = (__nv_bfloat16*)p; p += tens;
   w.kp = (__nv_bfloat16*)p; p += tens;
   w.vp = (void*)p; p += tens;
+  w.qp_lo = w.kp_lo = w.vp_lo = nullptr;
+  if (x3) {
+    w.qp_lo = (__nv_bfloat16*)p; p += tens;
+    w.kp_lo = (__nv_bfloat16*)p; p += tens;
+    w.vp_lo = (__nv_bfloat16*)p; p += tens;
+  }
   w.items = (int32_t*)p; p += capb;
   w.counter = (int32_t*)p; p += 256;
   w.counts = (int32_t*)p; p += align_up((size_t)(G.H * G.nq) * 4, 256);
@@ -487,7 +509,7 @@ static TcWorkspace tc_ws_layout(void* base, const AttnGeom& G, const KeyRanges& 
 }
 
 int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloat16* out,
-                cudaStream_t st) {
+                cudaStream_t st, __nv_bfloat16* lo) {
   const int64_t total = G.H * G.T * (G.d / 8);
   const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
   const bool bf = x->dtype == BSA_BF16;
@@ -497,10 +519,11 @@ int launch_pack(const bsa_tensor* x, const AttnGeom& G, int permuted, __nv_bfloa
   if (bf)
     pack_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x->data,
                                                      x->stride_head, x->stride_token, G.H, G.T,
-                                                     G.d, G.L, permuted, out);
+                                                     G.d, G.L, permuted, out, nullptr);
   else
     pack_kernel<float><<<grid, 256, 0, st>>>((const float*)x->data, x->stride_head,
-                                             x->stride_token, G.H, G.T, G.d, G.L, permuted, out);
+                                             x->stride_token, G.H, G.T, G.d, G.L, permuted, out,
+                                             lo);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
@@ -553,7 +576,9 @@ size_t bsa_sparse_attention_workspace(const bsa_layout* layout, int64_t heads, i
   const AttnGeom G = make_geom(to_layout(layout), heads, (int)dim, block_q, block_k);
   if (choose_path(G, in_dtype, flags) != BSA_PATH_TC) return 256;
   // fp32 partials cover either output dtype
-  return tc_ws_layout(nullptr, G, choose_ranges(G, BSA_FLAG_RANGES_GET(flags)), false).bytes + 256;
+  const bool x3 = in_dtype == BSA_F32;
+  return tc_ws_layout(nullptr, G, choose_ranges(G, BSA_FLAG_RANGES_GET(flags), x3), false, x3).bytes +
+         256;
 }
 
 static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
@@ -584,10 +609,24 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   if (num_shards < 1) num_shards = 1;
   if (shard < 0 || shard >= num_shards) return fail(BSA_EINVAL, "shard %d of %d", shard, num_shards);
   const AttnGeom G = make_geom(L, q->heads, (int)q->dim, block_q, block_k);
-  const int path = choose_path(G, q->dtype, flags);
+  int path = choose_path(G, q->dtype, flags);
+  const bool x3 = path == BSA_PATH_TC && q->dtype == BSA_F32;
+  if (x3) {
+    // the split pack reads 16-byte fp32 vectors; unaligned inputs (or the
+    // multi-GPU scatter, bf16-only) keep the CUDA-core path
+    auto al16 = [](const bsa_tensor* t) {
+      return (uintptr_t)t->data % 16 == 0 && (t->stride_token * 4) % 16 == 0 &&
+             (t->stride_head * 4) % 16 == 0;
+    };
+    if (!al16(q) || !al16(k) || !al16(v) || scatter) {
+      if ((flags & 0xF) == BSA_PATH_TC)
+        return fail(BSA_EUNSUPPORTED, "fp32 tensor-core path: 16-byte aligned inputs, no scatter");
+      path = BSA_PATH_SIMT;
+    }
+  }
   if (path < 0)
     return fail(BSA_EUNSUPPORTED,
-                "tensor-core path needs bf16 inputs, head_dim 64, block_q 128, block_k 64");
+                "tensor-core path needs bf16 or fp32 inputs, head_dim 64, block_q 128, block_k 64");
   cudaStream_t st = (cudaStream_t)stream;
   if (scatter) {
     if (path != BSA_PATH_TC || out_dtype != BSA_BF16 || inputs_permuted)
@@ -609,9 +648,9 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   }
   const int req_ranges = BSA_FLAG_RANGES_GET(flags) ? BSA_FLAG_RANGES_GET(flags)
                                                     : (env_ranges > 0 ? env_ranges : 0);
-  const KeyRanges KR = choose_ranges(G, req_ranges);
+  const KeyRanges KR = choose_ranges(G, req_ranges, x3);
   const bool part_bf16 = out_dtype == BSA_BF16;
-  TcWorkspace W = tc_ws_layout(ws, G, KR, part_bf16);
+  TcWorkspace W = tc_ws_layout(ws, G, KR, part_bf16, x3);
   if (ws_bytes < W.bytes) return fail(BSA_EINVAL, "sparse_attention: workspace too small");
   // kernel variant: exp2 split between MUFU and the FMA pipe, P/V precision
   static int env_poly = -2, env_f16 = -2;
@@ -621,11 +660,11 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
     const char* f = getenv("BSA_TC_F16P");
     env_f16 = f ? atoi(f) : -1;
   }
-  const int v_f16 = env_f16 >= 0 ? env_f16 : 0;
+  const int v_f16 = x3 ? 0 : (env_f16 >= 0 ? env_f16 : 0);
   // 3 of every 8 exp2 pairs on the FMA pipe (degree-2 polynomial), the rest
   // on MUFU: the kernel is MUFU-bound at d=64 (profiles/r01_summary.md);
   // measured 0: 90.0 ms, 2: 85.4, 3: 84.5, 4: 90.9
-  const int exp_poly = env_poly >= 0 ? env_poly : 3;
+  const int exp_poly = x3 ? 0 : (env_poly >= 0 ? env_poly : 3);
   // Pack passes only where the kernel cannot read the caller's tensors:
   //  * Q (read row by row by the softmax warps) is used in place whenever it
   //    is bf16 with 16-byte aligned rows: the partitioned-order gather is the
@@ -638,15 +677,15 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
     return t->dtype == BSA_BF16 && (uintptr_t)t->data % 16 == 0 && (t->stride_token * 2) % 16 == 0 &&
            (t->stride_head * 2) % 16 == 0;
   };
-  const bool q_direct = aligned16(q);
-  const bool kv_direct = !v_f16 && inputs_permuted && aligned16(k) && aligned16(v) &&
+  const bool q_direct = !x3 && aligned16(q);
+  const bool kv_direct = !x3 && !v_f16 && inputs_permuted && aligned16(k) && aligned16(v) &&
                          k->stride_token == v->stride_token && k->stride_head == v->stride_head;
-  if (!q_direct) rc = launch_pack(q, G, inputs_permuted, W.qp, st);
+  if (!q_direct) rc = launch_pack(q, G, inputs_permuted, W.qp, st, W.qp_lo);
   if (!rc && !kv_direct) {
-    rc = launch_pack(k, G, inputs_permuted, W.kp, st);
+    rc = launch_pack(k, G, inputs_permuted, W.kp, st, W.kp_lo);
     if (!rc)
       rc = v_f16 ? launch_pack_v(v, G, inputs_permuted, W.vamax, W.vshift, (__half*)W.vp, st)
-                 : launch_pack(v, G, inputs_permuted, (__nv_bfloat16*)W.vp, st);
+                 : launch_pack(v, G, inputs_permuted, (__nv_bfloat16*)W.vp, st, W.vp_lo);
   }
   if (rc) return rc;
   const int64_t rows = G.H * G.nq;
@@ -692,6 +731,10 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   a.part_lse = W.part_lse;
   a.qp = q_direct ? (const __nv_bfloat16*)q->data : W.qp;
   a.q_src = q_direct ? 1 : 0;
+  a.x3 = x3 ? 1 : 0;
+  a.qp_lo = W.qp_lo;
+  a.kp_lo = W.kp_lo;
+  a.vp_lo = W.vp_lo;
   a.q_sH = q_direct ? q->stride_head : G.T * G.d;
   a.q_sT = q_direct ? q->stride_token : G.d;
   a.kp = kv_direct ? (const __nv_bfloat16*)k->data : W.kp;
@@ -741,7 +784,12 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
   c.scatter_world = a.scatter_world;
   c.out_ptrs = a.out_ptrs;
   c.token_begin = a.token_begin;
-  return launch_tc_attention(G, a, st, &c);
+  SimtRepair sr;
+  sr.q = q;
+  sr.k = k;
+  sr.v = v;
+  sr.scale = scale;
+  return launch_tc_attention(G, a, st, &c, x3 ? &sr : nullptr);
 }
 
 int bsa_sparse_attention(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,

@@ -14,6 +14,8 @@
 // Inputs are read in interleaved source order with the [specials | patches]
 // permutation (layout.py:113-132) folded into row addressing, and outputs
 // are written back in source order (sparse.py:176-177, :205).
+#include <algorithm>
+
 #include "bsa_attn.cuh"
 
 namespace bsa {
@@ -22,26 +24,19 @@ constexpr int SM_ROWS = 32;    // query rows per CTA
 constexpr int SM_CHUNK = 64;   // keys per smem chunk
 constexpr int SM_THREADS = 256;
 
+// one 32-row tile ti of head h (special-row tiles first, then 4 tiles per
+// patch q-block of 128 rows)
 template <typename T, int DMAX>
-__global__ void __launch_bounds__(SM_THREADS)
-    simt_attn_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
-                     int64_t qsH, int64_t qsT, int64_t ksH, int64_t ksT, int64_t vsH,
-                     int64_t vsT, void* __restrict__ out, int out_bf16, AttnGeom G,
-                     const uint8_t* __restrict__ mask_bits, int permuted, float scale,
-                     int shard, int num_shards) {
+__device__ void simt_tile(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                          int64_t qsH, int64_t qsT, int64_t ksH, int64_t ksT, int64_t vsH,
+                          int64_t vsT, void* __restrict__ out, int out_bf16, const AttnGeom& G,
+                          const uint8_t* __restrict__ mask_bits, int permuted, float scale,
+                          int64_t h, int64_t ti) {
   extern __shared__ float smem_f[];
   float (*Qs)[DMAX] = reinterpret_cast<float (*)[DMAX]>(smem_f);
   float (*Ks)[DMAX + 1] = reinterpret_cast<float (*)[DMAX + 1]>(smem_f + SM_ROWS * DMAX);
   float (*Vs)[DMAX] =
       reinterpret_cast<float (*)[DMAX]>(smem_f + SM_ROWS * DMAX + SM_CHUNK * (DMAX + 1));
-
-  const int64_t tiles_per_head = G.simt_tiles_per_head();
-  int64_t item = blockIdx.x;
-  if (num_shards > 1) {
-    if (item % num_shards != shard) return;
-  }
-  const int64_t h = item / tiles_per_head;
-  const int64_t ti = item % tiles_per_head;
   const int64_t nspec_tiles = ceil_div(G.Ts, SM_ROWS);
   const int sub_per_qb = (int)ceil_div(G.bq, SM_ROWS);
 
@@ -171,6 +166,51 @@ __global__ void __launch_bounds__(SM_THREADS)
 }
 
 template <typename T, int DMAX>
+__global__ void __launch_bounds__(SM_THREADS)
+    simt_attn_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                     int64_t qsH, int64_t qsT, int64_t ksH, int64_t ksT, int64_t vsH,
+                     int64_t vsT, void* __restrict__ out, int out_bf16, AttnGeom G,
+                     const uint8_t* __restrict__ mask_bits, int permuted, float scale,
+                     int shard, int num_shards) {
+  const int64_t tiles_per_head = G.simt_tiles_per_head();
+  int64_t item = blockIdx.x;
+  if (num_shards > 1) {
+    if (item % num_shards != shard) return;
+  }
+  simt_tile<T, DMAX>(q, k, v, qsH, qsT, ksH, ksT, vsH, vsT, out, out_bf16, G, mask_bits, permuted,
+                     scale, item / tiles_per_head, item % tiles_per_head);
+}
+
+// recomputes listed tensor-core items (128-row tiles: 4 SIMT tiles each)
+template <typename T, int DMAX>
+__global__ void __launch_bounds__(SM_THREADS)
+    simt_list_kernel(const T* __restrict__ q, const T* __restrict__ k, const T* __restrict__ v,
+                     int64_t qsH, int64_t qsT, int64_t ksH, int64_t ksT, int64_t vsH,
+                     int64_t vsT, void* __restrict__ out, int out_bf16, AttnGeom G,
+                     const uint8_t* __restrict__ mask_bits, int permuted, float scale,
+                     SimtList sl) {
+  const int64_t n = 4 * (int64_t)*sl.count;
+  const int64_t nspec_tiles = ceil_div(G.Ts, SM_ROWS);
+  const int64_t sub_per_qb = ceil_div(G.bq, SM_ROWS);
+  for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
+    const int32_t code = sl.list[idx / 4];
+    const int sub = (int)(idx % 4);
+    const int64_t li = code % sl.M, h = (code / sl.M) / sl.nr;
+    int64_t ti;
+    if (li < sl.nst) {
+      ti = li * 4 + sub;
+      if (ti >= nspec_tiles) continue;
+    } else {
+      if (sub >= sub_per_qb) continue;
+      ti = nspec_tiles + (li - sl.nst) * sub_per_qb + sub;
+    }
+    __syncthreads();  // the previous tile's warps are done with shared memory
+    simt_tile<T, DMAX>(q, k, v, qsH, qsT, ksH, ksT, vsH, vsT, out, out_bf16, G, mask_bits,
+                       permuted, scale, h, ti);
+  }
+}
+
+template <typename T, int DMAX>
 static int launch_simt_t(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
                          void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
                          int permuted, float scale, int shard, int num_shards, cudaStream_t st) {
@@ -183,6 +223,24 @@ static int launch_simt_t(const bsa_tensor* q, const bsa_tensor* k, const bsa_ten
       (const T*)q->data, (const T*)k->data, (const T*)v->data, q->stride_head, q->stride_token,
       k->stride_head, k->stride_token, v->stride_head, v->stride_token, out,
       out_dtype == BSA_BF16, G, bits, permuted, scale, shard, num_shards);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+int launch_simt_attention_list(const bsa_tensor* q, const bsa_tensor* k, const bsa_tensor* v,
+                               void* out, int out_dtype, const AttnGeom& G, const uint8_t* bits,
+                               int permuted, float scale, const SimtList& sl, cudaStream_t st) {
+  if (q->dtype != BSA_F32 || G.d != 64 || G.bq != 128)
+    return fail(BSA_EUNSUPPORTED, "SIMT item repair: fp32 inputs, head_dim 64, block_q 128");
+  constexpr int DMAX = 64;
+  const size_t smem = sizeof(float) * (SM_ROWS * DMAX + SM_CHUNK * (DMAX + 1) + SM_CHUNK * DMAX);
+  BSA_CUDA_TRY(cudaFuncSetAttribute(simt_list_kernel<float, DMAX>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(4 * sl.cap, 1), 148 * 4);
+  simt_list_kernel<float, DMAX><<<grid, SM_THREADS, smem, st>>>(
+      (const float*)q->data, (const float*)k->data, (const float*)v->data, q->stride_head,
+      q->stride_token, k->stride_head, k->stride_token, v->stride_head, v->stride_token, out,
+      out_dtype == BSA_BF16, G, bits, permuted, scale, sl);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }

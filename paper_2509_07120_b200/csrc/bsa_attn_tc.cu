@@ -81,14 +81,19 @@ constexpr uint32_t O_COLS = LSUM ? 80 : 64;
 // Narrow (the exact-max repair launch): two CTAs per SM, 256 columns each,
 // two groups splitting every tile into column halves, two buffers, one
 // producer and one MMA warp.
-template <bool WIDE>
+// X3 (fp32 inputs): every operand is split into bf16 hi + lo parts and
+// each product is formed from three MMAs (hi*hi + hi*lo + lo*hi, fp32
+// accumulation): S and O carry ~2^-16 relative error instead of bf16's 2^-8,
+// which meets the fp32 path's 1e-4 bar.  Five S/P buffers (Q hi and lo both
+// in TMEM), K stages [hi | lo], V stages [hi | ones | lo].
+template <bool WIDE, bool X3 = false>
 struct Cfg {
   static constexpr int NG = WIDE ? BSA_TC_NG : 2;  // softmax warps per TMEM lane quarter
   // key halves per tile (2: each of a tile's two 32-key halves has its own
   // four warps) and tile groups (tile j goes to group j % NTG)
   static constexpr int HALVES = WIDE ? (BSA_TC_COLH ? 2 : 1) : 2;
   static constexpr int NTG = NG / HALVES;
-  static constexpr int NB = WIDE ? BSA_TC_NB : 2;  // S buffers (64 columns, P over S)
+  static constexpr int NB = X3 ? 5 : (WIDE ? BSA_TC_NB : 2);  // S buffers (64 columns, P over S)
   static constexpr int LEAD = 1;  // (one issuer warp) S(j + LEAD) is issued before PV(j)
   static constexpr int SM_WARPS = 4 * NG;
   // SPLIT: S MMAs and PV MMAs come from two issuer warps (one warp issuing
@@ -106,11 +111,13 @@ struct Cfg {
   // every 4th warp of the SM's CTAs (8-register granules)
   static constexpr int WARPS_PER_SMSP = (CTAS_PER_SM * NUM_THREADS / 32 + 3) / 4;
   static constexpr int MAX_REGS = (16384 / (32 * WARPS_PER_SMSP)) / 8 * 8;
-  static constexpr int NK = WIDE ? 8 : 5, NV = WIDE ? (LSUM ? 6 : 10) : 4;
+  static constexpr int NK = X3 ? 5 : (WIDE ? 8 : 5), NV = X3 ? 4 : (WIDE ? (LSUM ? 6 : 10) : 4);
   static constexpr int VLAG = 2;  // (one producer warp) K(j) is loaded VLAG tiles before V(j)
-  static constexpr int V_STAGE = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // V tile (+ ones block)
+  static constexpr int V_STAGE = (LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES) + (X3 ? CHUNK_BYTES : 0);
+  static constexpr int K_STAGE = X3 ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // K tile (X3: hi | lo)
+  static constexpr int V_LO = LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES;   // (X3) V lo tile offset
   static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + NK * CHUNK_BYTES;
+  static constexpr int OFF_V = OFF_K + NK * K_STAGE;
   static constexpr int OFF_XCH = OFF_V + NV * V_STAGE;  // [3][NG][128] floats
   static constexpr int OFF_QUEUE = OFF_XCH + 3 * NG * BQ * 4;  // (SPLIT) [2][QUEUE] int32
   static constexpr int OFF_BAR = OFF_QUEUE + (SPLIT ? 2 * QUEUE * 4 : 0);
@@ -118,6 +125,7 @@ struct Cfg {
   static constexpr uint32_t TMEM_COLS = WIDE ? 512 : 256;
   // TMEM: S0..S(NB-1) (64 columns each, P over S) | O (80) | Q (32, last)
   static constexpr uint32_t TM_S = 0, TM_O = NB * 64, TM_Q = TMEM_COLS - 32;
+  static constexpr uint32_t TM_QL = TM_Q - 32;  // (X3) Q lo
   // barrier slots (8 bytes each) inside the barrier region
   static constexpr int B_QFULL = 0;              // [1]  Q in TMEM (all softmax warps)
   static constexpr int B_KFULL = 1;              // [NK]
@@ -134,7 +142,8 @@ struct Cfg {
   static constexpr int B_COUNT = B_IEMPTY + 2;
   static_assert(B_COUNT * 8 + 100 <= 1024, "barrier region (+ item ring, TMEM address)");
   static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
-  static_assert(TM_O + O_COLS <= TM_Q, "TMEM columns");
+  static_assert(TM_O + O_COLS <= (X3 ? TM_QL : TM_Q), "TMEM columns");
+  static_assert(!X3 || (WIDE && LSUM), "X3 runs in the stale-max launch with LSUM");
   static_assert(LEAD >= 1 && LEAD < NB, "S(j+LEAD) must only wait for a PV issued earlier");
 };
 using CfgMain = Cfg<BSA_TC_WIDE != 0>;
@@ -188,6 +197,29 @@ __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float
   return t.x + t.y;
 }
 
+// (X3) largest |logit| (log2 units) a row may reach on the tensor cores:
+// there a score's ~2^-16 relative error stays below ~2.5e-4 in the exponent
+constexpr float X3_XLIM = 16.0f;
+
+// (X3) P = exp2(s * scale_log2 - m) for one 32-key half row, all on MUFU
+// (ex2.approx, ~2^-22 relative), split into bf16 hi + lo = P to ~2^-16:
+// hi packed into 16 TMEM columns at p_taddr, lo into the 16 after them.
+__device__ __forceinline__ void exp_half_x3(const float (&s)[32], float sl2, float m,
+                                            uint32_t p_taddr) {
+  const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
+  uint32_t hi[16], lo[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
+    const float p0 = ex2(x.x), p1 = ex2(x.y);
+    hi[e] = pack_bf16(p0, p1);
+    const float2 h = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hi[e]));
+    lo[e] = pack_bf16(p0 - h.x, p1 - h.y);
+  }
+  tmem_st16(p_taddr, hi);
+  tmem_st16(p_taddr + 16, lo);
+}
+
 // debug pipeline trace (BSA_TC_TRACE): clock64 of event `ev` for key tile `idx`
 // of CTA 0; TRACE_TILES tiles per event.  Compiled in only with
 // -DBSA_TC_TRACE_BUILD: the clock reads split the scheduler's basic blocks.
@@ -208,11 +240,16 @@ constexpr int TRACE_TILES = 512, TRACE_EVENTS = 20;
 // the kernel.  EXACT: the repair launch (per-tile max, lazy O rescaling) over
 // the items the stale-max launch listed.
 // ---------------------------------------------------------------------------
-template <int POLY, bool F16P, bool EXACT>
-__global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
-    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, AttnGeom G, TcArgs A) {
-  using C = Cfg<BSA_TC_WIDE != 0 && !EXACT>;
+template <bool WIDE, bool X3>
+constexpr int max_regs_of() { return Cfg<WIDE, X3>::MAX_REGS; }
+
+template <int POLY, bool F16P, bool EXACT, bool X3 = false>
+__global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
+    bsa_tc_kernel(const __grid_constant__ CUtensorMap tm_kl, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_vl,
+                  AttnGeom G, TcArgs A) {
+  using C = Cfg<BSA_TC_WIDE != 0 && !EXACT, X3>;
+  static_assert(!X3 || (POLY == 0 && !F16P && !EXACT), "X3: MUFU exponentials, bf16 P, stale max");
   constexpr int NG = C::NG, NB = C::NB, NK = C::NK, NV = C::NV, VLAG = C::VLAG;
   constexpr int SM_WARPS = C::SM_WARPS;
   // warps that write one tile's P: one group (stale max, whole tiles), or
@@ -220,7 +257,8 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   constexpr int HALVES = C::HALVES, NTG = C::NTG;
   constexpr int TILE_WARPS = 4 * HALVES;
   static_assert(!EXACT || (NG == 2 && HALVES == 2), "the exact launch splits tiles into two column halves");
-  (void)tm_q;  // Q goes to TMEM from the softmax warps' registers
+  (void)tm_kl;  // (X3 only) K lo, V lo maps
+  (void)tm_vl;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -291,6 +329,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
   if (warp == C::PRODUCER_WARP && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
+    if constexpr (X3) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_kl) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_vl) : "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -387,18 +429,24 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
           if (lane == 0) BSA_TR(9, gx);
           mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
           if (elect_one()) {
-            mbar_expect_tx(BAR(C::B_KFULL + st), CHUNK_BYTES);
-            tma_load_3d(sbase + C::OFF_K + st * CHUNK_BYTES, &tm_k, BAR(C::B_KFULL + st), 0, s0,
+            mbar_expect_tx(BAR(C::B_KFULL + st), C::K_STAGE);
+            tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0, s0,
                         I.h);
+            if constexpr (X3)
+              tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE + CHUNK_BYTES, &tm_kl,
+                          BAR(C::B_KFULL + st), 0, s0, I.h);
             BSA_TR(0, gx);
           }
         } else {
           const uint32_t st = gx % NV;
           mbar_wait(BAR(C::B_VEMPTY + st), ((gx / NV) & 1) ^ 1);
           if (elect_one()) {
-            mbar_expect_tx(BAR(C::B_VFULL + st), CHUNK_BYTES);
+            mbar_expect_tx(BAR(C::B_VFULL + st), X3 ? 2 * CHUNK_BYTES : CHUNK_BYTES);
             tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0,
                         I.h);
+            if constexpr (X3)
+              tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE + C::V_LO, &tm_vl,
+                          BAR(C::B_VFULL + st), 0, s0, I.h);
             BSA_TR(6, gx);
           }
         }
@@ -454,7 +502,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         mbar_wait(BAR(C::B_KEMPTY + st), ((gk / NK) & 1) ^ 1);
         if (elect_one()) {
           mbar_expect_tx(BAR(C::B_KFULL + st), CHUNK_BYTES);
-          tma_load_3d(sbase + C::OFF_K + st * CHUNK_BYTES, &tm_k, BAR(C::B_KFULL + st), 0, (int)s0,
+          tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0, (int)s0,
                       I.h);
           BSA_TR(0, gk);
         }
@@ -483,8 +531,10 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
     uint32_t pb = 0, pph = 0, sv = 0, vph = 0;  // PV issue: P buffer, V stage
     const uint32_t id_s = idesc_f16(128, 64, 0, 1);                  // bf16 Q x bf16 K
     const uint32_t id_pv = idesc_f16(128, O_COLS, 1, F16P ? 0 : 1);   // P x [V | ones]
+    const uint32_t id_pv64 = idesc_f16(128, 64, 1, 1);                // (X3) P hi x V lo
     const uint64_t dk0 = sdesc(sbase + C::OFF_K, 16, 1024);
     const uint64_t dv0 = sdesc(sbase + C::OFF_V, 8192, 1024);
+    const uint64_t dvl0 = sdesc(sbase + C::OFF_V + C::V_LO, 8192, 1024);
     while (true) {
       const uint32_t slot = it & 1;
       mbar_wait(BAR(C::B_IFULL + slot), (it >> 1) & 1);
@@ -512,12 +562,17 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
 #endif
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t dk = dk0 + (uint64_t)(sk * (CHUNK_BYTES >> 4));
+          const uint64_t dk = dk0 + (uint64_t)(sk * (C::K_STAGE >> 4));
           const uint32_t ds = tmem + C::TM_S + sb * 64;
 #pragma unroll
           for (int k = 0; k < D / 16; ++k) {
             if (BSA_TC_EXPERIMENT == 2) continue;
             mma_ts(ds, tmem + C::TM_Q + k * 8, dk + (uint64_t)(2 * k), id_s, k > 0 ? 1u : 0u);
+            if constexpr (X3) {
+              // Q hi x K lo, Q lo x K hi
+              mma_ts(ds, tmem + C::TM_Q + k * 8, dk + (uint64_t)((CHUNK_BYTES >> 4) + 2 * k), id_s, 1u);
+              mma_ts(ds, tmem + C::TM_QL + k * 8, dk + (uint64_t)(2 * k), id_s, 1u);
+            }
           }
           tc_commit(BAR(C::B_SFULL + sb));
           tc_commit(BAR(C::B_KEMPTY + sk));
@@ -542,14 +597,26 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         tc_fence_after();
         if (elect_one()) {
           const uint64_t dv = dv0 + (uint64_t)(sv * (C::V_STAGE >> 4));
+          const uint64_t dvl = dvl0 + (uint64_t)(sv * (C::V_STAGE >> 4));
           const uint32_t pa = tmem + C::TM_S + pb * 64;
           // keys 16k..16k+15.  Whole tiles: P packed over S columns 0-31;
           // column halves: half k>>1 wrote its P over S columns 32*(k>>1)
 #pragma unroll
-          for (int k = 0; k < CH / 16; ++k)
-            if (BSA_TC_EXPERIMENT != 2)
+          for (int k = 0; k < CH / 16; ++k) {
+            if (BSA_TC_EXPERIMENT == 2) continue;
+            if constexpr (X3) {
+              // keys 16k..: P hi at S columns 32(k>>1) + 8(k&1), P lo 16 further;
+              // O += Ph [Vh | 1] + Pl [Vh | 1] + Ph Vl (the ones column sums Ph + Pl)
+              const uint32_t ph = pa + (k >> 1) * 32 + (k & 1) * 8;
+              mma_ts(tmem + C::TM_O, ph, dv + (uint64_t)(k * (2048 >> 4)), id_pv,
+                     (jj > 0 || k > 0) ? 1u : 0u);
+              mma_ts(tmem + C::TM_O, ph + 16, dv + (uint64_t)(k * (2048 >> 4)), id_pv, 1u);
+              mma_ts(tmem + C::TM_O, ph, dvl + (uint64_t)(k * (2048 >> 4)), id_pv64, 1u);
+            } else {
               mma_ts(tmem + C::TM_O, pa + (HALVES == 2 ? (k >> 1) * 32 + (k & 1) * 8 : k * 8),
                      dv + (uint64_t)(k * (2048 >> 4)), id_pv, (jj > 0 || k > 0) ? 1u : 0u);
+            }
+          }
           tc_commit(BAR(C::B_PFREE + pb));
           tc_commit(BAR(C::B_VEMPTY + sv));
           BSA_TR(2, gp);
@@ -644,6 +711,17 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
             for (int e = 0; e < 8; ++e) qr[e] = 0u;
           }
           tmem_st8(tmem + lane_off + C::TM_Q + c * 8, qr);
+          if constexpr (X3) {
+            // Q lo: packed beside Q hi (same partitioned layout and strides)
+            if (pr < (int32_t)G.T) {
+              const uint4* src = reinterpret_cast<const uint4*>(
+                  A.qp_lo + (int64_t)I.h * A.q_sH + qrow * A.q_sT + c * 16);
+              const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+              qr[0] = v0.x; qr[1] = v0.y; qr[2] = v0.z; qr[3] = v0.w;
+              qr[4] = v1.x; qr[5] = v1.y; qr[6] = v1.z; qr[7] = v1.w;
+            }
+            tmem_st8(tmem + lane_off + C::TM_QL + c * 8, qr);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
@@ -652,6 +730,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
       }
       float m = NEG_INF, l = 0.0f;
       bool ovf = false;
+      float xm = NEG_INF;  // (X3) the row's largest score over this warp's tiles
       if constexpr (!EXACT) {
         // ---- stale max: tile group tg takes tiles j with (g + j) % NTG == tg;
         // with HALVES == 2 its warps split every tile into key halves ----
@@ -713,7 +792,7 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               for (int e = 0; e < 32; ++e)
                 if (e + hh * 32 >= len) s[e] = NEG_INF;
             }
-            const uint32_t p_col = tmem + lane_off + z.col + hh * (HALVES == 2 ? 32 : 16);
+            const uint32_t p_col = tmem + lane_off + z.col + hh * (HALVES == 2 || X3 ? 32 : 16);
 #if BSA_TC_EXPERIMENT == 1
             {  // timing experiment: no exponentials (results are wrong)
               uint32_t r[16];
@@ -722,10 +801,15 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
               tmem_st16(p_col, r);
             }
 #else
-            const float lt = exp_half<POLY, F16P, !LSUM>(s, sl2, m, p_col);
-            if constexpr (!LSUM) {
-              ovf |= !(lt <= P_LIMIT);
-              l += lt;
+            if constexpr (X3) {
+              xm = fmaxf(xm, max32(s));
+              exp_half_x3(s, sl2, m, p_col);
+            } else {
+              const float lt = exp_half<POLY, F16P, !LSUM>(s, sl2, m, p_col);
+              if constexpr (!LSUM) {
+                ovf |= !(lt <= P_LIMIT);
+                l += lt;
+              }
             }
 #endif
           }
@@ -822,6 +906,17 @@ __global__ void __maxnreg__(Cfg<BSA_TC_WIDE != 0 && !EXACT>::MAX_REGS)
         asm volatile("" : "+r"(lr));
         ltot = __uint_as_float(lr);
         ovf = !(ltot <= 1.2676506e30f);  // 2^100: also keeps O = sum p v finite
+      }
+      if constexpr (X3) {
+        // split-bf16 scores carry ~2^-16 relative error, i.e. an absolute
+        // error growing with the logit: rows whose largest logit exceeds
+        // X3_XLIM (log2 units) go to the exact CUDA-core repair as well
+        x_tile[grp * BQ + row] = xm;
+        quarter_sync();
+        float xall = x_tile[row];
+#pragma unroll
+        for (int q = 1; q < NG; ++q) xall = fmaxf(xall, x_tile[q * BQ + row]);
+        ovf |= !(fabsf(xall * sl2) <= X3_XLIM);
       }
       const bool store = row < I.rows;
       const int32_t pr = I.row0 + row;
@@ -938,6 +1033,11 @@ static int make_map(CUtensorMap* map, const void* base, int64_t H, int64_t T, in
 
 size_t tc_smem_bytes() { return tc::CfgMain::SMEM_BYTES; }
 
+// maps of one launch: K and V (bf16 or fp16 V), and (X3) the K / V lo parts
+struct TcMaps {
+  CUtensorMap k, v, kl, vl;
+};
+
 // events bracketing the most recent timed attention-kernel launch (per thread)
 cudaEvent_t timing_events(int which) {
   static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -948,32 +1048,34 @@ cudaEvent_t timing_events(int which) {
   return ev[which];
 }
 
-template <int POLY, bool F16P, bool EXACT>
-static int launch_variant(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                          const AttnGeom& G,
-                          const TcArgs& a, int grid, cudaStream_t st) {
-  using C = tc::Cfg<BSA_TC_WIDE != 0 && !EXACT>;
-  auto kern = tc::bsa_tc_kernel<POLY, F16P, EXACT>;
+template <int POLY, bool F16P, bool EXACT, bool X3 = false>
+static int launch_variant(const TcMaps& m, const AttnGeom& G, const TcArgs& a, int grid,
+                          cudaStream_t st) {
+  using C = tc::Cfg<BSA_TC_WIDE != 0 && !EXACT, X3>;
+  auto kern = tc::bsa_tc_kernel<POLY, F16P, EXACT, X3>;
   BSA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES));
-  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(mq, mk, mv, G, a);
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, st>>>(m.kl, m.k, m.v, m.vl, G, a);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
 
 template <bool EXACT>
-static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                       const AttnGeom& G,
-                       const TcArgs& a, int grid, cudaStream_t st) {
+static int launch_pick(const TcMaps& m, const AttnGeom& G, const TcArgs& a, int grid,
+                       cudaStream_t st) {
+  if (a.x3) {
+    if constexpr (EXACT) return fail(BSA_EINVAL, "X3 items are repaired by the SIMT kernel");
+    else return launch_variant<0, false, false, true>(m, G, a, grid, st);
+  }
   switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {
-    case 0: return launch_variant<0, false, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 1: return launch_variant<1, false, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 2: return launch_variant<2, false, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 3: return launch_variant<3, false, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 4: return launch_variant<4, false, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 16: return launch_variant<0, true, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 18: return launch_variant<2, true, EXACT>(mq, mk, mv, G, a, grid, st);
-    case 19: return launch_variant<3, true, EXACT>(mq, mk, mv, G, a, grid, st);
+    case 0: return launch_variant<0, false, EXACT>(m, G, a, grid, st);
+    case 1: return launch_variant<1, false, EXACT>(m, G, a, grid, st);
+    case 2: return launch_variant<2, false, EXACT>(m, G, a, grid, st);
+    case 3: return launch_variant<3, false, EXACT>(m, G, a, grid, st);
+    case 4: return launch_variant<4, false, EXACT>(m, G, a, grid, st);
+    case 16: return launch_variant<0, true, EXACT>(m, G, a, grid, st);
+    case 18: return launch_variant<2, true, EXACT>(m, G, a, grid, st);
+    case 19: return launch_variant<3, true, EXACT>(m, G, a, grid, st);
     default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
   }
 }
@@ -984,32 +1086,56 @@ static int launch_pick(const CUtensorMap& mq, const CUtensorMap& mk, const CUten
 // launch reads a zero count and its CTAs exit at once).  With a key-range
 // split, the combine kernel then merges each row's range partials.
 int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
-                        const CombineArgs* comb) {
-  CUtensorMap mk, mv;
-  int rc = make_map(&mk, a.kp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH);
+                        const CombineArgs* comb, const SimtRepair* rep) {
+  TcMaps m;
+  int rc = make_map(&m.k, a.kp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH);
   if (!rc)
-    rc = make_map(&mv, a.vp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH,
+    rc = make_map(&m.v, a.vp, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH,
                   a.v_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
   if (rc) return rc;
-  const CUtensorMap& mq = mk;  // the kernel's Q map parameter is unused (Q goes via registers)
+  m.kl = m.k;
+  m.vl = m.v;
+  if (a.x3) {
+    rc = make_map(&m.kl, a.kp_lo, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH);
+    if (!rc) rc = make_map(&m.vl, a.vp_lo, G.H, G.T, tc::CH, a.kv_sT, a.kv_sH);
+    if (rc) return rc;
+    if (!rep) return fail(BSA_EINVAL, "X3 launch needs the SIMT repair inputs");
+  }
   int dev = 0, sms = 148;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = (int)std::min<int64_t>((int64_t)sms * tc::CfgMain::CTAS_PER_SM,
                                           std::max<int64_t>(1, a.n_items));
+  static_assert(tc::Cfg<true, true>::CTAS_PER_SM == tc::CfgMain::CTAS_PER_SM, "X3 grid");
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_flags, 0, (size_t)a.n_items * 4, st));
   BSA_CUDA_TRY(cudaMemsetAsync(a.ovf_count, 0, 4, st));
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(0), st));
-  rc = launch_pick<false>(mq, mk, mv, G, a, grid, st);
+  rc = launch_pick<false>(m, G, a, grid, st);
   if (rc) return rc;
-  TcArgs r = a;  // repair launch
-  r.items = a.ovf_list;
-  r.n_items_dev = a.ovf_count;
-  r.work_counter = a.work_counter + 1;
-  rc = launch_pick<true>(mq, mk, mv, G, r, sms, st);
-  if (rc) return rc;
+  if (!a.x3) {
+    TcArgs r = a;  // repair launch
+    r.items = a.ovf_list;
+    r.n_items_dev = a.ovf_count;
+    r.work_counter = a.work_counter + 1;
+    rc = launch_pick<true>(m, G, r, sms, st);
+    if (rc) return rc;
+  }
   if (a.kr.nr > 1 && comb) {
     rc = launch_combine(G, *comb, st);
+    if (rc) return rc;
+  }
+  if (a.x3) {
+    // overflowed items (stale offset exceeded by ~2^100): whole rows again on
+    // the CUDA cores, exact online softmax, after the combine so they win
+    SimtList sl;
+    sl.list = a.ovf_list;
+    sl.count = a.ovf_count;
+    sl.nst = ceil_div(G.Ts, 128);
+    sl.M = sl.nst + G.nq;
+    sl.nr = a.kr.nr;
+    sl.cap = a.n_items;
+    rc = launch_simt_attention_list(rep->q, rep->k, rep->v, a.out, a.out_bf16 ? BSA_BF16 : BSA_F32,
+                                    G, a.bits, a.permuted_out, rep->scale, sl, st);
     if (rc) return rc;
   }
   if (a.timing) BSA_CUDA_TRY(cudaEventRecord(timing_events(1), st));

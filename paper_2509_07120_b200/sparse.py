@@ -82,7 +82,7 @@ def attention_path(job: SparseAttentionJob, path: str = "auto") -> str:
         N.layout_desc(job.layout), job.inputs.head_dim, g.block_q, g.block_k,
         N.BSA_BF16 if job.inputs.q.dtype == torch.bfloat16 else N.BSA_F32, _PATHS[path])
     if code < 0:
-        raise ValueError("tensor-core path needs bf16 inputs, head_dim 64, block_q 128, block_k 64")
+        raise ValueError("tensor-core path needs bf16 or fp32 inputs, head_dim 64, block_q 128, block_k 64")
     return "tc" if code == N.PATH_TC else "simt"
 
 

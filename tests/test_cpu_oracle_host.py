@@ -234,7 +234,8 @@ def test_path_selection_without_gpu():
     L = N.lib()
     lay = N.BsaLayout(200, 1369, 5, 1)
     assert L.bsa_sparse_attention_path(lay, 64, 128, 64, N.BSA_BF16, 0) == N.PATH_TC
-    assert L.bsa_sparse_attention_path(lay, 64, 128, 64, N.BSA_F32, 0) == N.PATH_SIMT
+    assert L.bsa_sparse_attention_path(lay, 64, 128, 64, N.BSA_F32, 0) == N.PATH_TC  # X3
+    assert L.bsa_sparse_attention_path(lay, 64, 128, 64, N.BSA_F32, 1) == N.PATH_SIMT
     assert L.bsa_sparse_attention_path(lay, 32, 64, 32, N.BSA_BF16, 0) == N.PATH_SIMT
     assert L.bsa_sparse_attention_path(lay, 32, 64, 32, N.BSA_BF16, 2) < 0
     ws = L.bsa_sparse_attention_workspace(lay, 16, 64, 128, 64, N.BSA_BF16, 0, 0)
