@@ -350,7 +350,18 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
     // mask bytes per step: popc + warp scan) into a shared-memory queue, so
     // the per-tile cost is one queue read, one barrier wait and one TMA.
     const bool is_k = warp == C::PRODUCER_WARP;
-    int32_t* queue = reinterpret_cast<int32_t*>(smem + C::OFF_QUEUE) + (is_k ? 0 : C::QUEUE);
+    // the queue through its shared-window address (LDS / STS): the generic
+    // pointer (smem is realigned at run time) compiles to generic LD / ST,
+    // slower on this per-tile path
+    const uint32_t qbase = sbase + C::OFF_QUEUE + (is_k ? 0u : 4u * C::QUEUE);
+    auto q_st = [&](int i, int32_t v) {
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(qbase + 4u * (uint32_t)i), "r"(v) : "memory");
+    };
+    auto q_ld = [&](int i) -> int32_t {
+      int32_t v;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(qbase + 4u * (uint32_t)i) : "memory");
+      return v;
+    };
     uint32_t it = 0, gx = 0;
     while (true) {
       const uint32_t slot = it & 1;
@@ -393,7 +404,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
           if (pos < end) {
             const int64_t left = (end - pos + CH - 1) / CH;
             const int n = (int)(left < C::QUEUE ? left : C::QUEUE);
-            for (int e = lane; e < n; e += 32) queue[e] = (int32_t)(pos + (int64_t)e * CH);
+            for (int e = lane; e < n; e += 32) q_st(e, (int32_t)(pos + (int64_t)e * CH));
             pos += (int64_t)n * CH;
             qt = n;
           } else {
@@ -411,19 +422,19 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
               while (byte) {
                 const int bit = __ffs(byte) - 1;
                 byte &= byte - 1;
-                queue[k++] = (int32_t)(G.Ts + (b * 8 + bit) * CH);
+                q_st(k++, (int32_t)(G.Ts + (b * 8 + bit) * CH));
               }
               qt = __shfl_sync(0xffffffffu, incl, 31);
               bp += 32;
             }
             if (qt == 0) {  // mask and counts disagree: keep the pipeline moving
-              queue[0] = (int32_t)G.Ts;
+              q_st(0, (int32_t)G.Ts);
               qt = 1;
             }
           }
           __syncwarp();
         }
-        const int32_t s0 = queue[qh++];
+        const int32_t s0 = q_ld(qh++);
         if (is_k) {
           const uint32_t st = gx % NK;
           if (lane == 0) BSA_TR(9, gx);
