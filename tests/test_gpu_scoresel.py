@@ -84,5 +84,5 @@ def test_fused_scoring_engaged_at_the_bench_shape():
     L = N.lib()
     assert L.bsa_scoring_rows_per_cta(4280, 64) == 4    # N=200 (bench): two CTAs per SM
     assert L.bsa_scoring_rows_per_cta(6418, 64) == 4    # N=300 (pi3)
-    assert L.bsa_scoring_rows_per_cta(21390, 64) == 0   # N=1000: rows exceed shared memory
+    assert L.bsa_scoring_rows_per_cta(21390, 64) == 1   # N=1000: one row per CTA, 16-CTA clusters
     assert L.bsa_scoring_rows_per_cta(4280, 16) == 0    # head_dim not a multiple of 32
