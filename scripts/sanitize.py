@@ -1,10 +1,12 @@
 """Small-shape driver for compute-sanitizer (memcheck / racecheck / synccheck
 / initcheck) over every kernel family of libbsa.so:
 
-  scoring     pool8/pool8a/pool, scores, pw_plan, softsel (softmax + select,
-              tau=0 and tau>0), fallback (forced by an unnormalised row)
+  scoring     pool8/pool8a/pool, kblock + the fused scoresel kernel (tau=0
+              and tau>0; BSA_SCORESEL=0: scores, pw_plan, softsel), fallback
+              (forced by an unnormalised row)
   attention   pack, schedule, bsa_tc_kernel stale-max launch + exact-max
               repair launch (large logits force overflowed items), the fp32
+              X3 launch + its CUDA-core repair of large-logit rows, the fp32
               SIMT kernel, the scatter epilogue (1 emulated rank)
   analysis    bsa_stats_kernel passes 1 and 2
 
@@ -63,7 +65,15 @@ def main():
     out = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(qr, kr, vb), lay, mask))
     ok &= bool(torch.isfinite(out.float()).all())
     print("tc attention (repair launch): finite", bool(torch.isfinite(out.float()).all()), flush=True)
-    out32 = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask))
+    job32 = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask)
+    out32 = bsa.sparse_attention(job32)
+    ok &= bool(torch.isfinite(out32).all())
+    print("fp32 tc (X3) attention: finite", bool(torch.isfinite(out32).all()), flush=True)
+    out32 = bsa.sparse_attention(bsa.SparseAttentionJob(
+        bsa.AttentionInputs(q * 6.0, k * 6.0 * ramp, v), lay, mask))
+    ok &= bool(torch.isfinite(out32).all())
+    print("fp32 tc (X3) + CUDA-core repair: finite", bool(torch.isfinite(out32).all()), flush=True)
+    out32 = bsa.sparse_attention(job32, path="simt")
     ok &= bool(torch.isfinite(out32).all())
     print("simt attention: finite", bool(torch.isfinite(out32).all()), flush=True)
 
