@@ -342,3 +342,30 @@ def test_fp32_tensor_core_large_logit_rows_repaired(bsa, oracle, gain):
     ref = oracle.masked_attention_f64(q, k, v, 2, 600, 5, blocks, 128, 64)
     assert np.isfinite(out).all()
     assert np.abs(out - ref).max() <= FP32_ABS_TOL
+
+
+@pytest.mark.parametrize("ranges", [1, 3])
+def test_fp32_tensor_core_key_ranges_and_shards(bsa, oracle, ranges):
+    """The X3 path with its key range split (per-range partials merged by the
+    combine kernel, then the CUDA-core repair of large-logit rows on top) and
+    with the work list dealt to 3 shards: the union equals the unsharded
+    call bit for bit, and both meet the fp32 bar against float64."""
+    import torch
+    lay = bsa.TokenLayout(4, 700, 5)
+    q, k, v = make_qkv(2, lay.total_tokens, 64, 123)
+    pidx = bsa.patch_token_indices(lay)
+    k[:, pidx[-200:]] *= 8.0  # some rows past the X3 logit limit -> repaired
+    g = bsa.BlockGeometry(lay.patch_tokens, 128, 64)
+    blocks = _random_mask(np.random.default_rng(9), g, 2, 0.4)
+    dq, dk, dv = (torch.from_numpy(t).cuda() for t in (q, k, v))
+    job = bsa.SparseAttentionJob(bsa.AttentionInputs(dq, dk, dv), lay, bsa.BlockMask(blocks, g))
+    assert bsa.attention_path(job) == "tc"
+    full = bsa.sparse_attention(job, key_ranges=ranges)
+    union = torch.zeros_like(full)
+    for s in range(3):
+        part = torch.zeros_like(full)
+        bsa.sparse_attention(job, shard=s, num_shards=3, key_ranges=ranges, out=part)
+        union += part
+    assert torch.equal(union, full)
+    ref = oracle.masked_attention_f64(q, k, v, 4, 700, 5, blocks, 128, 64)
+    assert np.abs(full.cpu().numpy() - ref).max() <= FP32_ABS_TOL
