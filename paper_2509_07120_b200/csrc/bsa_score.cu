@@ -1619,6 +1619,7 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
     BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
     rc = launch_scoresel(qp, kp, H, nq, nk, d, scale, tau, k_floor, kb, mask_bits, counts,
                          probs_out, z, fb_list, fb_count, st);
+    if (rc == FS_NO_CLUSTER) goto three_kernels;
     if (rc) return rc;
     const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
     BSA_CUDA_TRY(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1628,6 +1629,7 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
     BSA_LAUNCH_CHECK();
     return BSA_OK;
   }
+three_kernels:
   rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
   if (!rc)
     rc = launch_softsel<true, true>(z, nk, H * nq, nk, tau, k_floor, probs_out, mask_bits, counts,

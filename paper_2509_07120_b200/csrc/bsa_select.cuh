@@ -58,6 +58,9 @@ int fs_rows_per_cta(int64_t nk, int64_t d);
 // proven exact on the fast path get their probabilities written to
 // fb_probs + r*nk and are listed in fb_list / fb_count (*fb_count zeroed by
 // the caller) for fallback_kernel.  kb: fs_kblock_bytes() of workspace.
+// returned by launch_scoresel (before its kernel) when the GPU cannot
+// co-schedule the cluster shape; the caller then runs the three kernels
+constexpr int FS_NO_CLUSTER = 1000;
 int launch_scoresel(const float* qp, const float* kp, int64_t H, int64_t nq, int64_t nk,
                     int64_t d, float scale, double tau, int64_t k_floor, float* kb,
                     uint8_t* bits, int32_t* counts, float* probs_out, float* fb_probs,
