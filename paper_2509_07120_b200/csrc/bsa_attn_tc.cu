@@ -57,6 +57,9 @@ namespace tc {
 #ifndef BSA_TC_COLH
 #define BSA_TC_COLH 0  // stale-max launch: tiles split into key halves (2 tile groups of 8 warps)
 #endif
+#ifndef BSA_TC_MERGED
+#define BSA_TC_MERGED 1
+#endif
 #ifndef BSA_TC_NG
 #define BSA_TC_NG 4
 #endif
@@ -111,7 +114,11 @@ struct Cfg {
   // every 4th warp of the SM's CTAs (8-register granules)
   static constexpr int WARPS_PER_SMSP = (CTAS_PER_SM * NUM_THREADS / 32 + 3) / 4;
   static constexpr int MAX_REGS = (16384 / (32 * WARPS_PER_SMSP)) / 8 * 8;
-  static constexpr int NK = X3 ? 5 : (WIDE ? 8 : 5), NV = X3 ? 4 : (WIDE ? (LSUM ? 6 : 10) : 4);
+  // MERGED: K and V rings of NB stages, released by the S / PV commits that
+  // already signal SFULL / PFREE (one commit per tile per issuer, not two)
+  static constexpr bool MERGED = WIDE && !X3 && LSUM && BSA_TC_MERGED != 0;
+  static constexpr int NK = MERGED ? NB : (X3 ? 5 : (WIDE ? 8 : 5));
+  static constexpr int NV = MERGED ? NB : (X3 ? 4 : (WIDE ? (LSUM ? 6 : 10) : 4));
   static constexpr int VLAG = 2;  // (one producer warp) K(j) is loaded VLAG tiles before V(j)
   static constexpr int V_STAGE = (LSUM ? 2 * CHUNK_BYTES : CHUNK_BYTES) + (X3 ? CHUNK_BYTES : 0);
   static constexpr int K_STAGE = X3 ? 2 * CHUNK_BYTES : CHUNK_BYTES;  // K tile (X3: hi | lo)
@@ -438,7 +445,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
         if (is_k) {
           const uint32_t st = gx % NK;
           if (lane == 0) BSA_TR(9, gx);
-          mbar_wait(BAR(C::B_KEMPTY + st), ((gx / NK) & 1) ^ 1);
+          mbar_wait(BAR((C::MERGED ? C::B_SFULL : C::B_KEMPTY) + st), ((gx / NK) & 1) ^ 1);
           if (elect_one()) {
             mbar_expect_tx(BAR(C::B_KFULL + st), C::K_STAGE);
             tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0, s0,
@@ -450,7 +457,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
           }
         } else {
           const uint32_t st = gx % NV;
-          mbar_wait(BAR(C::B_VEMPTY + st), ((gx / NV) & 1) ^ 1);
+          mbar_wait(BAR((C::MERGED ? C::B_PFREE : C::B_VEMPTY) + st), ((gx / NV) & 1) ^ 1);
           if (elect_one()) {
             mbar_expect_tx(BAR(C::B_VFULL + st), X3 ? 2 * CHUNK_BYTES : CHUNK_BYTES);
             tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0,
@@ -586,7 +593,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
             }
           }
           tc_commit(BAR(C::B_SFULL + sb));
-          tc_commit(BAR(C::B_KEMPTY + sk));
+          if constexpr (!C::MERGED) tc_commit(BAR(C::B_KEMPTY + sk));
           BSA_TR(1, gs);
         }
         __syncwarp();
@@ -629,7 +636,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
             }
           }
           tc_commit(BAR(C::B_PFREE + pb));
-          tc_commit(BAR(C::B_VEMPTY + sv));
+          if constexpr (!C::MERGED) tc_commit(BAR(C::B_VEMPTY + sv));
           BSA_TR(2, gp);
         }
         __syncwarp();
