@@ -661,10 +661,12 @@ static int sparse_attention_impl(const bsa_tensor* q, const bsa_tensor* k, const
     env_f16 = f ? atoi(f) : -1;
   }
   const int v_f16 = x3 ? 0 : (env_f16 >= 0 ? env_f16 : 0);
-  // 3 of every 8 exp2 pairs on the FMA pipe (degree-2 polynomial), the rest
-  // on MUFU: the kernel is MUFU-bound at d=64 (profiles/r01_summary.md);
-  // measured 0: 90.0 ms, 2: 85.4, 3: 84.5, 4: 90.9
-  const int exp_poly = x3 ? 0 : (env_poly >= 0 ? env_poly : 3);
+  // 2 of every 8 exp2 pairs on the FMA pipe (degree-2 polynomial), the rest
+  // on MUFU: the kernel is MUFU-bound at d=64 (profiles/r01_summary.md).
+  // Round 1 measured 0: 90.0 ms, 2: 85.4, 3: 84.5, 4: 90.9; with the round-2
+  // pipeline (power-capped, two boxes, profiles/r02c/ab_exp_poly_*):
+  // 1: 85.9, 2: 81.2-82.4, 3: 84.2-86.4, 4: 88.8
+  const int exp_poly = x3 ? 0 : (env_poly >= 0 ? env_poly : 2);
   // Pack passes only where the kernel cannot read the caller's tensors:
   //  * Q (read row by row by the softmax warps) is used in place whenever it
   //    is bf16 with 16-byte aligned rows: the partitioned-order gather is the

@@ -150,7 +150,7 @@ struct Cfg {
   static_assert(B_COUNT * 8 + 100 <= 1024, "barrier region (+ item ring, TMEM address)");
   static_assert(CTAS_PER_SM * (SMEM_BYTES + 1024) <= 228 * 1024, "CTAs per SM vs shared memory");
   static_assert(TM_O + O_COLS <= (X3 ? TM_QL : TM_Q), "TMEM columns");
-  static_assert(!X3 || (WIDE && LSUM), "X3 runs in the stale-max launch with LSUM");
+  static_assert(!X3 || WIDE, "X3 runs in the stale-max launch (with LSUM: launch_pick)");
   static_assert(LEAD >= 1 && LEAD < NB, "S(j+LEAD) must only wait for a PV issued earlier");
 };
 using CfgMain = Cfg<BSA_TC_WIDE != 0>;
@@ -1082,7 +1082,7 @@ template <bool EXACT>
 static int launch_pick(const TcMaps& m, const AttnGeom& G, const TcArgs& a, int grid,
                        cudaStream_t st) {
   if (a.x3) {
-    if constexpr (EXACT) return fail(BSA_EINVAL, "X3 items are repaired by the SIMT kernel");
+    if constexpr (EXACT || !tc::LSUM) return fail(BSA_EINVAL, "X3 needs the stale-max launch with LSUM");
     else return launch_variant<0, false, false, true>(m, G, a, grid, st);
   }
   switch (a.exp_poly | (a.v_f16 ? 16 : 0)) {

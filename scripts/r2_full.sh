@@ -1,8 +1,8 @@
 # Round-2 full pass: quick check, GPU parity suite, smoke, driver-shaped bench
 # (20 steps), ragged/LPT bench lines, N=1000 leg, ncu launch list and --set
 # full captures of the attention and scoring kernels.
-mkdir -p gpurun_out/r2full
-O=gpurun_out/r2full
+O=${O:-gpurun_out/r2full}; mkdir -p $O
+
 timeout -s KILL 90 python scripts/quick_check.py > $O/quick.log 2>&1 || { echo "quick check failed" >> $O/quick.log; exit 1; }
 timeout -s KILL 1500 python -m pytest tests -m gpu -q --durations=10 2>&1 | tail -30 > $O/t_gpu.log
 timeout -s KILL 200 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
