@@ -129,6 +129,34 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
                      int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
                      void* ws, size_t ws_bytes, void* stream);
 
+/* predict_mask from pooled inputs: score -> select on (H,nq,d) / (H,nk,d)
+ * fp32 block means (e.g. from bsa_qkv_project_pooled's epilogue), the
+ * second half of maskpred.py:177-194.  Same masks, counts and probabilities
+ * as bsa_predict_mask on the tensors those means were pooled from.
+ * ws: bsa_predict_mask_pooled_workspace() bytes. */
+size_t bsa_predict_mask_pooled_workspace(int64_t heads, int64_t nq, int64_t nk, int64_t dim);
+int bsa_predict_mask_pooled(const float* q_pooled, const float* k_pooled, int64_t heads,
+                            int64_t nq, int64_t nk, int64_t dim, float scale, double tau,
+                            int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* The step before the path, fused (the reference has no
+ * model code, SPEC.md:8 -- the harness's QKV projection is the caller of
+ * predict_mask, maskpred.py:177, and sparse_attention, sparse.py:182).
+ * q/k/v (H,T,64) bf16 = x W^T + bias on the tensor cores (fp32 accumulate),
+ * x (T, C=H*64) bf16 with rows in partitioned order [special_rows | patches]
+ * (layout.py:113-138), W (3C, C) bf16 [Q | K | V] x C, bias (3C) bf16 or
+ * NULL.  Outputs are head-major in the same row order, the layout
+ * bsa_sparse_attention reads in place with inputs_permuted = 1.  The
+ * epilogue also writes q_pooled (H, ceil(Tp/128), 64) and k_pooled
+ * (H, ceil(Tp/64), 64) fp32 -- block_pool (maskpred.py:104-120) of the
+ * bf16 patch rows, bit-identical to bsa_block_pool -- unless NULL.
+ * C % 256 == 0, block_q 128 / block_k 64 (else BSA_EUNSUPPORTED). */
+int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const void* weight,
+                           const void* bias, int64_t heads, int64_t head_dim, int64_t special_rows,
+                           int32_t block_q, int32_t block_k, void* q, void* k, void* v,
+                           float* q_pooled, float* k_pooled, void* stream);
+
 /* Which scoring kernel predict_mask runs for nk key blocks of head_dim
  * dim: the fused score+softmax+select kernel's rows per CTA (8 or 4), or 0
  * for the three-kernel path (rows longer than shared memory holds, head_dim

@@ -81,6 +81,11 @@ def _declare(L):
         "bsa_predict_mask_workspace": ([i64, i64, i64, i32, i32], sz),
         "bsa_predict_mask": ([pt, pt, pl, i32, i32, f32, f64, i64, vp, vp, vp, vp, sz, vp],
                              ctypes.c_int),
+        "bsa_predict_mask_pooled_workspace": ([i64, i64, i64, i64], sz),
+        "bsa_predict_mask_pooled": ([vp, vp, i64, i64, i64, i64, f32, f64, i64, vp, vp, vp, vp, sz,
+                                     vp], ctypes.c_int),
+        "bsa_qkv_project_pooled": ([vp, i64, i64, vp, vp, i64, i64, i64, i32, i32, vp, vp, vp, vp,
+                                    vp, vp], ctypes.c_int),
         "bsa_sparse_attention_workspace": ([pl, i64, i64, i32, i32, i32, i32, i32], sz),
         "bsa_sparse_attention": ([pt, pt, pt, vp, i32, pl, i32, i32, vp, vp, f32, i32, i32, i32,
                                   i32, vp, sz, vp], ctypes.c_int),
@@ -122,6 +127,7 @@ def exported_symbols():
         "bsa_ipc_close", "bsa_ipc_free", "bsa_attention_stats_workspace",
         "bsa_attention_row_stats", "bsa_block_attention_map", "bsa_check_finite",
         "bsa_scoring_rows_per_cta", "bsa_debug_scoring_trace",
+        "bsa_predict_mask_pooled_workspace", "bsa_predict_mask_pooled", "bsa_qkv_project_pooled",
     ]
 
 

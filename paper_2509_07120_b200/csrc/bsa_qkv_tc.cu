@@ -1,0 +1,502 @@
+// bsa_qkv_tc.cu -- the step before the path, fused:
+// the QKV projection of a global-attention block as a tcgen05 GEMM whose
+// epilogue writes Q, K and V head-major in the partitioned token order the
+// attention kernel reads in place (no pack pass), and the block-pooled
+// patch Q / K the scorer needs (no pooling pass re-reading Q and K).
+//
+//   x   (T, C) bf16, rows in partitioned order [Ts special rows | Tp patch
+//       rows] (layout.py:113-138; the stack keeps its tokens in that order)
+//   W   (3C, C) bf16 (nn.Linear layout: [Q heads | K heads | V heads] x C)
+//   out q, k, v (H, T, 64) bf16 = x W^T + b, fp32 accumulation in TMEM
+//       q_pooled (H, nq, 64) fp32, k_pooled (H, nk, 64) fp32: block means of
+//       the bf16 patch rows of q / k (block_q 128 / block_k 64), summed in
+//       numpy's order -- x0 + pairwise(x1..x_{n-1}), then an IEEE divide --
+//       exactly as maskpred.py:104-120 (block_pool, np.add.reduceat) on the
+//       bf16 tensors upcast to fp32 (bit-identical to bsa_block_pool).
+//
+// Tiles: M = 128 rows aligned to the pooling blocks (ceil(Ts/128) special
+// tiles, then one tile per patch q-block), N = 256 features (four heads of
+// one of Q/K/V), K in 64-element chunks.  Persistent, one CTA per SM,
+// 192 threads:
+//   warp 0     TMA producer: A (128 x 64) and B (256 x 64) SW128 boxes into a
+//              3-stage ring
+//   warp 1     MMA issuer (elect.sync): 4 x tcgen05.mma M128 N256 K16 per
+//              chunk into one of two TMEM accumulators (2 x 256 columns), so
+//              the epilogue of tile i overlaps the MMAs of tile i+1
+//   warps 2-5  epilogue: TMEM -> +bias -> bf16 -> swizzled shared staging;
+//              accumulator released; then coalesced 16-byte stores of whole
+//              head tiles (128 rows x 128 B contiguous in (H, T, 64)), and
+//              for patch Q/K tiles the block pools from the staging copy.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "bsa_tc_common.cuh"
+
+namespace bsa {
+namespace qkv {
+
+using namespace tc;
+
+constexpr int BM = 128, BN = 256, BK = 64;
+#ifndef QKV_STAGES
+#define QKV_STAGES 3
+#endif
+#ifndef QKV_SH
+#define QKV_SH 2  // heads staged per epilogue pass
+#endif
+#ifndef QKV_EPI_GROUPS
+#define QKV_EPI_GROUPS 2  // epilogue warpgroups; group g drains accumulator g (tiles i % 2 == g)
+#endif
+#ifndef QKV_EXP
+#define QKV_EXP 0  // timing experiments only: 1 = epilogue drains TMEM and stores nothing
+#endif
+constexpr int STAGES = QKV_STAGES;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int HEADS_PER_TILE = BN / 64;
+constexpr int STG_HEAD = BM * 128;     // one head tile, bf16, 16 KB
+constexpr int OFF_STG = STAGES * STAGE_BYTES;
+constexpr int SH = QKV_SH;
+constexpr int NPASS = HEADS_PER_TILE / SH;
+static_assert(HEADS_PER_TILE % SH == 0, "staging passes");
+constexpr int EPI_GROUPS = QKV_EPI_GROUPS;
+static_assert(EPI_GROUPS == 1 || EPI_GROUPS == 2, "one or two epilogue warpgroups");
+constexpr int STG_GROUP = SH * STG_HEAD;
+constexpr int OFF_BAR = OFF_STG + EPI_GROUPS * STG_GROUP;
+constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + 1 KB alignment slack
+constexpr int THREADS = 64 + 128 * EPI_GROUPS;
+constexpr int EPI_WARP0 = 2;
+// barrier slots (8 bytes each)
+constexpr int B_FULL = 0, B_EMPTY = STAGES, B_TFULL = 2 * STAGES, B_TEMPTY = 2 * STAGES + 2;
+constexpr int B_TMEM = 2 * STAGES + 4;
+
+struct Args {
+  int64_t T, Ts, Tp, C, H;
+  int32_t nst, nq, nk, m_tiles, n_tiles;
+  const __nv_bfloat16* bias;  // (3C) or null
+  __nv_bfloat16* out[3];      // q, k, v: (H, T, 64)
+  float* pooled[2];           // q (H, nq, 64), k (H, nk, 64); null: skip
+};
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// staging: per head, 128 rows x 128 B, 16-byte chunk c of row r at chunk
+// position c ^ (r & 7) (the SW128 pattern: conflict-free row writes by the
+// row-owning threads and conflict-free column reads by the pooling threads)
+__device__ __forceinline__ uint32_t stg_off(int j, int r, int c16) {
+  return (uint32_t)(j * STG_HEAD + r * 128 + ((c16 ^ (r & 7)) << 4));
+}
+
+// two adjacent columns (bf16x2 at byte offset cb of the row's 16-byte chunk
+// group) of row r, upcast (exact)
+__device__ __forceinline__ float2 stg_ld2(const char* stg, int j, int r, int col2) {
+  const int c16 = col2 >> 2, w = col2 & 3;
+  const uint32_t v = *reinterpret_cast<const uint32_t*>(stg + stg_off(j, r, c16) + w * 4);
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
+}
+
+// block mean of rows first..first+n-1 (n >= 1, n <= 128) for the column pair
+// col2 of head j: (x0 + pairwise(x1..x_{n-1})) / n in numpy's order
+// (pw_leaf of bsa_score.cu, maskpred.py:117-120)
+__device__ __forceinline__ float2 pool_pair(const char* stg, int j, int first, int n, int col2) {
+  float2 s = stg_ld2(stg, j, first, col2);
+  const int m = n - 1, b = first + 1;
+  if (m > 0) {
+    float2 res;
+    if (m < 8) {
+      res = make_float2(0.0f, 0.0f);
+      for (int i = 0; i < m; ++i) {
+        const float2 v = stg_ld2(stg, j, b + i, col2);
+        res.x = __fadd_rn(res.x, v.x);
+        res.y = __fadd_rn(res.y, v.y);
+      }
+    } else {
+      float2 r[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r[q] = stg_ld2(stg, j, b + q, col2);
+      int i = 8;
+      const int stop = m - (m % 8);
+      for (; i < stop; i += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float2 v = stg_ld2(stg, j, b + i + q, col2);
+          r[q].x = __fadd_rn(r[q].x, v.x);
+          r[q].y = __fadd_rn(r[q].y, v.y);
+        }
+      }
+      res.x = __fadd_rn(__fadd_rn(__fadd_rn(r[0].x, r[1].x), __fadd_rn(r[2].x, r[3].x)),
+                        __fadd_rn(__fadd_rn(r[4].x, r[5].x), __fadd_rn(r[6].x, r[7].x)));
+      res.y = __fadd_rn(__fadd_rn(__fadd_rn(r[0].y, r[1].y), __fadd_rn(r[2].y, r[3].y)),
+                        __fadd_rn(__fadd_rn(r[4].y, r[5].y), __fadd_rn(r[6].y, r[7].y)));
+      for (; i < m; ++i) {
+        const float2 v = stg_ld2(stg, j, b + i, col2);
+        res.x = __fadd_rn(res.x, v.x);
+        res.y = __fadd_rn(res.y, v.y);
+      }
+    }
+    s.x = __fadd_rn(s.x, res.x);
+    s.y = __fadd_rn(s.y, res.y);
+  }
+  const float fn = (float)n;
+  return make_float2(__fdiv_rn(s.x, fn), __fdiv_rn(s.y, fn));
+}
+
+// pool_pair with the 8 accumulator chains split over a lane pair (sub 0:
+// chains 0-3, sub 1: chains 4-7); numpy's tree ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) joins the two halves with one shuffle, so the value is
+// pool_pair's bit for bit.  Both lanes return it.
+__device__ __forceinline__ float2 pool_pair_split(const char* stg, int j, int first, int n,
+                                                  int col2, int sub) {
+  const int m = n - 1, b = first + 1;
+  if (m < 8) return pool_pair(stg, j, first, n, col2);
+  float2 r[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = stg_ld2(stg, j, b + 4 * sub + q, col2);
+  int i = 8;
+  const int stop = m - (m % 8);
+  for (; i < stop; i += 8) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 v = stg_ld2(stg, j, b + i + 4 * sub + q, col2);
+      r[q].x = __fadd_rn(r[q].x, v.x);
+      r[q].y = __fadd_rn(r[q].y, v.y);
+    }
+  }
+  float2 half;
+  half.x = __fadd_rn(__fadd_rn(r[0].x, r[1].x), __fadd_rn(r[2].x, r[3].x));
+  half.y = __fadd_rn(__fadd_rn(r[0].y, r[1].y), __fadd_rn(r[2].y, r[3].y));
+  const float ox = __shfl_xor_sync(0xffffffffu, half.x, 1);
+  const float oy = __shfl_xor_sync(0xffffffffu, half.y, 1);
+  float2 res = make_float2(__fadd_rn(half.x, ox), __fadd_rn(half.y, oy));  // left + right
+  for (; i < m; ++i) {
+    const float2 v = stg_ld2(stg, j, b + i, col2);
+    res.x = __fadd_rn(res.x, v.x);
+    res.y = __fadd_rn(res.y, v.y);
+  }
+  const float2 x0 = stg_ld2(stg, j, first, col2);
+  const float fn = (float)n;
+  return make_float2(__fdiv_rn(__fadd_rn(x0.x, res.x), fn), __fdiv_rn(__fadd_rn(x0.y, res.y), fn));
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    qkv_pool_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const Args A) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char* smem = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  auto BAR = [&](int i) { return smem_u32(bars + i); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + B_TMEM);
+  char* stg = smem + OFF_STG;
+
+  const int32_t tiles = A.m_tiles * A.n_tiles;
+  const int kchunks = (int)(A.C / BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(BAR(B_FULL + s), 1);
+      mbar_init(BAR(B_EMPTY + s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(BAR(B_TFULL + b), 1);
+      mbar_init(BAR(B_TEMPTY + b), 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  // tile t: m = t / n_tiles (row tile), n = t % n_tiles (feature tile)
+  auto tile_row0 = [&](int32_t m) -> int32_t {
+    return m < A.nst ? m * BM : (int32_t)A.Ts + (m - A.nst) * BM;
+  };
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    uint32_t s = 0, ph = 0;
+    for (int32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int32_t m = t / A.n_tiles, n = t - m * A.n_tiles;
+      const int32_t row0 = tile_row0(m), f0 = n * BN;
+      for (int kc = 0; kc < kchunks; ++kc) {
+        mbar_wait(BAR(B_EMPTY + s), ph ^ 1);
+        if (elect_one()) {
+          const uint32_t dst = sbase + s * STAGE_BYTES;
+          mbar_expect_tx(BAR(B_FULL + s), STAGE_BYTES);
+          tma_load_2d(dst, &tm_a, BAR(B_FULL + s), kc * BK, row0);
+          tma_load_2d(dst + A_BYTES, &tm_b, BAR(B_FULL + s), kc * BK, f0);
+        }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    const uint32_t idesc = idesc_f16(BM, BN, 0, 1);
+    const uint64_t da0 = sdesc(sbase, 16, 1024), db0 = sdesc(sbase + A_BYTES, 16, 1024);
+    uint32_t s = 0, ph = 0, i = 0;
+    for (int32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const uint32_t ab = i & 1;
+      mbar_wait(BAR(B_TEMPTY + ab), ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dt = tmem + ab * BN;
+      for (int kc = 0; kc < kchunks; ++kc) {
+        mbar_wait(BAR(B_FULL + s), ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t so = (uint64_t)((s * STAGE_BYTES) >> 4);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_ss(dt, da0 + so + 2 * k, db0 + so + 2 * k, idesc, (kc | k) ? 1u : 0u);
+          tc_commit(BAR(B_EMPTY + s));
+          if (kc == kchunks - 1) tc_commit(BAR(B_TFULL + ab));
+        }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    // ============================== epilogue ==============================
+    const int quarter = warp & 3;               // TMEM lanes 32*quarter..+31
+    const int r = quarter * 32 + lane;          // tile row owned by this thread
+    const int grp = (warp - EPI_WARP0) >> 2;    // epilogue warpgroup
+    const int et = threadIdx.x - EPI_WARP0 * 32 - grp * 128;  // 0..127
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int64_t C = A.C;
+    stg += grp * STG_GROUP;
+    const uint32_t named_bar = 1 + grp;
+    uint32_t i = grp;
+    for (int32_t t = blockIdx.x + grp * gridDim.x; t < tiles; t += EPI_GROUPS * gridDim.x, i += EPI_GROUPS) {
+      const int32_t m = t / A.n_tiles, n = t - m * A.n_tiles;
+      const bool special = m < A.nst;
+      const int32_t row0 = tile_row0(m);
+      const int32_t rows = special ? min(BM, (int32_t)A.Ts - row0)
+                                   : min(BM, (int32_t)A.Tp - (m - A.nst) * BM);
+      const int32_t f0 = n * BN;
+      const int which = (int)(f0 / C);                  // 0 q, 1 k, 2 v
+      const int h0 = (int)((f0 - which * C) >> 6);      // first head of the tile
+      const uint32_t ab = i & 1;
+      mbar_wait(BAR(B_TFULL + ab), (i >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* const outp = which == 0 ? A.out[0] : which == 1 ? A.out[1] : A.out[2];
+      float* const poolp = which == 0 ? A.pooled[0] : which == 1 ? A.pooled[1] : nullptr;
+#pragma unroll 1
+      for (int pass = 0; pass < NPASS; ++pass) {
+#pragma unroll 1
+        for (int jj = 0; jj < SH; ++jj) {
+          const int j = pass * SH + jj;
+          uint32_t v[64];
+          const uint32_t ta = tmem + lane_off + ab * BN + j * 64;
+          tmem_ld32(ta, v);
+          tmem_ld32(ta + 32, v + 32);
+          tmem_wait_ld();
+          if (QKV_EXP == 1) continue;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float b8[8];
+            if (A.bias) {
+              const uint4 u = __ldg(reinterpret_cast<const uint4*>(A.bias + f0 + j * 64) + c);
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[q]));
+                b8[2 * q] = f.x;
+                b8[2 * q + 1] = f.y;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) b8[q] = 0.0f;
+            }
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              w[q] = pack_bf16(__fadd_rn(__uint_as_float(v[8 * c + 2 * q]), b8[2 * q]),
+                               __fadd_rn(__uint_as_float(v[8 * c + 2 * q + 1]), b8[2 * q + 1]));
+            *reinterpret_cast<uint4*>(stg + stg_off(jj, r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        if (pass == NPASS - 1) {
+          // accumulator drained: the MMA warp may start tile i + 2 in it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(BAR(B_TEMPTY + ab));
+        }
+        if (QKV_EXP == 1) continue;
+        asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");
+        // coalesced stores: head tile j is rows*128 contiguous bytes of out
+#pragma unroll 1
+        for (int jj = 0; jj < SH; ++jj) {
+          char* dst = reinterpret_cast<char*>(outp + ((int64_t)(h0 + pass * SH + jj) * A.T + row0) * 64);
+          const int nbytes = rows * 128;
+#pragma unroll 4
+          for (int o = et * 16; o < nbytes; o += 128 * 16) {
+            const int rr = o >> 7, c16 = (o >> 4) & 7;
+            *reinterpret_cast<uint4*>(dst + o) =
+                *reinterpret_cast<const uint4*>(stg + stg_off(jj, rr, c16));
+          }
+        }
+        // block pools of patch Q (one 128-row block) and patch K (two 64-row blocks)
+        if (!special && poolp) {
+          const int32_t b = m - A.nst;
+          if (which == 0) {
+            // SH heads x 32 column pairs, 128 / (SH * 32) lanes per item
+            static_assert(SH == 2 || SH == 4, "pool lane mapping");
+            if constexpr (SH == 2) {
+              const int item = et >> 1, sub = et & 1;
+              const int jj = item >> 5, col2 = item & 31;
+              const float2 p = pool_pair_split(stg, jj, 0, rows, col2, sub);
+              if (sub == 0)
+                *reinterpret_cast<float2*>(poolp + ((int64_t)(h0 + pass * SH + jj) * A.nq + b) * 64 +
+                                           2 * col2) = p;
+            } else {
+              const int jj = et >> 5, col2 = et & 31;
+              const float2 p = pool_pair(stg, jj, 0, rows, col2);
+              *reinterpret_cast<float2*>(poolp + ((int64_t)(h0 + pass * SH + jj) * A.nq + b) * 64 +
+                                         2 * col2) = p;
+            }
+          } else {
+            // SH heads x 32 column pairs x 2 key blocks over 128 lanes
+            for (int it2 = et; it2 < SH * 64; it2 += 128) {
+              const int kb = it2 / (SH * 32), rem = it2 % (SH * 32);
+              const int jj = rem >> 5, col2 = rem & 31;
+              const int first = kb * 64, nrow = min(64, rows - first);
+              if (nrow <= 0) continue;
+              const float2 p = pool_pair(stg, jj, first, nrow, col2);
+              *reinterpret_cast<float2*>(poolp + ((int64_t)(h0 + pass * SH + jj) * A.nk + 2 * b + kb) * 64 +
+                                         2 * col2) = p;
+            }
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");  // staging free for the next pass
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D (cols, rows) map of a row-major bf16 matrix, box (64, box_rows), SW128
+static int make_map_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols,
+                       int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BSA_OK;
+}
+
+}  // namespace qkv
+}  // namespace bsa
+
+using namespace bsa;
+
+extern "C" {
+
+int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const void* weight,
+                           const void* bias, int64_t heads, int64_t head_dim, int64_t special_rows,
+                           int32_t block_q, int32_t block_k, void* q, void* k, void* v,
+                           float* q_pooled, float* k_pooled, void* stream) {
+  using namespace bsa::qkv;
+  if (!x || !weight || !q || !k || !v) return fail(BSA_EINVAL, "qkv_project: null pointer");
+  if (head_dim != 64)
+    return fail(BSA_EUNSUPPORTED, "qkv_project: head_dim must be 64, got %lld", (long long)head_dim);
+  if (heads < 1 || dim_in != heads * head_dim)
+    return fail(BSA_EINVAL, "qkv_project: dim_in %lld != heads %lld x head_dim 64",
+                (long long)dim_in, (long long)heads);
+  if (dim_in % BN != 0)
+    return fail(BSA_EUNSUPPORTED, "qkv_project: heads*head_dim must be a multiple of 256, got %lld",
+                (long long)dim_in);
+  if (block_q != BM || block_k != 64)
+    return fail(BSA_EUNSUPPORTED, "qkv_project: pooling needs block_q 128 / block_k 64, got %d/%d",
+                block_q, block_k);
+  if (tokens < 1 || special_rows < 0 || special_rows > tokens)
+    return fail(BSA_EINVAL, "qkv_project: bad token counts (%lld tokens, %lld special rows)",
+                (long long)tokens, (long long)special_rows);
+  if (tokens >= ((int64_t)1 << 31)) return fail(BSA_EUNSUPPORTED, "qkv_project: T >= 2^31");
+  for (const void* p : {x, weight, (const void*)q, (const void*)k, (const void*)v})
+    if ((uintptr_t)p % 16) return fail(BSA_EINVAL, "qkv_project: pointers must be 16-byte aligned");
+  if (bias && (uintptr_t)bias % 16) return fail(BSA_EINVAL, "qkv_project: bias must be 16-byte aligned");
+  Args a;
+  a.T = tokens;
+  a.Ts = special_rows;
+  a.Tp = tokens - special_rows;
+  a.C = dim_in;
+  a.H = heads;
+  a.nst = (int32_t)ceil_div(special_rows, (int64_t)BM);
+  a.nq = (int32_t)ceil_div(a.Tp, (int64_t)BM);
+  a.nk = (int32_t)ceil_div(a.Tp, (int64_t)64);
+  a.m_tiles = a.nst + a.nq;
+  a.n_tiles = (int32_t)(3 * dim_in / BN);
+  a.bias = (const __nv_bfloat16*)bias;
+  a.out[0] = (__nv_bfloat16*)q;
+  a.out[1] = (__nv_bfloat16*)k;
+  a.out[2] = (__nv_bfloat16*)v;
+  a.pooled[0] = q_pooled;
+  a.pooled[1] = k_pooled;
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
+  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, BN);
+  if (rc) return rc;
+  int dev = 0, sms = 0;
+  BSA_CUDA_TRY(cudaGetDevice(&dev));
+  BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    SMEM_BYTES));
+  qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, a);
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
+}  // extern "C"

@@ -1494,6 +1494,45 @@ static int launch_softsel(float* src, int64_t ld, int64_t rows, int64_t nk, doub
 
 using namespace bsa;
 
+// scores + softmax + selection from pooled Q / K (the fused kernel when the
+// rows fit shared memory, else the three-kernel path).  z: (H, nq, nk) fp32
+// scratch; w: selection workspace followed by the blocked-K buffer.
+static int score_select(const float* qp, const float* kp, int64_t H, int64_t nq, int64_t nk,
+                        int64_t d, float scale, double tau, int64_t k_floor, uint8_t* mask_bits,
+                        int32_t* counts, float* probs_out, float* z, char* w, cudaStream_t st) {
+  int rc = BSA_OK;
+  if (fs_rows_per_cta(nk, d) > 0) {
+    // fused: scores, softmax and selection in one kernel (bsa_scoresel.cu);
+    // z only receives the probability rows of rows handed to the fallback
+    char* sw = w;
+    float* kb = (float*)(w + align_up(select_ws_bytes(H * nq, nk), 256));
+    int32_t* fb_count = (int32_t*)sw;
+    sw += 256;
+    sw += align_up((size_t)plan_ints_for(nk) * 4, 256);
+    int32_t* fb_list = (int32_t*)sw;
+    sw += align_up((size_t)(H * nq) * 4, 256);
+    unsigned long long* scratch = (unsigned long long*)sw;
+    BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
+    rc = launch_scoresel(qp, kp, H, nq, nk, d, scale, tau, k_floor, kb, mask_bits, counts,
+                         probs_out, z, fb_list, fb_count, st);
+    if (rc == FS_NO_CLUSTER) goto three_kernels;
+    if (rc) return rc;
+    const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
+    BSA_CUDA_TRY(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)std::max<size_t>(fsmem, 16)));
+    fallback_kernel<<<FB_GRID, SS_THREADS, std::max<size_t>(fsmem, 16), st>>>(
+        z, nk, nk, tau, k_floor, mask_bits, counts, fb_list, fb_count, scratch, next_pow2(nk));
+    BSA_LAUNCH_CHECK();
+    return BSA_OK;
+  }
+three_kernels:
+  rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
+  if (!rc)
+    rc = launch_softsel<true, true>(z, nk, H * nq, nk, tau, k_floor, probs_out, mask_bits, counts,
+                                    w, st);
+  return rc;
+}
+
 extern "C" {
 
 int bsa_block_pool(const bsa_tensor* x, const bsa_layout* patch_gather, int32_t block,
@@ -1572,6 +1611,12 @@ size_t bsa_predict_mask_workspace(int64_t heads, int64_t patch_tokens, int64_t d
          align_up(fs_kblock_bytes(heads, nk, dim), 256);
 }
 
+size_t bsa_predict_mask_pooled_workspace(int64_t heads, int64_t nq, int64_t nk, int64_t dim) {
+  if (heads < 1 || nq < 1 || nk < 1 || dim < 1) return 0;
+  return align_up((size_t)(heads * nq * nk) * 4, 256) + align_up(select_ws_bytes(heads * nq, nk), 256) +
+         align_up(fs_kblock_bytes(heads, nk, dim), 256);
+}
+
 int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout* patch_gather,
                      int32_t block_q, int32_t block_k, float scale, double tau,
                      int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
@@ -1605,36 +1650,30 @@ int bsa_predict_mask(const bsa_tensor* q, const bsa_tensor* k, const bsa_layout*
   rc = launch_pool(q, patch_gather, block_q, qp, st, &n1);
   if (!rc) rc = launch_pool(k, patch_gather, block_k, kp, st, &n2);
   if (rc) return rc;
-  if (fs_rows_per_cta(nk, d) > 0) {
-    // fused: scores, softmax and selection in one kernel (bsa_scoresel.cu);
-    // z only receives the probability rows of rows handed to the fallback
-    char* sw = w;
-    float* kb = (float*)(w + align_up(select_ws_bytes(H * nq, nk), 256));
-    int32_t* fb_count = (int32_t*)sw;
-    sw += 256;
-    sw += align_up((size_t)plan_ints_for(nk) * 4, 256);
-    int32_t* fb_list = (int32_t*)sw;
-    sw += align_up((size_t)(H * nq) * 4, 256);
-    unsigned long long* scratch = (unsigned long long*)sw;
-    BSA_CUDA_TRY(cudaMemsetAsync(fb_count, 0, 4, st));
-    rc = launch_scoresel(qp, kp, H, nq, nk, d, scale, tau, k_floor, kb, mask_bits, counts,
-                         probs_out, z, fb_list, fb_count, st);
-    if (rc == FS_NO_CLUSTER) goto three_kernels;
-    if (rc) return rc;
-    const size_t fsmem = align_up((size_t)ceil_div(nk, 32) * 4, 16);
-    BSA_CUDA_TRY(cudaFuncSetAttribute(fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)std::max<size_t>(fsmem, 16)));
-    fallback_kernel<<<FB_GRID, SS_THREADS, std::max<size_t>(fsmem, 16), st>>>(
-        z, nk, nk, tau, k_floor, mask_bits, counts, fb_list, fb_count, scratch, next_pow2(nk));
-    BSA_LAUNCH_CHECK();
-    return BSA_OK;
-  }
-three_kernels:
-  rc = launch_scores(qp, kp, H, nq, nk, d, scale, z, nk, st);
-  if (!rc)
-    rc = launch_softsel<true, true>(z, nk, H * nq, nk, tau, k_floor, probs_out, mask_bits, counts,
-                                    w, st);
-  return rc;
+  return score_select(qp, kp, H, nq, nk, d, scale, tau, k_floor, mask_bits, counts, probs_out, z,
+                      w, st);
+}
+
+int bsa_predict_mask_pooled(const float* q_pooled, const float* k_pooled, int64_t heads,
+                            int64_t nq, int64_t nk, int64_t dim, float scale, double tau,
+                            int64_t k_floor, uint8_t* mask_bits, int32_t* counts, float* probs_out,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (!q_pooled || !k_pooled || !mask_bits || !counts || !ws)
+    return fail(BSA_EINVAL, "predict_mask_pooled: null pointer");
+  if (heads < 1 || nq < 1 || nk < 1 || dim < 1)
+    return fail(BSA_EINVAL, "predict_mask_pooled: bad shape (%lld, %lld, %lld, %lld)",
+                (long long)heads, (long long)nq, (long long)nk, (long long)dim);
+  if (!(tau >= 0.0 && tau <= 1.0)) return fail(BSA_EINVAL, "tau must be in [0, 1], got %g", tau);
+  if (k_floor < 1 || k_floor > nk)
+    return fail(BSA_EINVAL, "k_floor must be in [1, %lld], got %lld", (long long)nk,
+                (long long)k_floor);
+  if (ws_bytes < bsa_predict_mask_pooled_workspace(heads, nq, nk, dim))
+    return fail(BSA_EINVAL, "predict_mask_pooled: workspace too small");
+  char* w = (char*)ws;
+  float* z = (float*)w;
+  w += align_up((size_t)(heads * nq * nk) * 4, 256);
+  return score_select(q_pooled, k_pooled, heads, nq, nk, dim, scale, tau, k_floor, mask_bits,
+                      counts, probs_out, z, w, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -316,6 +316,44 @@ def predict_mask(q_patches, k_patches, policy: MaskPolicy, *, layout: TokenLayou
     return mask
 
 
+def predict_mask_pooled(q_pooled, k_pooled, policy: MaskPolicy, *, return_probs: bool = False,
+                        validate: bool = True):
+    """predict_mask from block means already pooled (maskpred.py:177-194
+    minus its two block_pool calls): (heads, nq, d) / (heads, nk, d) fp32,
+    e.g. the QKV-projection epilogue's (qkv.qkv_projection).  Same mask and
+    probabilities as predict_mask on the tensors they were pooled from."""
+    qp, _ = _to_device(q_pooled, "q_pooled", allow_bf16=False, validate=validate)
+    kp, _ = _to_device(k_pooled, "k_pooled", allow_bf16=False, validate=validate)
+    if kp.device != qp.device:
+        raise ValueError(f"q_pooled on {qp.device} but k_pooled on {kp.device}")
+    if qp.dim() != 3 or kp.dim() != 3:
+        raise ValueError(f"pooled tensors must be 3-D, got {tuple(qp.shape)} and {tuple(kp.shape)}")
+    g = policy.geometry
+    if qp.shape[1] != g.nq_blocks or kp.shape[1] != g.nk_blocks:
+        raise ValueError(f"pooled shapes {tuple(qp.shape)} / {tuple(kp.shape)} inconsistent with "
+                         f"geometry ({g.nq_blocks}, {g.nk_blocks})")
+    if qp.shape[0] != kp.shape[0] or qp.shape[2] != kp.shape[2]:
+        raise ValueError(f"pooled shapes incompatible: {tuple(qp.shape)} vs {tuple(kp.shape)}")
+    qp, kp = qp.contiguous(), kp.contiguous()
+    h, nq, d = qp.shape
+    nk = kp.shape[1]
+    L = N.lib()
+    bits = torch.empty((h * nq, -(-nk // 8)), dtype=torch.uint8, device=qp.device)
+    counts = torch.empty(h * nq, dtype=torch.int32, device=qp.device)
+    probs = torch.empty((h, nq, nk), dtype=torch.float32, device=qp.device) if return_probs else None
+    ws = N.workspace(L.bsa_predict_mask_pooled_workspace(h, nq, nk, d), qp.device)
+    scale = np.float32(1.0 / float(np.sqrt(d)))
+    with N.on_device(qp.device):
+        N.check(L.bsa_predict_mask_pooled(qp.data_ptr(), kp.data_ptr(), h, nq, nk, d, float(scale),
+                                          float(policy.tau), policy.min_blocks, bits.data_ptr(),
+                                          counts.data_ptr(), N.ptr(probs), ws.data_ptr(),
+                                          ws.numel(), N.stream_ptr()), "predict_mask_pooled")
+    mask = BlockMask._from_device(bits, counts, h, g)
+    if return_probs:
+        return mask, probs
+    return mask
+
+
 def full_mask(geometry: BlockGeometry, heads: int) -> BlockMask:
     """All-selected mask (sparsity zero)."""
     return BlockMask(np.ones((heads, geometry.nq_blocks, geometry.nk_blocks), dtype=bool), geometry)

@@ -23,8 +23,9 @@ import torch
 import torch.nn.functional as F
 
 from .dense import AttentionInputs
-from .layout import BlockGeometry, TokenLayout
-from .maskpred import MaskPolicy, predict_mask
+from .layout import BlockGeometry, TokenLayout, partition_permutation
+from .maskpred import MaskPolicy, predict_mask, predict_mask_pooled
+from .qkv import qkv_projection
 from .sparse import SparseAttentionJob, sparse_attention
 
 
@@ -87,8 +88,10 @@ class GlobalAttentionStack:
                 mode: str = "sparse") -> torch.Tensor:
         if x.shape != (layout.total_tokens, self.dim):
             raise ValueError(f"x must be ({layout.total_tokens}, {self.dim}), got {tuple(x.shape)}")
-        if mode == "sparse" and policy is None:
-            raise ValueError("sparse mode needs a MaskPolicy")
+        if mode in ("sparse", "fused") and policy is None:
+            raise ValueError(f"{mode} mode needs a MaskPolicy")
+        if mode == "fused":
+            return self._forward_fused(x, layout, policy)
         for blk in self.blocks:
             x = x + self.attention(x, blk, layout, policy, mode)
             if blk.mlp is not None:
@@ -98,6 +101,40 @@ class GlobalAttentionStack:
         return x
 
     __call__ = forward
+
+    def attention_fused(self, xp: torch.Tensor, blk: BlockWeights, layout: TokenLayout,
+                        policy: MaskPolicy) -> torch.Tensor:
+        """One block's attention branch with tokens in partitioned order
+        [specials | patches]: LayerNorm, then the tensor-core QKV projection
+        whose epilogue writes head-major Q/K/V plus the pooled patch Q/K
+        (qkv.qkv_projection), predict_mask_pooled (no pooling pass), the
+        block-sparse kernel on the in-place permuted inputs (no pack pass),
+        and the output projection.  Same mask as mode="sparse" on the same
+        Q/K; Q/K/V themselves come from this GEMM instead of cuBLAS."""
+        T, C = xp.shape
+        h = F.layer_norm(xp, (C,), blk.ln_w, blk.ln_b)
+        q, k, v, qp, kp = qkv_projection(h, blk.qkv_w, blk.qkv_b, self.heads, layout,
+                                         policy.geometry)
+        mask = predict_mask_pooled(qp, kp, policy, validate=False)
+        o = sparse_attention(SparseAttentionJob(AttentionInputs(q, k, v, validate=False), layout,
+                                                mask), inputs_permuted=True)
+        o = o.permute(1, 0, 2).reshape(T, C)
+        return F.linear(o, blk.proj_w, blk.proj_b)
+
+    def _forward_fused(self, x: torch.Tensor, layout: TokenLayout, policy: MaskPolicy):
+        # every op but attention acts per token: keep the residual stream in
+        # partitioned order for the whole stack, permute once each way
+        perm, inv = partition_permutation(layout)
+        perm_t = torch.from_numpy(perm).to(x.device)
+        inv_t = torch.from_numpy(inv).to(x.device)
+        xp = x.index_select(0, perm_t)
+        for blk in self.blocks:
+            xp = xp + self.attention_fused(xp, blk, layout, policy)
+            if blk.mlp is not None:
+                lw, lb, w1, b1, w2, b2 = blk.mlp
+                h = F.layer_norm(xp, (self.dim,), lw, lb)
+                xp = xp + F.linear(F.gelu(F.linear(h, w1, b1)), w2, b2)
+        return xp.index_select(0, inv_t)
 
     def forward_sharded(self, x_local: torch.Tensor, layout: TokenLayout, policy: MaskPolicy, *,
                         group=None, comm_group=None, combine: str = "auto",

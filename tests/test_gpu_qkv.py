@@ -1,0 +1,170 @@
+"""The fused QKV projection: tcgen05 GEMM whose
+epilogue writes head-major partitioned Q/K/V and the pooled patch Q/K.
+
+Bars:
+* Q/K/V: the fp32-accumulated product rounded once to bf16: every element
+  within half a bf16 ulp of x W^T + b (float64, same bf16 inputs) plus the
+  fp32 accumulation error 2^-21 |x||W|^T (cancellation); and > 99.9% of the
+  elements equal to cuBLAS's F.linear on the same inputs;
+* pooled Q/K: bit-identical to block_pool of the bf16 patch rows (the
+  device pool kernel, itself bit-exact with the reference) and to the
+  oracle's numpy block_pool (maskpred.py:104-120) on small cases;
+* predict_mask_pooled: mask bits, counts and probabilities identical to
+  predict_mask on the Q/K the means were pooled from.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bsa():
+    import paper_2509_07120_b200 as m
+    return m
+
+
+def _inputs(F, P, S, H, seed, bias=True):
+    import torch
+    from paper_2509_07120_b200 import TokenLayout
+    lay = TokenLayout(F, P, S)
+    C = H * 64
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.randn((lay.total_tokens, C), generator=g).to("cuda", torch.bfloat16)
+    w = (torch.randn((3 * C, C), generator=g) / np.sqrt(C)).to("cuda", torch.bfloat16)
+    b = (0.1 * torch.randn((3 * C,), generator=g)).to("cuda", torch.bfloat16) if bias else None
+    return lay, x, w, b
+
+
+def _ref_qkv(x, w, b, H):
+    xd, wd = x.double(), w.double()
+    y = xd @ wd.T
+    if b is not None:
+        y = y + b.double()
+    T = x.shape[0]
+    return y.view(T, 3, H, 64).permute(1, 2, 0, 3)  # (3, H, T, 64) float64
+
+
+CASES = [
+    # frames, patches, specials, heads: ragged last q/k blocks, partial special tile
+    (3, 300, 5, 4),
+    (2, 1369, 5, 4),     # VGGT frame size (blocks straddle frames)
+    (4, 1369, 5, 16),    # headline head count, C = 1024
+    (1, 70, 0, 4),       # no special rows, one ragged q-block
+    (1, 129, 200, 4),    # more special rows than patches; 1-row last q-block
+]
+
+
+@pytest.mark.parametrize("F,P,S,H", CASES)
+def test_qkv_projection_values_and_pools(bsa, F, P, S, H):
+    import torch
+    lay, x, w, b = _inputs(F, P, S, H, seed=F * 7 + P + S + H)
+    q, k, v, qp, kp = bsa.qkv_projection(x, w, b, H, lay)
+    torch.cuda.synchronize()
+    ref = _ref_qkv(x, w, b, H)
+    # |x| |W|^T: the scale of the fp32 accumulation error (cancellation cases)
+    mag = _ref_qkv(x.abs(), w.abs(), None, H)
+    T = lay.total_tokens
+    cub = torch.nn.functional.linear(x, w, b).view(T, 3, H, 64).permute(1, 2, 0, 3)
+    for i, (name, got) in enumerate((("q", q), ("k", k), ("v", v))):
+        r = ref[i]
+        err = (got.double() - r).abs()
+        bound = r.abs() * 2.0 ** -8 + mag[i] * 2.0 ** -21  # final bf16 rounding + fp32 sums
+        assert bool((err <= bound).all()), (
+            f"{name}: {int((err > bound).sum())} elements beyond the bound, max err {err.max().item()}")
+        same = (got == cub[i]).double().mean().item()
+        assert same > 0.999, f"{name}: only {same:.5f} of elements equal cuBLAS's"
+    Ts = lay.special_tokens
+    g = bsa.geometry_for(lay)
+    assert torch.equal(qp, bsa.block_pool(q[:, Ts:], 128)), "pooled Q differs from block_pool"
+    assert torch.equal(kp, bsa.block_pool(k[:, Ts:], 64)), "pooled K differs from block_pool"
+    assert qp.shape == (H, g.nq_blocks, 64) and kp.shape == (H, g.nk_blocks, 64)
+
+
+def test_pools_match_oracle_numpy(bsa):
+    import oracle
+    lay, x, w, b = _inputs(3, 300, 5, 4, seed=11)
+    q, k, _, qp, kp = bsa.qkv_projection(x, w, b, 4, lay)
+    Ts = lay.special_tokens
+    qn = q[:, Ts:].float().cpu().numpy()
+    kn = k[:, Ts:].float().cpu().numpy()
+    np.testing.assert_array_equal(qp.cpu().numpy(), oracle.block_pool(qn, 128))
+    np.testing.assert_array_equal(kp.cpu().numpy(), oracle.block_pool(kn, 64))
+
+
+@pytest.mark.parametrize("tau,rho", [(0.4, 0.8), (0.0, 0.75), (0.9, 0.5)])
+def test_predict_mask_pooled_equals_predict_mask(bsa, tau, rho):
+    import torch
+    lay, x, w, b = _inputs(4, 1369, 5, 16, seed=3)
+    q, k, _, qp, kp = bsa.qkv_projection(x, w, b, 16, lay)
+    g = bsa.geometry_for(lay)
+    pol = bsa.MaskPolicy(tau, rho, g)
+    m1, p1 = bsa.predict_mask_pooled(qp, kp, pol, return_probs=True)
+    Ts = lay.special_tokens  # q/k rows are in partitioned order: patches follow the specials
+    m2, p2 = bsa.predict_mask(q[:, Ts:], k[:, Ts:], pol, return_probs=True)
+    assert torch.equal(m1.device_bits(), m2.device_bits())
+    assert torch.equal(m1.device_counts(), m2.device_counts())
+    assert torch.equal(p1, p2)
+
+
+def test_fused_layer_equals_composition(bsa):
+    """The stack's fused attention branch is exactly qkv_projection ->
+    predict_mask (on the full interleaved Q/K) -> sparse_attention."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2509_07120_b200.stack import GlobalAttentionStack, policy_for
+    lay = bsa.TokenLayout(3, 1369, 5)
+    st = GlobalAttentionStack(layers=1, heads=16, seed=5)
+    pol = policy_for(lay, 0.0, 0.75)
+    perm, _ = bsa.partition_permutation(lay)
+    x = torch.randn((lay.total_tokens, 1024), generator=torch.Generator().manual_seed(1)).to(
+        "cuda", torch.bfloat16)
+    xp = x[torch.from_numpy(perm).cuda()]
+    blk = st.blocks[0]
+    got = st.attention_fused(xp, blk, lay, pol)
+    h = F.layer_norm(xp, (1024,), blk.ln_w, blk.ln_b)
+    q, k, v, _, _ = bsa.qkv_projection(h, blk.qkv_w, blk.qkv_b, 16, lay, pooled=False)
+    Ts = lay.special_tokens
+    mask = bsa.predict_mask(q[:, Ts:], k[:, Ts:], pol)
+    o = bsa.sparse_attention(bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask),
+                             inputs_permuted=True)
+    want = F.linear(o.permute(1, 0, 2).reshape(lay.total_tokens, 1024), blk.proj_w, blk.proj_b)
+    assert torch.equal(got, want)
+
+
+def test_fused_stack_close_to_sparse_stack(bsa):
+    """mode="fused" (own GEMM, pooled epilogue, permuted residual stream) vs
+    mode="sparse" (cuBLAS projection, interleaved order): the projections
+    round differently in the last bf16 bit, so the bar is the bf16 attention
+    tolerance on the block output, not bit equality."""
+    import torch
+    from paper_2509_07120_b200.stack import GlobalAttentionStack, policy_for
+    lay = bsa.TokenLayout(4, 1369, 5)
+    st = GlobalAttentionStack(layers=2, heads=16, seed=2, mlp=True)
+    pol = policy_for(lay, 0.0, 0.75)
+    x = torch.randn((lay.total_tokens, 1024), generator=torch.Generator().manual_seed(4)).to(
+        "cuda", torch.bfloat16)
+    a = st.forward(x, lay, pol, mode="fused").float()
+    r = st.forward(x, lay, pol, mode="sparse").float()
+    rel = ((a - r).norm() / r.norm()).item()
+    assert rel < 2e-2, rel
+
+
+def test_qkv_projection_rejects_bad_inputs(bsa):
+    import torch
+    lay, x, w, b = _inputs(1, 70, 0, 4, seed=0)
+    with pytest.raises(ValueError):
+        bsa.qkv_projection(x.float(), w, b, 4, lay)
+    with pytest.raises(ValueError):
+        bsa.qkv_projection(x, w[:-1], b, 4, lay)
+    with pytest.raises(ValueError):
+        bsa.qkv_projection(x, w, b, 2, lay)
+    with pytest.raises(ValueError):
+        bsa.qkv_projection(x[:-1], w, b, 4, lay)
+    with pytest.raises(ValueError):  # geometry other than 128/64
+        bsa.qkv_projection(x, w, b, 4, lay, bsa.BlockGeometry(lay.patch_tokens, 64, 64))
+    with pytest.raises(ValueError):
+        bsa.predict_mask_pooled(torch.zeros(4, 3, 64, device="cuda"),
+                                torch.zeros(4, 2, 64, device="cuda"),
+                                bsa.MaskPolicy(0.0, 0.5, bsa.geometry_for(lay)))
