@@ -49,6 +49,9 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef QKV_EPI_GROUPS
 #define QKV_EPI_GROUPS 2  // epilogue warpgroups; group g drains accumulator g (tiles i % 2 == g)
 #endif
+#ifndef QKV_TMA_STORE
+#define QKV_TMA_STORE 1  // head tiles leave the staging buffer by TMA bulk tensor stores
+#endif
 #ifndef QKV_EXP
 #define QKV_EXP 0  // timing experiments only: 1 = epilogue drains TMEM and stores nothing
 #endif
@@ -65,7 +68,8 @@ static_assert(HEADS_PER_TILE % SH == 0, "staging passes");
 constexpr int EPI_GROUPS = QKV_EPI_GROUPS;
 static_assert(EPI_GROUPS == 1 || EPI_GROUPS == 2, "one or two epilogue warpgroups");
 constexpr int STG_GROUP = SH * STG_HEAD;
-constexpr int OFF_BAR = OFF_STG + EPI_GROUPS * STG_GROUP;
+constexpr int OFF_BIAS = OFF_STG + EPI_GROUPS * STG_GROUP;  // per group: the tile's BN biases, fp32
+constexpr int OFF_BAR = OFF_BIAS + EPI_GROUPS * BN * 4;
 constexpr int SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + 1 KB alignment slack
 constexpr int THREADS = 64 + 128 * EPI_GROUPS;
 constexpr int EPI_WARP0 = 2;
@@ -190,6 +194,8 @@ __device__ __forceinline__ float2 pool_pair_split(const char* stg, int j, int fi
 
 __global__ void __launch_bounds__(THREADS, 1)
     qkv_pool_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v,
                     const Args A) {
   extern __shared__ __align__(1024) char smem_raw[];
   char* smem = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -286,6 +292,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int64_t C = A.C;
     stg += grp * STG_GROUP;
+    float* const sbias = reinterpret_cast<float*>(smem + OFF_BIAS) + grp * BN;
     const uint32_t named_bar = 1 + grp;
     uint32_t i = grp;
     for (int32_t t = blockIdx.x + grp * gridDim.x; t < tiles; t += EPI_GROUPS * gridDim.x, i += EPI_GROUPS) {
@@ -298,6 +305,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int which = (int)(f0 / C);                  // 0 q, 1 k, 2 v
       const int h0 = (int)((f0 - which * C) >> 6);      // first head of the tile
       const uint32_t ab = i & 1;
+      // the tile's biases into shared memory (fp32) while its MMAs run
+      if (et < BN / 2) {
+        const uint32_t bb = A.bias ? __ldg(reinterpret_cast<const uint32_t*>(A.bias + f0) + et) : 0u;
+        reinterpret_cast<float2*>(sbias)[et] =
+            __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb));
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");
       mbar_wait(BAR(B_TFULL + ab), (i >> 1) & 1);
       tc_fence_after();
       __nv_bfloat16* const outp = which == 0 ? A.out[0] : which == 1 ? A.out[1] : A.out[2];
@@ -316,18 +330,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             float b8[8];
-            if (A.bias) {
-              const uint4 u = __ldg(reinterpret_cast<const uint4*>(A.bias + f0 + j * 64) + c);
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[q]));
-                b8[2 * q] = f.x;
-                b8[2 * q + 1] = f.y;
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < 8; ++q) b8[q] = 0.0f;
+            {
+              const float4 lo = reinterpret_cast<const float4*>(sbias + j * 64 + c * 8)[0];
+              const float4 hi = reinterpret_cast<const float4*>(sbias + j * 64 + c * 8)[1];
+              b8[0] = lo.x; b8[1] = lo.y; b8[2] = lo.z; b8[3] = lo.w;
+              b8[4] = hi.x; b8[5] = hi.y; b8[6] = hi.z; b8[7] = hi.w;
             }
             uint32_t w[4];
 #pragma unroll
@@ -344,17 +351,37 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (lane == 0) mbar_arrive(BAR(B_TEMPTY + ab));
         }
         if (QKV_EXP == 1) continue;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging -> bulk-store proxy
         asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");
-        // coalesced stores: head tile j is rows*128 contiguous bytes of out
+        // head tile j is rows*128 contiguous bytes of out.  Whole tiles (and
+        // the last patch tile, whose extra rows fall past T and are clipped)
+        // go out as one TMA bulk tensor store per head, straight from the
+        // staging layout (it is the SW128 box layout); a partial special
+        // tile, whose extra rows belong to the first patch tile, is stored
+        // row by row.
+        const bool tma_store = QKV_TMA_STORE && (rows == BM || !special);
+        if (tma_store) {
+          if (et == 0) {
+            const CUtensorMap* om = which == 0 ? &tm_q : which == 1 ? &tm_k : &tm_v;
 #pragma unroll 1
-        for (int jj = 0; jj < SH; ++jj) {
-          char* dst = reinterpret_cast<char*>(outp + ((int64_t)(h0 + pass * SH + jj) * A.T + row0) * 64);
-          const int nbytes = rows * 128;
+            for (int jj = 0; jj < SH; ++jj)
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(om),
+                  "r"(smem_u32(stg + jj * STG_HEAD)), "r"(0), "r"(row0), "r"(h0 + pass * SH + jj)
+                  : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else {
+#pragma unroll 1
+          for (int jj = 0; jj < SH; ++jj) {
+            char* dst = reinterpret_cast<char*>(outp + ((int64_t)(h0 + pass * SH + jj) * A.T + row0) * 64);
+            const int nbytes = rows * 128;
 #pragma unroll 4
-          for (int o = et * 16; o < nbytes; o += 128 * 16) {
-            const int rr = o >> 7, c16 = (o >> 4) & 7;
-            *reinterpret_cast<uint4*>(dst + o) =
-                *reinterpret_cast<const uint4*>(stg + stg_off(jj, rr, c16));
+            for (int o = et * 16; o < nbytes; o += 128 * 16) {
+              const int rr = o >> 7, c16 = (o >> 4) & 7;
+              *reinterpret_cast<uint4*>(dst + o) =
+                  *reinterpret_cast<const uint4*>(stg + stg_off(jj, rr, c16));
+            }
           }
         }
         // block pools of patch Q (one 128-row block) and patch K (two 64-row blocks)
@@ -389,7 +416,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");  // staging free for the next pass
+        // staging free for the next pass once the bulk stores have read it
+        if (tma_store && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(named_bar) : "memory");
       }
     }
   }
@@ -432,6 +461,21 @@ static int make_map_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BSA_OK;
+}
+
+// 3-D (64, T, H) map of a (H, T, 64) bf16 output, box (64, 128, 1), SW128
+static int make_map_out(CUtensorMap* map, void* base, int64_t H, int64_t T) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {64, (cuuint64_t)T, (cuuint64_t)H};
+  cuuint64_t strides[2] = {128, (cuuint64_t)T * 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BSA_ECUDA, "cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
   return BSA_OK;
 }
 
@@ -483,9 +527,10 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
   a.out[2] = (__nv_bfloat16*)v;
   a.pooled[0] = q_pooled;
   a.pooled[1] = k_pooled;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mo[3];
   int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
   if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, BN);
+  for (int i = 0; i < 3 && !rc; ++i) rc = make_map_out(&mo[i], a.out[i], heads, tokens);
   if (rc) return rc;
   int dev = 0, sms = 0;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
@@ -494,7 +539,7 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     SMEM_BYTES));
-  qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, a);
+  qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1], mo[2], a);
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }

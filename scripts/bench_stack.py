@@ -20,6 +20,8 @@ ap.add_argument("--rho", type=float, default=0.75)
 ap.add_argument("--specials", type=int, default=5)
 ap.add_argument("--dense", action="store_true", help="also time the dense (cuDNN SDPA) stack")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--fused", action="store_true",
+                help="also time mode='fused' (own QKV GEMM with pooled epilogue, no pool/pack passes)")
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -48,6 +50,11 @@ res = {"config": "24-layer VGGT global-attention stack (random init), block-spar
        "frames": a.frames, "tokens": lay.total_tokens, "layers": a.layers, "tau": a.tau,
        "rho": a.rho, "ms_per_forward": ms_sparse, "ms_per_layer": ms_sparse / a.layers,
        "frames_per_s": a.frames / (ms_sparse * 1e-3), "finite": bool(torch.isfinite(ys).all())}
+if a.fused:
+    ms_fused, yf = timed("fused")
+    res.update({"fused_ms_per_forward": ms_fused, "fused_ms_per_layer": ms_fused / a.layers,
+                "fused_frames_per_s": a.frames / (ms_fused * 1e-3),
+                "fused_vs_sparse_rel_diff": float((yf.float() - ys.float()).norm() / ys.float().norm())})
 if a.dense:
     ms_dense, yd = timed("dense")
     res.update({"dense_ms_per_forward": ms_dense, "dense_ms_per_layer": ms_dense / a.layers,

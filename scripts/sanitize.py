@@ -91,6 +91,16 @@ def main():
     bm = analysis.block_attention_map(inp, lay, rs)
     ok &= bool(torch.isfinite(rs).all()) and bool(torch.isfinite(bm).all())
     print("stats kernels: finite", bool(torch.isfinite(bm).all()), flush=True)
+    # fused QKV projection (tcgen05 GEMM + pooled epilogue) and scoring from the pools
+    C = 4 * 64
+    x = torch.randn((lay.total_tokens, C), device="cuda").to(torch.bfloat16)
+    w = (torch.randn((3 * C, C), device="cuda") / 16).to(torch.bfloat16)
+    b = torch.randn((3 * C,), device="cuda").to(torch.bfloat16)
+    q4, k4, v4, qp4, kp4 = bsa.qkv_projection(x, w, b, 4, lay)
+    m4 = bsa.predict_mask_pooled(qp4, kp4, bsa.MaskPolicy(0.4, 0.8, g))
+    ok &= bool(torch.isfinite(qp4).all()) and bool(torch.isfinite(v4.float()).all())
+    print(f"qkv_projection + predict_mask_pooled: {int(m4.device_counts().sum().item())} blocks",
+          flush=True)
     torch.cuda.synchronize()
     print("SANITIZE_DRIVER_OK" if ok else "SANITIZE_DRIVER_BAD", flush=True)
     return 0 if ok else 1
