@@ -52,10 +52,14 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #ifndef QKV_TMA_STORE
 #define QKV_TMA_STORE 1  // head tiles leave the staging buffer by TMA bulk tensor stores
 #endif
+#ifndef QKV_PAIR
+#define QKV_PAIR 1  // CTA pairs (clusters of 2) on row tiles 2p, 2p+1 of one feature tile share B by TMA multicast
+#endif
 #ifndef QKV_EXP
 #define QKV_EXP 0  // timing experiments only: 1 = epilogue drains TMEM and stores nothing
 #endif
 constexpr int STAGES = QKV_STAGES;
+constexpr int PAIR = QKV_PAIR;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -92,6 +96,27 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// multicast: the box lands at the same shared offset in every CTA of
+// cta_mask and completes bytes on the mbarrier at the same offset in each
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar), "h"(cta_mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 
 // staging: per head, 128 rows x 128 B, 16-byte chunk c of row r at chunk
@@ -212,7 +237,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(BAR(B_FULL + s), 1);
-      mbar_init(BAR(B_EMPTY + s), 1);
+      mbar_init(BAR(B_EMPTY + s), PAIR ? 2 : 1);  // pair: both CTAs' MMAs read the multicast B half
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(BAR(B_TFULL + b), 1);
@@ -232,19 +257,35 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer's multicasts and commits target initialised barriers
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  // tile t: m = t / n_tiles (row tile), n = t % n_tiles (feature tile)
+  // work units: unit u is row tile m = u / n_tiles, feature tile n = u % n_tiles;
+  // pair mode: unit u is row tiles 2(u / n_tiles) + {0, 1} (one per CTA of the
+  // pair, a CTA whose row tile is past the end computes a zero tile and stores
+  // nothing) with one feature tile
+  uint32_t crank = 0;
+  if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int32_t U = PAIR ? ((A.m_tiles + 1) / 2) * A.n_tiles : tiles;
+  const int32_t u0 = PAIR ? (int32_t)(blockIdx.x >> 1) : (int32_t)blockIdx.x;
+  const int32_t ustride = PAIR ? (int32_t)(gridDim.x >> 1) : (int32_t)gridDim.x;
+  auto decode = [&](int32_t u, int32_t& m, int32_t& n) {
+    const int32_t mu = u / A.n_tiles;
+    n = u - mu * A.n_tiles;
+    m = PAIR ? 2 * mu + (int32_t)crank : mu;
+  };
   auto tile_row0 = [&](int32_t m) -> int32_t {
+    if (m >= A.m_tiles) return (int32_t)A.T;  // TMA zero-fills rows past the end
     return m < A.nst ? m * BM : (int32_t)A.Ts + (m - A.nst) * BM;
   };
 
   if (warp == 0) {
     // ============================ TMA producer ============================
     uint32_t s = 0, ph = 0;
-    for (int32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int32_t m = t / A.n_tiles, n = t - m * A.n_tiles;
+    for (int32_t u = u0; u < U; u += ustride) {
+      int32_t m, n;
+      decode(u, m, n);
       const int32_t row0 = tile_row0(m), f0 = n * BN;
       for (int kc = 0; kc < kchunks; ++kc) {
         mbar_wait(BAR(B_EMPTY + s), ph ^ 1);
@@ -252,7 +293,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t dst = sbase + s * STAGE_BYTES;
           mbar_expect_tx(BAR(B_FULL + s), STAGE_BYTES);
           tma_load_2d(dst, &tm_a, BAR(B_FULL + s), kc * BK, row0);
-          tma_load_2d(dst + A_BYTES, &tm_b, BAR(B_FULL + s), kc * BK, f0);
+          if constexpr (PAIR) {
+            // this CTA's half of B (128 feature rows) into both CTAs' stage s
+            const uint32_t half = crank * (B_BYTES / 2);
+            tma_load_2d_mc(dst + A_BYTES + half, &tm_b, BAR(B_FULL + s), kc * BK,
+                           f0 + (int)crank * (BN / 2), (uint16_t)0x3);
+          } else {
+            tma_load_2d(dst + A_BYTES, &tm_b, BAR(B_FULL + s), kc * BK, f0);
+          }
         }
         __syncwarp();
         if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -263,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t idesc = idesc_f16(BM, BN, 0, 1);
     const uint64_t da0 = sdesc(sbase, 16, 1024), db0 = sdesc(sbase + A_BYTES, 16, 1024);
     uint32_t s = 0, ph = 0, i = 0;
-    for (int32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    for (int32_t u = u0; u < U; u += ustride, ++i) {
       const uint32_t ab = i & 1;
       mbar_wait(BAR(B_TEMPTY + ab), ((i >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -276,7 +324,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             mma_ss(dt, da0 + so + 2 * k, db0 + so + 2 * k, idesc, (kc | k) ? 1u : 0u);
-          tc_commit(BAR(B_EMPTY + s));
+          if constexpr (PAIR) tc_commit_mc(BAR(B_EMPTY + s), (uint16_t)0x3);  // frees s in both CTAs
+          else tc_commit(BAR(B_EMPTY + s));
           if (kc == kchunks - 1) tc_commit(BAR(B_TFULL + ab));
         }
         __syncwarp();
@@ -295,12 +344,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* const sbias = reinterpret_cast<float*>(smem + OFF_BIAS) + grp * BN;
     const uint32_t named_bar = 1 + grp;
     uint32_t i = grp;
-    for (int32_t t = blockIdx.x + grp * gridDim.x; t < tiles; t += EPI_GROUPS * gridDim.x, i += EPI_GROUPS) {
-      const int32_t m = t / A.n_tiles, n = t - m * A.n_tiles;
+    for (int32_t u = u0 + grp * ustride; u < U; u += EPI_GROUPS * ustride, i += EPI_GROUPS) {
+      int32_t m, n;
+      decode(u, m, n);
       const bool special = m < A.nst;
       const int32_t row0 = tile_row0(m);
-      const int32_t rows = special ? min(BM, (int32_t)A.Ts - row0)
-                                   : min(BM, (int32_t)A.Tp - (m - A.nst) * BM);
+      const int32_t rows = m >= A.m_tiles ? 0
+                           : special     ? min(BM, (int32_t)A.Ts - row0)
+                                         : min(BM, (int32_t)A.Tp - (m - A.nst) * BM);
       const int32_t f0 = n * BN;
       const int which = (int)(f0 / C);                  // 0 q, 1 k, 2 v
       const int h0 = (int)((f0 - which * C) >> 6);      // first head of the tile
@@ -359,7 +410,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // staging layout (it is the SW128 box layout); a partial special
         // tile, whose extra rows belong to the first patch tile, is stored
         // row by row.
-        const bool tma_store = QKV_TMA_STORE && (rows == BM || !special);
+        const bool tma_store = QKV_TMA_STORE && rows > 0 && (rows == BM || !special);
         if (tma_store) {
           if (et == 0) {
             const CUtensorMap* om = which == 0 ? &tm_q : which == 1 ? &tm_k : &tm_v;
@@ -385,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
         // block pools of patch Q (one 128-row block) and patch K (two 64-row blocks)
-        if (!special && poolp) {
+        if (!special && poolp && rows > 0) {
           const int32_t b = m - A.nst;
           if (which == 0) {
             // SH heads x 32 column pairs, 128 / (SH * 32) lanes per item
@@ -424,6 +475,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -529,17 +581,45 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
   a.pooled[1] = k_pooled;
   CUtensorMap ma, mb, mo[3];
   int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
-  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, BN);
+  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, PAIR ? BN / 2 : BN);
   for (int i = 0; i < 3 && !rc; ++i) rc = make_map_out(&mo[i], a.out[i], heads, tokens);
   if (rc) return rc;
   int dev = 0, sms = 0;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     SMEM_BYTES));
-  qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1], mo[2], a);
+  if (PAIR) {
+    // persistent pairs: as many as the GPU co-schedules (a GPC with an odd
+    // SM count leaves one SM out), never more, or the surplus would run as a
+    // second wave behind the static tile split
+    static int max_pairs = -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (max_pairs < 0) {
+      cfg.gridDim = dim3(2 * (sms / 2));
+      int n = 0;
+      BSA_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, qkv_pool_kernel, &cfg));
+      max_pairs = std::max(1, n);
+    }
+    grid = 2 * (unsigned)std::min<int64_t>((int64_t)((a.m_tiles + 1) / 2) * a.n_tiles, max_pairs);
+    cfg.gridDim = dim3(grid);
+    BSA_CUDA_TRY(cudaLaunchKernelEx(&cfg, qkv_pool_kernel, ma, mb, mo[0], mo[1], mo[2], a));
+  } else {
+    qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1], mo[2], a);
+  }
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }

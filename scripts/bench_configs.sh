@@ -16,4 +16,4 @@ for rho in 0.5 0.75 0.9; do
   timeout -s KILL 900 python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-dense --frames 1000 --rho $rho > gpurun_out/configs/c5_n1000_rho$rho.json 2>&1
 done
 # config 3: 24-layer stack at N=200, sparse vs dense
-timeout -s KILL 900 python scripts/bench_stack.py --frames 200 --dense --reps 1 > gpurun_out/configs/c3_stack_n200.json 2>&1
+timeout -s KILL 900 python scripts/bench_stack.py --frames 200 --dense --fused --reps 1 > gpurun_out/configs/c3_stack_n200.json 2>&1
