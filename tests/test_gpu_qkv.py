@@ -82,6 +82,27 @@ def test_qkv_projection_values_and_pools(bsa, F, P, S, H):
     assert qp.shape == (H, g.nq_blocks, 64) and kp.shape == (H, g.nk_blocks, 64)
 
 
+def test_full_size_n200_pools_and_mask(bsa):
+    """The config-3 layer shape (N=200, 16 heads, T=274,800), no bias: pools
+    bit-identical to block_pool of the outputs, mask identical to
+    predict_mask's, and Q/K/V equal to cuBLAS's projection (same rounding)."""
+    import torch
+    lay, x, w, _ = _inputs(200, 1369, 5, 16, seed=200, bias=False)
+    q, k, v, qp, kp = bsa.qkv_projection(x, w, None, 16, lay)
+    Ts = lay.special_tokens
+    assert torch.equal(qp, bsa.block_pool(q[:, Ts:], 128, validate=False))
+    assert torch.equal(kp, bsa.block_pool(k[:, Ts:], 64, validate=False))
+    pol = bsa.MaskPolicy(0.0, 0.75, bsa.geometry_for(lay))
+    m1 = bsa.predict_mask_pooled(qp, kp, pol)
+    m2 = bsa.predict_mask(q[:, Ts:], k[:, Ts:], pol, validate=False)
+    assert torch.equal(m1.device_bits(), m2.device_bits())
+    T = lay.total_tokens
+    cub = torch.nn.functional.linear(x, w).view(T, 3, 16, 64).permute(1, 2, 0, 3)
+    for i, got in enumerate((q, k, v)):
+        same = (got == cub[i]).double().mean().item()
+        assert same > 0.999, same
+
+
 def test_pools_match_oracle_numpy(bsa):
     import oracle
     lay, x, w, b = _inputs(3, 300, 5, 4, seed=11)
