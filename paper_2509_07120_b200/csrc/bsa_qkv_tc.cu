@@ -53,13 +53,13 @@ constexpr int BM = 128, BN = 256, BK = 64;
 #define QKV_TMA_STORE 1  // head tiles leave the staging buffer by TMA bulk tensor stores
 #endif
 #ifndef QKV_PAIR
-#define QKV_PAIR 1  // CTA pairs (clusters of 2) on row tiles 2p, 2p+1 of one feature tile share B by TMA multicast
+#define QKV_PAIR 1  // CTA pairs (clusters of 2) on row tiles 2p, 2p+1 of one feature tile share B by TMA
+                    // multicast; 0 forces single CTAs (also the fallback when pairs cannot be co-scheduled)
 #endif
 #ifndef QKV_EXP
 #define QKV_EXP 0  // timing experiments only: 1 = epilogue drains TMEM and stores nothing
 #endif
 constexpr int STAGES = QKV_STAGES;
-constexpr int PAIR = QKV_PAIR;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -217,6 +217,7 @@ __device__ __forceinline__ float2 pool_pair_split(const char* stg, int j, int fi
   return make_float2(__fdiv_rn(__fadd_rn(x0.x, res.x), fn), __fdiv_rn(__fadd_rn(x0.y, res.y), fn));
 }
 
+template <bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     qkv_pool_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -579,46 +580,56 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
   a.out[2] = (__nv_bfloat16*)v;
   a.pooled[0] = q_pooled;
   a.pooled[1] = k_pooled;
-  CUtensorMap ma, mb, mo[3];
-  int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
-  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, PAIR ? BN / 2 : BN);
-  for (int i = 0; i < 3 && !rc; ++i) rc = make_map_out(&mo[i], a.out[i], heads, tokens);
-  if (rc) return rc;
   int dev = 0, sms = 0;
   BSA_CUDA_TRY(cudaGetDevice(&dev));
   BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
-  unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-  BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    SMEM_BYTES));
-  if (PAIR) {
-    // persistent pairs: as many as the GPU co-schedules (a GPC with an odd
-    // SM count leaves one SM out), never more, or the surplus would run as a
-    // second wave behind the static tile split
-    static int max_pairs = -1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(THREADS);
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
-    cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (max_pairs < 0) {
-      cfg.gridDim = dim3(2 * (sms / 2));
-      int n = 0;
-      BSA_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, qkv_pool_kernel, &cfg));
-      max_pairs = std::max(1, n);
+  // persistent CTA pairs: as many as the GPU co-schedules (a GPC with an odd
+  // SM count leaves one SM out), never more, or the surplus would run as a
+  // second wave behind the static tile split; none co-schedulable (or
+  // QKV_PAIR=0): single CTAs
+  static int max_pairs[64];
+  static bool queried[64];
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int slot = dev & 63;
+  if (!queried[slot]) {
+    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    int n = 0;
+    cfg.gridDim = dim3(2 * std::max(1, sms / 2));
+    if (QKV_PAIR && cudaOccupancyMaxActiveClusters(&n, qkv_pool_kernel<true>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
     }
-    grid = 2 * (unsigned)std::min<int64_t>((int64_t)((a.m_tiles + 1) / 2) * a.n_tiles, max_pairs);
-    cfg.gridDim = dim3(grid);
-    BSA_CUDA_TRY(cudaLaunchKernelEx(&cfg, qkv_pool_kernel, ma, mb, mo[0], mo[1], mo[2], a));
+    max_pairs[slot] = QKV_PAIR ? n : 0;
+    queried[slot] = true;
+  }
+  const bool pair = max_pairs[slot] > 0;
+  CUtensorMap ma, mb, mo[3];
+  int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
+  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, pair ? BN / 2 : BN);
+  for (int i = 0; i < 3 && !rc; ++i) rc = make_map_out(&mo[i], a.out[i], heads, tokens);
+  if (rc) return rc;
+  const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
+  if (pair) {
+    const int64_t units = (int64_t)((a.m_tiles + 1) / 2) * a.n_tiles;
+    cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(units, max_pairs[slot]));
+    BSA_CUDA_TRY(cudaLaunchKernelEx(&cfg, qkv_pool_kernel<true>, ma, mb, mo[0], mo[1], mo[2], a));
   } else {
-    qkv_pool_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1], mo[2], a);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    qkv_pool_kernel<false><<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1],
+                                                                               mo[2], a);
   }
   BSA_LAUNCH_CHECK();
   return BSA_OK;
