@@ -48,6 +48,9 @@ namespace tc {
 #define BSA_TC_EXPERIMENT 0  // timing experiments only: 1 = no exps, 2 = no MMAs, 3 = no
                              // exp-argument FFMA2, 4 = no poly clamp
 #endif
+#ifndef BSA_TC_L2HINT
+#define BSA_TC_L2HINT 0  // K/V TMA loads evict_last; Q loads and output stores streaming
+#endif
 #ifndef BSA_TC_WIDE
 #define BSA_TC_WIDE 1
 #endif
@@ -357,6 +360,7 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
     // mask bytes per step: popc + warp scan) into a shared-memory queue, so
     // the per-tile cost is one queue read, one barrier wait and one TMA.
     const bool is_k = warp == C::PRODUCER_WARP;
+    const uint64_t l2_keep = BSA_TC_L2HINT ? l2_policy_evict_last() : 0;
     // the queue through its shared-window address (LDS / STS): the generic
     // pointer (smem is realigned at run time) compiles to generic LD / ST,
     // slower on this per-tile path
@@ -448,8 +452,12 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
           mbar_wait(BAR((C::MERGED ? C::B_SFULL : C::B_KEMPTY) + st), ((gx / NK) & 1) ^ 1);
           if (elect_one()) {
             mbar_expect_tx(BAR(C::B_KFULL + st), C::K_STAGE);
-            tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0, s0,
-                        I.h);
+            if constexpr (BSA_TC_L2HINT != 0)
+              tma_load_3d_hint(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0,
+                               s0, I.h, l2_keep);
+            else
+              tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE, &tm_k, BAR(C::B_KFULL + st), 0, s0,
+                          I.h);
             if constexpr (X3)
               tma_load_3d(sbase + C::OFF_K + st * C::K_STAGE + CHUNK_BYTES, &tm_kl,
                           BAR(C::B_KFULL + st), 0, s0, I.h);
@@ -460,8 +468,12 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
           mbar_wait(BAR((C::MERGED ? C::B_PFREE : C::B_VEMPTY) + st), ((gx / NV) & 1) ^ 1);
           if (elect_one()) {
             mbar_expect_tx(BAR(C::B_VFULL + st), X3 ? 2 * CHUNK_BYTES : CHUNK_BYTES);
-            tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0,
-                        I.h);
+            if constexpr (BSA_TC_L2HINT != 0)
+              tma_load_3d_hint(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0,
+                               s0, I.h, l2_keep);
+            else
+              tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE, &tm_v, BAR(C::B_VFULL + st), 0, s0,
+                          I.h);
             if constexpr (X3)
               tma_load_3d(sbase + C::OFF_V + st * C::V_STAGE + C::V_LO, &tm_vl,
                           BAR(C::B_VFULL + st), 0, s0, I.h);
@@ -721,7 +733,8 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
           if (pr < (int32_t)G.T) {
             const uint4* src = reinterpret_cast<const uint4*>(
                 A.qp + (int64_t)I.h * A.q_sH + qrow * A.q_sT + c * 16);
-            const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+            const uint4 v0 = BSA_TC_L2HINT ? __ldcs(src) : __ldg(src);
+            const uint4 v1 = BSA_TC_L2HINT ? __ldcs(src + 1) : __ldg(src + 1);
             qr[0] = v0.x; qr[1] = v0.y; qr[2] = v0.z; qr[3] = v0.w;
             qr[4] = v1.x; qr[5] = v1.y; qr[6] = v1.z; qr[7] = v1.w;
           } else {
@@ -972,7 +985,8 @@ __global__ void __maxnreg__((max_regs_of<BSA_TC_WIDE != 0 && !EXACT, X3>()))
               v.y = pack_bf16(__uint_as_float(orr[8 * q + 2]) * inv, __uint_as_float(orr[8 * q + 3]) * inv);
               v.z = pack_bf16(__uint_as_float(orr[8 * q + 4]) * inv, __uint_as_float(orr[8 * q + 5]) * inv);
               v.w = pack_bf16(__uint_as_float(orr[8 * q + 6]) * inv, __uint_as_float(orr[8 * q + 7]) * inv);
-              op[q] = v;
+              if (BSA_TC_L2HINT) __stcs(op + q, v);
+              else op[q] = v;
             }
           } else {
             float4* op = reinterpret_cast<float4*>(orow_f32 + col0);
