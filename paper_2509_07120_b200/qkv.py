@@ -34,7 +34,7 @@ def qkv_projection(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | N
     the same row order, the pooled tensors (heads, nq, 64) / (heads, nk, 64)
     fp32 (None when ``pooled=False``).  Needs head_dim 64, C % 256 == 0 and
     the 128/64 block geometry (ValueError otherwise)."""
-    dev = N.require_cuda()
+    N.require_cuda()  # a GPU and libbsa.so, or a loud error (no CPU path)
     if not isinstance(x, torch.Tensor) or x.device.type != "cuda":
         raise ValueError("x must be a CUDA tensor")
     if x.dim() != 2 or x.dtype != torch.bfloat16:
@@ -64,7 +64,6 @@ def qkv_projection(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | N
     if pooled:
         qp = torch.empty((H, g.nq_blocks, 64), dtype=torch.float32, device=x.device)
         kp = torch.empty((H, g.nk_blocks, 64), dtype=torch.float32, device=x.device)
-    del dev
     with N.on_device(x.device):
         N.check(N.lib().bsa_qkv_project_pooled(
             x.data_ptr(), T, C, weight.data_ptr(), N.ptr(bias), H, 64, layout.special_tokens,
