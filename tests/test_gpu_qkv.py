@@ -129,6 +129,25 @@ def test_predict_mask_pooled_equals_predict_mask(bsa, tau, rho):
     assert torch.equal(p1, p2)
 
 
+def test_predict_mask_pooled_long_rows(bsa):
+    """Long rows (N=500: 10,695 key blocks) run the one-row-per-CTA shape of
+    the fused scoring kernel (16-CTA clusters); from the pools as well."""
+    import torch
+    lay = bsa.TokenLayout(500, 1369, 5)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k = (torch.randn((2, lay.total_tokens, 64), generator=g, device="cuda").to(torch.bfloat16)
+            for _ in range(2))
+    geo = bsa.geometry_for(lay)
+    pol = bsa.MaskPolicy(0.4, 0.8, geo)
+    pidx = torch.from_numpy(bsa.patch_token_indices(lay)).cuda()
+    qp = bsa.block_pool(q[:, pidx].contiguous(), 128, validate=False)
+    kp = bsa.block_pool(k[:, pidx].contiguous(), 64, validate=False)
+    m1 = bsa.predict_mask_pooled(qp, kp, pol)
+    m2 = bsa.predict_mask(q, k, pol, layout=lay)
+    assert torch.equal(m1.device_bits(), m2.device_bits())
+    assert torch.equal(m1.device_counts(), m2.device_counts())
+
+
 def test_fused_layer_equals_composition(bsa):
     """The stack's fused attention branch is exactly qkv_projection ->
     predict_mask (on the full interleaved Q/K) -> sparse_attention."""
