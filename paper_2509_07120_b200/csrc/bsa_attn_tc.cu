@@ -182,9 +182,48 @@ __device__ __forceinline__ constexpr bool poly_pair(int e) {
   }
 }
 
+#ifndef BSA_TC_H2
+#define BSA_TC_H2 0  // (F16P) FMA-pipe exponentials in packed fp16 (HFMA2 polynomial)
+#endif
+// 2^x for a packed fp16 pair on the FMA pipe in half precision: clamp at
+// -15.4 (so j >= -15), j = rint(x) by the 1551 = 1.5*2^10 + 15 magic (the
+// rounded sum's low mantissa bits are j + 15), f = x - j in [-0.5, 0.5],
+// p(f) the degree-2 minimax polynomial (HFMA2), times 2^j built from the
+// exponent field j + 15 (0 for j = -15: exactly zero below 2^-14.5; 31 for
+// j = 16: inf, an overflow the caller's row sum flags).
+__device__ __forceinline__ uint32_t exp2_poly_h2(uint32_t xh) {
+  __half2 x = *reinterpret_cast<__half2*>(&xh);
+  x = __hmax2(x, __float2half2_rn(-15.4f));
+  const __half2 t = __hadd2(x, __float2half2_rn(1551.0f));
+  const __half2 j = __hsub2(t, __float2half2_rn(1551.0f));
+  const __half2 f = __hsub2(x, j);
+  __half2 p = __hfma2(__float2half2_rn(0.23842570f), f, __float2half2_rn(0.70344281f));
+  p = __hfma2(p, f, __float2half2_rn(1.00044298f));
+  const uint32_t tb = *reinterpret_cast<const uint32_t*>(&t);
+  const uint32_t eb = (tb << 10) & 0x7C007C00u;
+  const __half2 e = *reinterpret_cast<const __half2*>(&eb);
+  const __half2 r = __hmul2(p, e);
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+
 template <int POLY, bool F16P, bool SUM = true>
 __device__ __forceinline__ float exp_half(const float (&s)[32], float sl2, float m,
                                           uint32_t p_taddr) {
+  if constexpr (F16P && BSA_TC_H2 != 0 && !SUM) {
+    // argument in fp32 (f32x2 FMA), rounded once to fp16; P = 2^x in fp16
+    const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
+    uint32_t r[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const float2 x = __ffma2_rn(make_float2(s[2 * e], s[2 * e + 1]), sl2v, nmv);
+      // MUFU pairs: two f32 MUFU.EX2 (ex2.approx.f16x2 is two MUFU ops plus a
+      // repack), packed to fp16; polynomial pairs: in fp16 on the FMA pipe
+      if (poly_pair<POLY>(e)) r[e] = exp2_poly_h2(cvt_h2(x.x, x.y));
+      else r[e] = cvt_h2(ex2(x.x), ex2(x.y));
+    }
+    tmem_st16(p_taddr, r);
+    return 0.0f;
+  }
   const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-m, -m);
   float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                   make_float2(0.f, 0.f)};
@@ -1108,6 +1147,11 @@ static int launch_pick(const TcMaps& m, const AttnGeom& G, const TcArgs& a, int 
     case 16: return launch_variant<0, true, EXACT>(m, G, a, grid, st);
     case 18: return launch_variant<2, true, EXACT>(m, G, a, grid, st);
     case 19: return launch_variant<3, true, EXACT>(m, G, a, grid, st);
+#if BSA_TC_H2
+    case 20: return launch_variant<4, true, EXACT>(m, G, a, grid, st);
+    case 21: return launch_variant<5, true, EXACT>(m, G, a, grid, st);
+    case 22: return launch_variant<6, true, EXACT>(m, G, a, grid, st);
+#endif
     default: return fail(BSA_EINVAL, "unknown tensor-core kernel variant");
   }
 }
