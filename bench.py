@@ -388,7 +388,13 @@ def run_ours(a):
         scoring = {"bound": "hbm", "ms": sc_ms, "bytes": sc_bytes,
                    "achieved_gbs": sc_bytes / (sc_ms * 1e-3) / 1e9, "peak_gbs": hbm,
                    "frac": sc_bytes / (sc_ms * 1e-3) / 1e9 / hbm,
-                   "fma": fma, "fma_frac": fma / (sc_ms * 1e-3) / fma_peak}
+                   "fma": fma, "fma_frac": fma / (sc_ms * 1e-3) / fma_peak,
+                   # measured (profiles/r02d/README.md): bit-exact scoring is
+                   # sequential fp32 fmaf chains (OpenBLAS order) plus numpy's
+                   # exp per key block, not a byte stream: phase A is bounded
+                   # by the shared-memory port feeding the FMA pipe, phase B by
+                   # instruction issue (~120 per row x key block)
+                   "limiter": "smem port (exact fp32 FMA chains) + issue (numpy exp, select)"}
 
     # dense baseline on the same GPU: library SDPA (cuDNN / flash) in bf16
     dense_ms = None
