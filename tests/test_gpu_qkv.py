@@ -103,6 +103,23 @@ def test_full_size_n200_pools_and_mask(bsa):
         assert same > 0.999, same
 
 
+def test_config5_size_n1000(bsa):
+    """N=1000 frames (T=1,374,000; x is 2.8 GB, Q/K/V 8.4 GB): 64-bit
+    offsets throughout; pools bit-identical to block_pool; values equal to
+    cuBLAS's on a sample of rows spread over the whole sequence."""
+    import torch
+    lay, x, w, b = _inputs(1000, 1369, 5, 16, seed=1000)
+    q, k, v, qp, kp = bsa.qkv_projection(x, w, b, 16, lay)
+    Ts = lay.special_tokens
+    assert torch.equal(qp, bsa.block_pool(q[:, Ts:], 128, validate=False))
+    assert torch.equal(kp, bsa.block_pool(k[:, Ts:], 64, validate=False))
+    rows = torch.linspace(0, lay.total_tokens - 1, 4096, device="cuda").long()
+    cub = torch.nn.functional.linear(x[rows], w, b).view(-1, 3, 16, 64).permute(1, 2, 0, 3)
+    for i, got in enumerate((q, k, v)):
+        same = (got[:, rows] == cub[i]).double().mean().item()
+        assert same > 0.999, same
+
+
 def test_pools_match_oracle_numpy(bsa):
     import oracle
     lay, x, w, b = _inputs(3, 300, 5, 4, seed=11)
