@@ -157,6 +157,16 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
                            int32_t block_q, int32_t block_k, void* q, void* k, void* v,
                            float* q_pooled, float* k_pooled, void* stream);
 
+/* The step after the path, fused (the harness's caller side of
+ * sparse_attention, sparse.py:182): out (T, C) = residual + o W^T + bias, o
+ * the attention output (H, T, 64) bf16 head-major as bsa_sparse_attention
+ * writes it -- read in place as the GEMM's A operand, no transpose --,
+ * W (C, C) bf16, residual and out (T, C) bf16 (out may alias residual),
+ * bias (C) bf16 or NULL; fp32 accumulation, one rounding to bf16.
+ * C = H*64, C % 256 == 0 (else BSA_EUNSUPPORTED). */
+int bsa_proj_residual(const void* o, int64_t heads, int64_t tokens, const void* weight,
+                      const void* bias, const void* residual, void* out, void* stream);
+
 /* Which scoring kernel predict_mask runs for nk key blocks of head_dim
  * dim: the fused score+softmax+select kernel's rows per CTA (8 or 4), or 0
  * for the three-kernel path (rows longer than shared memory holds, head_dim

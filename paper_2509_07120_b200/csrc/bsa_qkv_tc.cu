@@ -79,7 +79,8 @@ constexpr int THREADS = 64 + 128 * EPI_GROUPS;
 constexpr int EPI_WARP0 = 2;
 // barrier slots (8 bytes each)
 constexpr int B_FULL = 0, B_EMPTY = STAGES, B_TFULL = 2 * STAGES, B_TEMPTY = 2 * STAGES + 2;
-constexpr int B_TMEM = 2 * STAGES + 4;
+constexpr int B_RES = 2 * STAGES + 4;  // [EPI_GROUPS] (PROJ) residual tile loads
+constexpr int B_TMEM = 2 * STAGES + 6;
 
 struct Args {
   int64_t T, Ts, Tp, C, H;
@@ -217,7 +218,14 @@ __device__ __forceinline__ float2 pool_pair_split(const char* stg, int j, int fi
   return make_float2(__fdiv_rn(__fadd_rn(x0.x, res.x), fn), __fdiv_rn(__fadd_rn(x0.y, res.y), fn));
 }
 
-template <bool PAIR>
+// PROJ = false: the QKV projection above.  PROJ = true: the block's output
+// projection with the residual fused, out (T, C) = res + o W^T + b, where
+// the A operand is the attention output o (H, T, 64) head-major itself:
+// K chunk kc of a row tile is head kc's 128 x 64 box (a 3-D map), so the
+// (H, T, d) -> (T, C) transpose never happens; tm_q is the (C, T) output
+// map, tm_k the residual's (the epilogue TMA-loads the residual tile into
+// its staging buffer, adds it in fp32 and stores the sum from there).
+template <bool PAIR, bool PROJ = false>
 __global__ void __launch_bounds__(THREADS, 1)
     qkv_pool_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -240,6 +248,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(BAR(B_FULL + s), 1);
       mbar_init(BAR(B_EMPTY + s), PAIR ? 2 : 1);  // pair: both CTAs' MMAs read the multicast B half
     }
+    if (PROJ)
+      for (int g = 0; g < EPI_GROUPS; ++g) mbar_init(BAR(B_RES + g), 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(BAR(B_TFULL + b), 1);
       mbar_init(BAR(B_TEMPTY + b), 4);  // one arrive per epilogue warp
@@ -255,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
+    if (PROJ) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_k) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -293,7 +304,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (elect_one()) {
           const uint32_t dst = sbase + s * STAGE_BYTES;
           mbar_expect_tx(BAR(B_FULL + s), STAGE_BYTES);
-          tma_load_2d(dst, &tm_a, BAR(B_FULL + s), kc * BK, row0);
+          if constexpr (PROJ) tma_load_3d(dst, &tm_a, BAR(B_FULL + s), 0, row0, kc);  // head kc
+          else tma_load_2d(dst, &tm_a, BAR(B_FULL + s), kc * BK, row0);
           if constexpr (PAIR) {
             // this CTA's half of B (128 feature rows) into both CTAs' stage s
             const uint32_t half = crank * (B_BYTES / 2);
@@ -344,6 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     stg += grp * STG_GROUP;
     float* const sbias = reinterpret_cast<float*>(smem + OFF_BIAS) + grp * BN;
     const uint32_t named_bar = 1 + grp;
+    uint32_t res_phase = 0;  // (PROJ) parity of this group's residual barrier
     uint32_t i = grp;
     for (int32_t u = u0 + grp * ustride; u < U; u += EPI_GROUPS * ustride, i += EPI_GROUPS) {
       int32_t m, n;
@@ -354,8 +367,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                            : special     ? min(BM, (int32_t)A.Ts - row0)
                                          : min(BM, (int32_t)A.Tp - (m - A.nst) * BM);
       const int32_t f0 = n * BN;
-      const int which = (int)(f0 / C);                  // 0 q, 1 k, 2 v
-      const int h0 = (int)((f0 - which * C) >> 6);      // first head of the tile
+      const int which = PROJ ? 0 : (int)(f0 / C);       // 0 q, 1 k, 2 v
+      const int h0 = (int)((f0 - which * C) >> 6);      // first head (PROJ: 64-column block) of the tile
       const uint32_t ab = i & 1;
       // the tile's biases into shared memory (fp32) while its MMAs run
       if (et < BN / 2) {
@@ -370,6 +383,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       float* const poolp = which == 0 ? A.pooled[0] : which == 1 ? A.pooled[1] : nullptr;
 #pragma unroll 1
       for (int pass = 0; pass < NPASS; ++pass) {
+        if constexpr (PROJ) {
+          // the residual's SH 128 x 64 blocks into the (free) staging buffer
+          if (et == 0 && rows > 0) {
+            mbar_expect_tx(BAR(B_RES + grp), SH * STG_HEAD);
+            for (int jj = 0; jj < SH; ++jj)
+              tma_load_2d(smem_u32(stg + jj * STG_HEAD), &tm_k, BAR(B_RES + grp),
+                          f0 + (pass * SH + jj) * 64, row0);
+          }
+          if (rows > 0) mbar_wait(BAR(B_RES + grp), res_phase);
+          res_phase ^= rows > 0 ? 1u : 0u;
+        }
 #pragma unroll 1
         for (int jj = 0; jj < SH; ++jj) {
           const int j = pass * SH + jj;
@@ -387,6 +411,17 @@ __global__ void __launch_bounds__(THREADS, 1)
               const float4 hi = reinterpret_cast<const float4*>(sbias + j * 64 + c * 8)[1];
               b8[0] = lo.x; b8[1] = lo.y; b8[2] = lo.z; b8[3] = lo.w;
               b8[4] = hi.x; b8[5] = hi.y; b8[6] = hi.z; b8[7] = hi.w;
+            }
+            if constexpr (PROJ) {
+              // + residual (fp32), one rounding to bf16 for the whole sum
+              const uint4 rv = *reinterpret_cast<const uint4*>(stg + stg_off(jj, r, c));
+              const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rw[q]));
+                b8[2 * q] = __fadd_rn(b8[2 * q], f.x);
+                b8[2 * q + 1] = __fadd_rn(b8[2 * q + 1], f.y);
+              }
             }
             uint32_t w[4];
 #pragma unroll
@@ -411,16 +446,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         // staging layout (it is the SW128 box layout); a partial special
         // tile, whose extra rows belong to the first patch tile, is stored
         // row by row.
-        const bool tma_store = QKV_TMA_STORE && rows > 0 && (rows == BM || !special);
+        const bool tma_store = (QKV_TMA_STORE || PROJ) && rows > 0 && (rows == BM || !special);
         if (tma_store) {
           if (et == 0) {
             const CUtensorMap* om = which == 0 ? &tm_q : which == 1 ? &tm_k : &tm_v;
 #pragma unroll 1
-            for (int jj = 0; jj < SH; ++jj)
-              asm volatile(
-                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(om),
-                  "r"(smem_u32(stg + jj * STG_HEAD)), "r"(0), "r"(row0), "r"(h0 + pass * SH + jj)
-                  : "memory");
+            for (int jj = 0; jj < SH; ++jj) {
+              if constexpr (PROJ)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tm_q),
+                    "r"(smem_u32(stg + jj * STG_HEAD)), "r"(f0 + (pass * SH + jj) * 64), "r"(row0)
+                    : "memory");
+              else
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(om),
+                    "r"(smem_u32(stg + jj * STG_HEAD)), "r"(0), "r"(row0), "r"(h0 + pass * SH + jj)
+                    : "memory");
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         } else {
@@ -532,6 +574,63 @@ static int make_map_out(CUtensorMap* map, void* base, int64_t H, int64_t T) {
   return BSA_OK;
 }
 
+// persistent launch of qkv_pool_kernel<PAIR, PROJ> over a's tiles; B is the
+// (w_rows, w_cols) bf16 weight
+template <bool PROJ>
+static int launch_gemm(const CUtensorMap& ma, const void* weight, int64_t w_rows, int64_t w_cols,
+                       const CUtensorMap (&mo)[3], const Args& a, cudaStream_t stream) {
+  int dev = 0, sms = 0;
+  BSA_CUDA_TRY(cudaGetDevice(&dev));
+  BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // persistent CTA pairs: as many as the GPU co-schedules (a GPC with an odd
+  // SM count leaves one SM out), never more, or the surplus would run as a
+  // second wave behind the static tile split; none co-schedulable (or
+  // QKV_PAIR=0): single CTAs
+  static int max_pairs[64];  // per PROJ instantiation (template static)
+  static bool queried[64];
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int slot = dev & 63;
+  if (!queried[slot]) {
+    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<true, PROJ>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<false, PROJ>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    int n = 0;
+    cfg.gridDim = dim3(2 * std::max(1, sms / 2));
+    if (QKV_PAIR && cudaOccupancyMaxActiveClusters(&n, qkv_pool_kernel<true, PROJ>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      n = 0;
+    }
+    max_pairs[slot] = QKV_PAIR ? n : 0;
+    queried[slot] = true;
+  }
+  const bool pair = max_pairs[slot] > 0;
+  CUtensorMap mb;
+  int rc = make_map_2d(&mb, weight, w_rows, w_cols, pair ? BN / 2 : BN);
+  if (rc) return rc;
+  const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
+  if (pair) {
+    const int64_t units = (int64_t)((a.m_tiles + 1) / 2) * a.n_tiles;
+    cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(units, max_pairs[slot]));
+    BSA_CUDA_TRY(cudaLaunchKernelEx(&cfg, qkv_pool_kernel<true, PROJ>, ma, mb, mo[0], mo[1], mo[2], a));
+  } else {
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    qkv_pool_kernel<false, PROJ><<<grid, THREADS, SMEM_BYTES, stream>>>(ma, mb, mo[0], mo[1], mo[2], a);
+  }
+  BSA_LAUNCH_CHECK();
+  return BSA_OK;
+}
+
 }  // namespace qkv
 }  // namespace bsa
 
@@ -580,59 +679,47 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
   a.out[2] = (__nv_bfloat16*)v;
   a.pooled[0] = q_pooled;
   a.pooled[1] = k_pooled;
-  int dev = 0, sms = 0;
-  BSA_CUDA_TRY(cudaGetDevice(&dev));
-  BSA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // persistent CTA pairs: as many as the GPU co-schedules (a GPC with an odd
-  // SM count leaves one SM out), never more, or the surplus would run as a
-  // second wave behind the static tile split; none co-schedulable (or
-  // QKV_PAIR=0): single CTAs
-  static int max_pairs[64];
-  static bool queried[64];
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  const int slot = dev & 63;
-  if (!queried[slot]) {
-    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    BSA_CUDA_TRY(cudaFuncSetAttribute(qkv_pool_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    int n = 0;
-    cfg.gridDim = dim3(2 * std::max(1, sms / 2));
-    if (QKV_PAIR && cudaOccupancyMaxActiveClusters(&n, qkv_pool_kernel<true>, &cfg) != cudaSuccess) {
-      (void)cudaGetLastError();
-      n = 0;
-    }
-    max_pairs[slot] = QKV_PAIR ? n : 0;
-    queried[slot] = true;
-  }
-  const bool pair = max_pairs[slot] > 0;
-  CUtensorMap ma, mb, mo[3];
+  CUtensorMap ma, mo[3];
   int rc = make_map_2d(&ma, x, tokens, dim_in, BM);
-  if (!rc) rc = make_map_2d(&mb, weight, 3 * dim_in, dim_in, pair ? BN / 2 : BN);
   for (int i = 0; i < 3 && !rc; ++i) rc = make_map_out(&mo[i], a.out[i], heads, tokens);
   if (rc) return rc;
-  const int64_t tiles = (int64_t)a.m_tiles * a.n_tiles;
-  if (pair) {
-    const int64_t units = (int64_t)((a.m_tiles + 1) / 2) * a.n_tiles;
-    cfg.gridDim = dim3(2 * (unsigned)std::min<int64_t>(units, max_pairs[slot]));
-    BSA_CUDA_TRY(cudaLaunchKernelEx(&cfg, qkv_pool_kernel<true>, ma, mb, mo[0], mo[1], mo[2], a));
-  } else {
-    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-    qkv_pool_kernel<false><<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(ma, mb, mo[0], mo[1],
-                                                                               mo[2], a);
-  }
-  BSA_LAUNCH_CHECK();
-  return BSA_OK;
+  return launch_gemm<false>(ma, weight, 3 * dim_in, dim_in, mo, a, (cudaStream_t)stream);
+}
+
+int bsa_proj_residual(const void* o, int64_t heads, int64_t tokens, const void* weight,
+                      const void* bias, const void* residual, void* out, void* stream) {
+  using namespace bsa::qkv;
+  if (!o || !weight || !residual || !out) return fail(BSA_EINVAL, "proj_residual: null pointer");
+  const int64_t C = heads * 64;
+  if (heads < 1 || C % BN != 0)
+    return fail(BSA_EUNSUPPORTED, "proj_residual: heads*64 must be a multiple of 256, got %lld",
+                (long long)C);
+  if (tokens < 1 || tokens >= ((int64_t)1 << 31))
+    return fail(BSA_EINVAL, "proj_residual: bad token count %lld", (long long)tokens);
+  for (const void* p : {o, weight, residual, (const void*)out})
+    if ((uintptr_t)p % 16) return fail(BSA_EINVAL, "proj_residual: pointers must be 16-byte aligned");
+  if (bias && (uintptr_t)bias % 16) return fail(BSA_EINVAL, "proj_residual: bias must be 16-byte aligned");
+  Args a;
+  a.T = tokens;
+  a.Ts = 0;  // no special/patch split: row tiles over all tokens
+  a.Tp = tokens;
+  a.C = C;
+  a.H = heads;
+  a.nst = 0;
+  a.nq = (int32_t)ceil_div(tokens, (int64_t)BM);
+  a.nk = 0;
+  a.m_tiles = a.nq;
+  a.n_tiles = (int32_t)(C / BN);
+  a.bias = (const __nv_bfloat16*)bias;
+  a.out[0] = a.out[1] = a.out[2] = (__nv_bfloat16*)out;
+  a.pooled[0] = a.pooled[1] = nullptr;
+  CUtensorMap ma, mo[3];
+  int rc = make_map_out(&ma, const_cast<void*>(o), heads, tokens);  // A: head kc's (64, 128) box
+  if (!rc) rc = make_map_2d(&mo[0], out, tokens, C, BM);              // output (C, T)
+  if (!rc) rc = make_map_2d(&mo[1], residual, tokens, C, BM);         // residual (C, T)
+  if (rc) return rc;
+  mo[2] = mo[0];
+  return launch_gemm<true>(ma, weight, C, C, mo, a, (cudaStream_t)stream);
 }
 
 }  // extern "C"

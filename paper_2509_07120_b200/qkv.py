@@ -70,3 +70,44 @@ def qkv_projection(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | N
             g.block_q, g.block_k, q.data_ptr(), k.data_ptr(), v.data_ptr(), N.ptr(qp), N.ptr(kp),
             N.stream_ptr()), "qkv_projection")
     return q, k, v, qp, kp
+
+
+def proj_residual(o: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None,
+                  residual: torch.Tensor, *, out: torch.Tensor | None = None):
+    """The block's output projection with its residual, on the tensor cores:
+    ``residual + o' W^T + bias`` with o' the (T, C) token-major view of the
+    attention output ``o`` (heads, T, 64) bf16 -- read head-major in place
+    as the GEMM's A operand (no transpose pass) -- and one bf16 rounding of
+    the fp32 sum.  ``out`` may be ``residual`` itself (in-place update).
+    Returns the (T, C) bf16 result."""
+    N.require_cuda()
+    for name, t in (("o", o), ("weight", weight), ("residual", residual)):
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda" or t.dtype != torch.bfloat16:
+            raise ValueError(f"{name} must be a bf16 CUDA tensor")
+    if o.dim() != 3 or o.shape[2] != 64:
+        raise ValueError(f"o must be (heads, tokens, 64), got {tuple(o.shape)}")
+    H, T, _ = o.shape
+    C = H * 64
+    if tuple(weight.shape) != (C, C):
+        raise ValueError(f"weight must be ({C}, {C}), got {tuple(weight.shape)}")
+    if tuple(residual.shape) != (T, C):
+        raise ValueError(f"residual must be ({T}, {C}), got {tuple(residual.shape)}")
+    if bias is not None and (tuple(bias.shape) != (C,) or bias.dtype != torch.bfloat16):
+        raise ValueError(f"bias must be ({C},) bf16")
+    for name, t in (("weight", weight), ("residual", residual), ("bias", bias)):
+        if t is not None and t.device != o.device:
+            raise ValueError(f"{name} is on {t.device}, o on {o.device}")
+    if out is None:
+        out = torch.empty((T, C), dtype=torch.bfloat16, device=o.device)
+    elif tuple(out.shape) != (T, C) or out.dtype != torch.bfloat16 or not out.is_contiguous() \
+            or out.device != o.device:
+        raise ValueError(f"out must be a contiguous ({T}, {C}) bf16 tensor on {o.device}")
+    o, weight = o.contiguous(), weight.contiguous()
+    if not residual.is_contiguous():
+        residual = residual.contiguous()
+    bias = bias.contiguous() if bias is not None else None
+    with N.on_device(o.device):
+        N.check(N.lib().bsa_proj_residual(o.data_ptr(), H, T, weight.data_ptr(), N.ptr(bias),
+                                          residual.data_ptr(), out.data_ptr(), N.stream_ptr()),
+                "proj_residual")
+    return out

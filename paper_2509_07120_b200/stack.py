@@ -25,7 +25,7 @@ import torch.nn.functional as F
 from .dense import AttentionInputs
 from .layout import BlockGeometry, TokenLayout, partition_permutation
 from .maskpred import MaskPolicy, predict_mask, predict_mask_pooled
-from .qkv import qkv_projection
+from .qkv import proj_residual, qkv_projection
 from .sparse import SparseAttentionJob, sparse_attention
 
 
@@ -109,17 +109,24 @@ class GlobalAttentionStack:
         whose epilogue writes head-major Q/K/V plus the pooled patch Q/K
         (qkv.qkv_projection), predict_mask_pooled (no pooling pass), the
         block-sparse kernel on the in-place permuted inputs (no pack pass),
-        and the output projection.  Same mask as mode="sparse" on the same
+        and the output projection (cuBLAS here; the fused stack uses
+        qkv.proj_residual, which also adds the residual).  Same mask as mode="sparse" on the same
         Q/K; Q/K/V themselves come from this GEMM instead of cuBLAS."""
         T, C = xp.shape
+        o = self._attend_fused(xp, blk, layout, policy)
+        return F.linear(o.permute(1, 0, 2).reshape(T, C), blk.proj_w, blk.proj_b)
+
+    def _attend_fused(self, xp, blk, layout, policy):
+        """LayerNorm -> fused QKV projection (+ pooled Q/K) -> scoring from
+        the pools -> block-sparse attention on the head-major partitioned
+        Q/K/V; returns the (H, T, 64) output, partitioned order."""
+        C = xp.shape[1]
         h = F.layer_norm(xp, (C,), blk.ln_w, blk.ln_b)
         q, k, v, qp, kp = qkv_projection(h, blk.qkv_w, blk.qkv_b, self.heads, layout,
                                          policy.geometry)
         mask = predict_mask_pooled(qp, kp, policy, validate=False)
-        o = sparse_attention(SparseAttentionJob(AttentionInputs(q, k, v, validate=False), layout,
-                                                mask), inputs_permuted=True)
-        o = o.permute(1, 0, 2).reshape(T, C)
-        return F.linear(o, blk.proj_w, blk.proj_b)
+        return sparse_attention(SparseAttentionJob(AttentionInputs(q, k, v, validate=False), layout,
+                                                   mask), inputs_permuted=True)
 
     def _forward_fused(self, x: torch.Tensor, layout: TokenLayout, policy: MaskPolicy):
         # every op but attention acts per token: keep the residual stream in
@@ -129,7 +136,10 @@ class GlobalAttentionStack:
         inv_t = torch.from_numpy(inv).to(x.device)
         xp = x.index_select(0, perm_t)
         for blk in self.blocks:
-            xp = xp + self.attention_fused(xp, blk, layout, policy)
+            # output projection + bias + residual in one GEMM reading the
+            # head-major attention output in place (qkv.proj_residual)
+            o = self._attend_fused(xp, blk, layout, policy)
+            xp = proj_residual(o, blk.proj_w, blk.proj_b, xp)
             if blk.mlp is not None:
                 lw, lb, w1, b1, w2, b2 = blk.mlp
                 h = F.layer_norm(xp, (self.dim,), lw, lb)

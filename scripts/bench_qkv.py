@@ -59,6 +59,14 @@ def main():
     res["fused_nopool_ms"] = timeit(lambda: bsa.qkv_projection(x, w, b, H, lay, geo, pooled=False),
                                     a.reps)
     res["fused_tflops"] = flops / res["fused_ms"] / 1e9
+    # output projection + residual: cuBLAS linear on the transposed
+    # attention output + add, vs proj_residual on the head-major output
+    o = torch.randn((H, T, 64), generator=g).to("cuda", torch.bfloat16)
+    wp = (torch.randn((C, C), generator=g) / 32).to("cuda", torch.bfloat16)
+    bp = torch.zeros(C, device="cuda", dtype=torch.bfloat16)
+    res["proj_cublas_ms"] = timeit(
+        lambda: x + F.linear(o.permute(1, 0, 2).reshape(T, C), wp, bp), a.reps)
+    res["proj_fused_ms"] = timeit(lambda: bsa.proj_residual(o, wp, bp, x), a.reps)
     res["cublas_tflops"] = flops / res["cublas_linear_ms"] / 1e9
     if a.layer:
         st = GlobalAttentionStack(layers=1, heads=H, seed=1)

@@ -101,6 +101,11 @@ def main():
     ok &= bool(torch.isfinite(qp4).all()) and bool(torch.isfinite(v4.float()).all())
     print(f"qkv_projection + predict_mask_pooled: {int(m4.device_counts().sum().item())} blocks",
           flush=True)
+    o4 = torch.randn((4, lay.total_tokens, 64), device="cuda").to(torch.bfloat16)
+    wp = (torch.randn((C, C), device="cuda") / 16).to(torch.bfloat16)
+    y4 = bsa.proj_residual(o4, wp, b[:C], x)
+    ok &= bool(torch.isfinite(y4.float()).all())
+    print("proj_residual: finite", bool(torch.isfinite(y4.float()).all()), flush=True)
     torch.cuda.synchronize()
     print("SANITIZE_DRIVER_OK" if ok else "SANITIZE_DRIVER_BAD", flush=True)
     return 0 if ok else 1

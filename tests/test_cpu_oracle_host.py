@@ -227,11 +227,12 @@ def test_tensor_core_kernel_uses_tcgen05_and_tma():
         pytest.skip("cuobjdump unavailable")
     for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM", "STTM"):
         assert mnemonic in out.stdout, mnemonic
-    # the fused QKV projection: tcgen05 MMAs, TMA loads
-    # (multicast B halves) and TMA bulk tensor stores of the head tiles
+    # the fused QKV projection and output projection:
+    # tcgen05 MMAs, TMA loads (multicast B halves) and TMA bulk tensor stores
     funcs = re.split(r"\n\s*Function : ", out.stdout)
     qkv = [f for f in funcs if f.split("\n", 1)[0].find("qkv_pool_kernel") >= 0]
-    assert len(qkv) == 2, "pair and single-CTA instances of qkv_pool_kernel"
+    # pair / single-CTA x QKV projection / output projection + residual
+    assert len(qkv) == 4, "four instances of qkv_pool_kernel"
     for body in qkv:
         for mnemonic in ("UTCHMMA", "UTMALDG", "UTMASTG", "LDTM"):
             assert mnemonic in body, mnemonic

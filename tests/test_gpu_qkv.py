@@ -225,3 +225,58 @@ def test_qkv_projection_rejects_bad_inputs(bsa):
         bsa.predict_mask_pooled(torch.zeros(4, 3, 64, device="cuda"),
                                 torch.zeros(4, 2, 64, device="cuda"),
                                 bsa.MaskPolicy(0.0, 0.5, bsa.geometry_for(lay)))
+
+
+# ---------------------------------------------------------------------------
+# the output projection with its residual (qkv.proj_residual)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("H,T,bias", [(4, 300, True), (16, 5496, True), (16, 27480, False),
+                                      (4, 1, True), (8, 129, False)])
+def test_proj_residual_values(bsa, H, T, bias):
+    """out = residual + o' W^T + b with o' the token-major view of the
+    head-major o: within half a bf16 ulp of float64 plus the fp32
+    accumulation bound (one rounding of the whole sum), and within the
+    rounding of torch's two-step residual + F.linear."""
+    import torch
+    C = H * 64
+    g = torch.Generator(device="cpu").manual_seed(H * 1000 + T)
+    o = torch.randn((H, T, 64), generator=g).to("cuda", torch.bfloat16)
+    w = (torch.randn((C, C), generator=g) / np.sqrt(C)).to("cuda", torch.bfloat16)
+    b = (0.1 * torch.randn((C,), generator=g)).to("cuda", torch.bfloat16) if bias else None
+    res = torch.randn((T, C), generator=g).to("cuda", torch.bfloat16)
+    out = bsa.proj_residual(o, w, b, res)
+    ot = o.permute(1, 0, 2).reshape(T, C)
+    ref = res.double() + ot.double() @ w.double().T + (b.double() if bias else 0.0)
+    mag = res.double().abs() + ot.double().abs() @ w.double().abs().T
+    err = (out.double() - ref).abs()
+    bound = ref.abs() * 2.0 ** -8 + mag * 2.0 ** -21
+    assert bool((err <= bound).all()), f"{int((err > bound).sum())} beyond bound, max {err.max().item()}"
+    # torch rounds the projection y to bf16 before adding the residual:
+    # its result is within half an ulp of |y| (plus its own final rounding)
+    y = torch.nn.functional.linear(ot, w, b)
+    tref = (res + y).double()
+    tb = (tref.abs() + y.double().abs()) * 2.0 ** -8 + ref.abs() * 2.0 ** -8 + mag * 2.0 ** -20
+    assert bool(((out.double() - tref).abs() <= tb).all())
+
+
+def test_proj_residual_in_place_and_guards(bsa):
+    import torch
+    H, T = 4, 1000
+    C = H * 64
+    o = torch.randn((H, T, 64), device="cuda").to(torch.bfloat16)
+    w = (torch.randn((C, C), device="cuda") / 16).to(torch.bfloat16)
+    res = torch.randn((T, C), device="cuda").to(torch.bfloat16)
+    want = bsa.proj_residual(o, w, None, res)
+    x = res.clone()
+    got = bsa.proj_residual(o, w, None, x, out=x)
+    assert got.data_ptr() == x.data_ptr() and torch.equal(got, want)
+    with pytest.raises(ValueError):
+        bsa.proj_residual(o.float(), w, None, res)
+    with pytest.raises(ValueError):
+        bsa.proj_residual(o, w[:, :-1], None, res)
+    with pytest.raises(ValueError):
+        bsa.proj_residual(o, w, None, res[:-1])
+    with pytest.raises(ValueError):  # C % 256 != 0
+        o2 = torch.zeros((2, T, 64), device="cuda", dtype=torch.bfloat16)
+        bsa.proj_residual(o2, torch.zeros((128, 128), device="cuda", dtype=torch.bfloat16), None,
+                          torch.zeros((T, 128), device="cuda", dtype=torch.bfloat16))
