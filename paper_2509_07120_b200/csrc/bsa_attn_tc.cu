@@ -173,9 +173,14 @@ using CfgExact = Cfg<false>;
 #endif
 // which of each 8 consecutive pairs take the FMA-pipe polynomial: the first
 // POLY (SPREAD 0), or POLY spread evenly over the 8 (SPREAD 1: 0,3,6 / 0,2,4,6)
+#ifndef BSA_TC_POLY_PER16
+#define BSA_TC_POLY_PER16 0  // (experiments) POLY counts pairs per 16 instead of per 8
+#endif
 template <int POLY>
 __device__ __forceinline__ constexpr bool poly_pair(int e) {
-  if constexpr (BSA_TC_POLY_SPREAD == 0 || POLY == 0) {
+  if constexpr (BSA_TC_POLY_PER16 != 0) {
+    return ((e & 15) * POLY) % 16 < POLY;  // POLY of every 16 pairs, spread evenly
+  } else if constexpr (BSA_TC_POLY_SPREAD == 0 || POLY == 0) {
     return (e & 7) < POLY;
   } else {
     return ((e & 7) * POLY) % 8 < POLY;
@@ -1144,6 +1149,10 @@ static int launch_pick(const TcMaps& m, const AttnGeom& G, const TcArgs& a, int 
     case 2: return launch_variant<2, false, EXACT>(m, G, a, grid, st);
     case 3: return launch_variant<3, false, EXACT>(m, G, a, grid, st);
     case 4: return launch_variant<4, false, EXACT>(m, G, a, grid, st);
+#if BSA_TC_POLY_PER16
+    case 5: return launch_variant<5, false, EXACT>(m, G, a, grid, st);
+    case 6: return launch_variant<6, false, EXACT>(m, G, a, grid, st);
+#endif
     case 16: return launch_variant<0, true, EXACT>(m, G, a, grid, st);
     case 18: return launch_variant<2, true, EXACT>(m, G, a, grid, st);
     case 19: return launch_variant<3, true, EXACT>(m, G, a, grid, st);
