@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true", help="skip the dense SDPA baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-interleaved", action="store_true",
+                    help="e2e leg: plain H2D copies + the pack pass instead of token-reordering copies")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
                     help="auto: sharded when N > 1")
@@ -443,7 +445,8 @@ def run_ours(a):
             else:
                 sizes = [int(x) for x in str(a.e2e_chunk).split(",")]
                 chunks = sizes[0] if len(sizes) == 1 else sizes
-            pipe = HostLayerPipeline(H, T, d, torch.bfloat16, chunk_heads=chunks)
+            pipe = HostLayerPipeline(H, T, d, torch.bfloat16, chunk_heads=chunks,
+                                     partitioned_copies=not a.e2e_interleaved)
 
             def e2e_step():
                 pipe.run(hq, hk, hv, lay, pol, out=hout)

@@ -167,6 +167,16 @@ int bsa_qkv_project_pooled(const void* x, int64_t tokens, int64_t dim_in, const 
 int bsa_proj_residual(const void* o, int64_t heads, int64_t tokens, const void* weight,
                       const void* bias, const void* residual, void* out, void* stream);
 
+/* Token-order conversion by the copy engines: (heads, T, row_bytes) between
+ * the interleaved source order and the partitioned order [specials |
+ * patches] (layout.py:113-138, partition_permutation), two strided copies
+ * per head (cudaMemcpy2DAsync, any host/device combination).
+ * to_partitioned = 1: src interleaved -> dst partitioned; 0: the inverse.
+ * Used by pipeline.HostLayerPipeline so host-resident layers arrive in the
+ * layout bsa_sparse_attention reads in place (inputs_permuted = 1). */
+int bsa_copy_tokens(void* dst, const void* src, const bsa_layout* layout, int64_t heads,
+                    int64_t row_bytes, int32_t to_partitioned, void* stream);
+
 /* Which scoring kernel predict_mask runs for nk key blocks of head_dim
  * dim: the fused score+softmax+select kernel's rows per CTA (8 or 4), or 0
  * for the three-kernel path (rows longer than shared memory holds, head_dim

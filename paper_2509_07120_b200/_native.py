@@ -87,6 +87,7 @@ def _declare(L):
         "bsa_qkv_project_pooled": ([vp, i64, i64, vp, vp, i64, i64, i64, i32, i32, vp, vp, vp, vp,
                                     vp, vp], ctypes.c_int),
         "bsa_proj_residual": ([vp, i64, i64, vp, vp, vp, vp, vp], ctypes.c_int),
+        "bsa_copy_tokens": ([vp, vp, pl, i64, i64, i32, vp], ctypes.c_int),
         "bsa_sparse_attention_workspace": ([pl, i64, i64, i32, i32, i32, i32, i32], sz),
         "bsa_sparse_attention": ([pt, pt, pt, vp, i32, pl, i32, i32, vp, vp, f32, i32, i32, i32,
                                   i32, vp, sz, vp], ctypes.c_int),
@@ -129,7 +130,7 @@ def exported_symbols():
         "bsa_attention_row_stats", "bsa_block_attention_map", "bsa_check_finite",
         "bsa_scoring_rows_per_cta", "bsa_debug_scoring_trace",
         "bsa_predict_mask_pooled_workspace", "bsa_predict_mask_pooled", "bsa_qkv_project_pooled",
-        "bsa_proj_residual",
+        "bsa_proj_residual", "bsa_copy_tokens",
     ]
 
 

@@ -125,3 +125,43 @@ extern "C" int bsa_check_finite(const bsa_tensor* x, int32_t* flag, void* stream
   BSA_LAUNCH_CHECK();
   return BSA_OK;
 }
+
+// Token-order conversion on the copy engines (host <-> device, or device <->
+// device): (heads, T, row) in the interleaved source order <-> the
+// partitioned order [specials | patches] (layout.py:113-138), as two strided
+// copies per head (a frame's specials and its patches are contiguous runs).
+// A host-resident layer then lands in HBM already partitioned -- the layout
+// the attention kernel reads in place -- and its output leaves the same way.
+extern "C" int bsa_copy_tokens(void* dst, const void* src, const bsa_layout* layout, int64_t heads,
+                               int64_t row_bytes, int32_t to_partitioned, void* stream) {
+  using namespace bsa;
+  if (!dst || !src || !layout) return fail(BSA_EINVAL, "copy_tokens: null argument");
+  const Layout L = to_layout(layout);
+  if (L.frames < 1 || L.P < 1 || L.S < 0 || heads < 1 || row_bytes < 1)
+    return fail(BSA_EINVAL, "copy_tokens: bad shape");
+  const int64_t T = L.tokens(), F = L.frames, S = L.S, P = L.P, Ts = L.n_spec();
+  const size_t frame = (size_t)(S + P) * row_bytes;
+  const size_t spec_off = (size_t)(L.specials_first ? 0 : P) * row_bytes;
+  const size_t patch_off = (size_t)(L.specials_first ? S : 0) * row_bytes;
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int64_t h = 0; h < heads; ++h) {
+    char* d = (char*)dst + (size_t)h * T * row_bytes;
+    const char* s = (const char*)src + (size_t)h * T * row_bytes;
+    if (to_partitioned) {
+      if (S > 0)
+        BSA_CUDA_TRY(cudaMemcpy2DAsync(d, (size_t)S * row_bytes, s + spec_off, frame,
+                                       (size_t)S * row_bytes, (size_t)F, cudaMemcpyDefault, st));
+      BSA_CUDA_TRY(cudaMemcpy2DAsync(d + (size_t)Ts * row_bytes, (size_t)P * row_bytes,
+                                     s + patch_off, frame, (size_t)P * row_bytes, (size_t)F,
+                                     cudaMemcpyDefault, st));
+    } else {
+      if (S > 0)
+        BSA_CUDA_TRY(cudaMemcpy2DAsync(d + spec_off, frame, s, (size_t)S * row_bytes,
+                                       (size_t)S * row_bytes, (size_t)F, cudaMemcpyDefault, st));
+      BSA_CUDA_TRY(cudaMemcpy2DAsync(d + patch_off, frame, s + (size_t)Ts * row_bytes,
+                                     (size_t)P * row_bytes, (size_t)P * row_bytes, (size_t)F,
+                                     cudaMemcpyDefault, st));
+    }
+  }
+  return BSA_OK;
+}

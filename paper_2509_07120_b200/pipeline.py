@@ -43,11 +43,16 @@ class HostLayerPipeline:
     """Reusable device buffers and streams for repeated layers of one shape."""
 
     def __init__(self, heads: int, tokens: int, head_dim: int, dtype=torch.bfloat16,
-                 chunk_heads="auto", device=None):
+                 chunk_heads="auto", device=None, partitioned_copies: bool = True):
         """chunk_heads: heads per pipeline chunk, the list of chunk sizes
         (summing to `heads`), or "auto" (ramp_chunks). Small first and last
         chunks shorten the ramp: the first H2D and the last D2H are the only
-        uncovered copies."""
+        uncovered copies.
+
+        partitioned_copies: the copy engines reorder tokens on the way in
+        (interleaved host rows -> partitioned device rows, two strided copies
+        per head: bsa_copy_tokens) and back on the way out, so the kernels
+        read Q/K/V in place (no pack pass) and score contiguous patch rows."""
         if isinstance(chunk_heads, str):
             if chunk_heads != "auto":
                 raise ValueError(f"chunk_heads must be an int, a list or 'auto', got {chunk_heads!r}")
@@ -71,6 +76,7 @@ class HostLayerPipeline:
             h0 += x
         self.bufs = [torch.empty(self.shape, dtype=dtype, device=self.device) for _ in range(3)]
         self.obuf = torch.empty(self.shape, dtype=dtype, device=self.device)
+        self.partitioned = bool(partitioned_copies)
         self.s_in = torch.cuda.Stream(self.device)
         self.s_out = torch.cuda.Stream(self.device)
 
@@ -102,27 +108,48 @@ class HostLayerPipeline:
         chunks = self.chunks
         # the copy-in stream must not overwrite buffers a previous call still reads
         self.s_in.wait_stream(comp)
+        part = self.partitioned
+        if part:
+            for name, t in (("q", q), ("k", k), ("v", v)):
+                if not t.is_contiguous():
+                    raise ValueError(f"{name} must be contiguous")
+            if layout.total_tokens != self.shape[1]:
+                raise ValueError(f"layout has {layout.total_tokens} tokens, buffers {self.shape[1]}")
+            lay_d = N.layout_desc(layout)
+            row = self.shape[2] * q.element_size()
+            Ts = layout.special_tokens
+
+        def copy_in(dst, src, a, b):
+            if part:
+                N.check(N.lib().bsa_copy_tokens(dst[a:b].data_ptr(), src[a:b].data_ptr(), lay_d,
+                                                b - a, row, 1, self.s_in.cuda_stream), "copy_tokens")
+            else:
+                dst[a:b].copy_(src[a:b], non_blocking=True)
+
         for a, b in chunks:
             with torch.cuda.stream(self.s_in):
                 # Q and K first: scoring can start while V is still in flight
-                dq[a:b].copy_(q[a:b], non_blocking=True)
-                dk[a:b].copy_(k[a:b], non_blocking=True)
+                copy_in(dq, q, a, b)
+                copy_in(dk, k, a, b)
                 ev_qk = torch.cuda.Event()
                 ev_qk.record(self.s_in)
-                dv[a:b].copy_(v[a:b], non_blocking=True)
+                copy_in(dv, v, a, b)
                 ev_v = torch.cuda.Event()
                 ev_v.record(self.s_in)
                 done_in.append((ev_qk, ev_v))
         for (a, b), (ev_qk, ev_v) in zip(chunks, done_in):
             comp.wait_event(ev_qk)
-            mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout, validate=False)
+            if part:  # patch rows are contiguous after the specials
+                mask = predict_mask(dq[a:b, Ts:], dk[a:b, Ts:], policy, validate=False)
+            else:
+                mask = predict_mask(dq[a:b], dk[a:b], policy, layout=layout, validate=False)
             comp.wait_event(ev_v)
             if validate:  # device scan into one flag, read once at the end
                 for x in (dq, dk, dv):
                     N.finite_scan(x[a:b], bad)
             job = SparseAttentionJob(AttentionInputs(dq[a:b], dk[a:b], dv[a:b], validate=False),
                                      layout, mask)
-            sparse_attention(job, out=self.obuf[a:b])
+            sparse_attention(job, out=self.obuf[a:b], inputs_permuted=part)
             ev = torch.cuda.Event()
             ev.record(comp)
             done_comp.append(ev)
@@ -130,7 +157,12 @@ class HostLayerPipeline:
                 masks.append(mask)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(ev)
-                out[a:b].copy_(self.obuf[a:b], non_blocking=True)
+                if part:  # back to the caller's interleaved token order
+                    N.check(N.lib().bsa_copy_tokens(out[a:b].data_ptr(), self.obuf[a:b].data_ptr(),
+                                                    lay_d, b - a, row, 0, self.s_out.cuda_stream),
+                            "copy_tokens")
+                else:
+                    out[a:b].copy_(self.obuf[a:b], non_blocking=True)
         comp.wait_stream(self.s_out)
         torch.cuda.current_stream(self.device).synchronize()
         if validate and int(bad.item()) != 0:
