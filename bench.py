@@ -282,13 +282,17 @@ def run_ours(a):
 
     fixed_mask = ragged_mask(bsa, H, g, pol.min_blocks, a.seed, dev) if a.mask == "ragged" else None
 
-    def step(qq, kk, vv, timing=False):
+    def step(qq, kk, vv, timing=False, score_ev=None):
         if sharded:
             return sharded_sparse_attention(qq, kk, vv, lay, pol, inputs="sharded",
                                             return_mask=True, chunk_heads=a.shard_chunk,
                                             comm_group=comm, combine=a.combine,
                                             scatter_target=target)
+        if score_ev is not None:
+            score_ev[0].record()
         mask = fixed_mask or bsa.predict_mask(qq, kk, pol, layout=lay)
+        if score_ev is not None:
+            score_ev[1].record()
         job = bsa.SparseAttentionJob(bsa.AttentionInputs(qq, kk, vv), lay, mask)
         return bsa.sparse_attention(job, timing=timing, schedule=a.schedule), mask
 
@@ -302,11 +306,18 @@ def run_ours(a):
     barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the stage split is measured inside the timed region itself: CUDA events
+    # around predict_mask on the stream, and the library's events around the
+    # tensor-core kernel launch (BSA_FLAG_TIMING, a ring read after the loop)
+    score_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                 for _ in range(a.steps)] if not sharded else [None] * a.steps
+    if not sharded:
+        sp.kernel_times(reset=True)
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
-        for _ in range(a.steps):
-            out, mask = step(q_in, k_in, v_in)
+        for i in range(a.steps):
+            out, mask = step(q_in, k_in, v_in, timing=not sharded, score_ev=score_evs[i])
         e1.record(stream)
         barrier()
     ms_total = e0.elapsed_time(e1)
@@ -316,18 +327,12 @@ def run_ours(a):
         ms_total = float(t.item())
     ms_step = ms_total / a.steps
 
-    # stage split + live kernel time of the dominant (tensor-core) kernel,
-    # CUDA events on the launching stream, averaged over `steps` launches
-    score_ms, kern_ms = [], []
-    for _ in range(a.steps if not sharded else 0):
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        mask = fixed_mask or bsa.predict_mask(q, k, pol, layout=lay)
-        s1.record(stream)
-        job = bsa.SparseAttentionJob(bsa.AttentionInputs(q, k, v), lay, mask)
-        bsa.sparse_attention(job, timing=True, schedule=a.schedule)
-        kern_ms.append(sp.last_kernel_ms())
-        score_ms.append(s0.elapsed_time(s1))
+    # stage split + live kernel time of the dominant (tensor-core) kernel over
+    # the timed steps themselves (events on the launching stream)
+    score_ms = [s0.elapsed_time(s1) for s0, s1 in score_evs] if not sharded else []
+    kern_ms = sp.kernel_times(a.steps, reset=True) if not sharded else []
+    if not sharded and len(kern_ms) != a.steps:
+        raise RuntimeError(f"expected {a.steps} kernel timings, got {len(kern_ms)}")
     # sharded mode: per-GPU share of the layer's work over the whole step
     kernel_ms = float(np.mean(kern_ms)) if kern_ms else ms_step * world
     area = mask.selected_area().astype(np.int64)

@@ -243,6 +243,12 @@ int bsa_ipc_free(void* dev_ptr);
 /* Device time (ms) of the last tensor-core attention kernel launched on this
  * host thread with BSA_FLAG_TIMING set (waits for it); -1 on error. */
 float bsa_last_kernel_ms(void);
+/* Durations (ms) of the n most recent BSA_FLAG_TIMING launches of the
+ * tensor-core kernel on this thread, oldest first (a ring of 64 event
+ * pairs: a timed loop needs no host sync inside it); synchronises on them.
+ * Returns n (<= max_n, <= 64) or -1 on a CUDA error; reset != 0 clears the
+ * count. */
+int bsa_kernel_times(float* out, int32_t max_n, int32_t reset);
 
 /* Which path bsa_sparse_attention would take for these arguments:
  * BSA_PATH_SIMT or BSA_PATH_TC (or <0 on invalid arguments). */

@@ -93,6 +93,7 @@ def _declare(L):
                                   i32, vp, sz, vp], ctypes.c_int),
         "bsa_sparse_attention_path": ([pl, i64, i32, i32, i32, i32], ctypes.c_int),
         "bsa_last_kernel_ms": ([], ctypes.c_float),
+        "bsa_kernel_times": ([vp, i32, i32], ctypes.c_int),
         "bsa_mask_selected_area": ([vp, i64, i64, i32, i32, vp, vp], ctypes.c_int),
         "bsa_mask_to_csr_workspace": ([i64, i64], sz),
         "bsa_mask_to_csr": ([vp, i64, i64, i64, vp, vp, vp, sz, vp], ctypes.c_int),
@@ -130,7 +131,7 @@ def exported_symbols():
         "bsa_attention_row_stats", "bsa_block_attention_map", "bsa_check_finite",
         "bsa_scoring_rows_per_cta", "bsa_debug_scoring_trace",
         "bsa_predict_mask_pooled_workspace", "bsa_predict_mask_pooled", "bsa_qkv_project_pooled",
-        "bsa_proj_residual", "bsa_copy_tokens",
+        "bsa_proj_residual", "bsa_copy_tokens", "bsa_kernel_times",
     ]
 
 

@@ -1115,13 +1115,27 @@ struct TcMaps {
 };
 
 // events bracketing the most recent timed attention-kernel launch (per thread)
+// a ring of TIMING_RING event pairs per thread: launch n records into slot
+// n % TIMING_RING, so a caller can time every launch of a loop without a
+// host sync inside it (bsa_kernel_times)
+constexpr int TIMING_RING = 64;
+struct TimingRing {
+  cudaEvent_t ev[TIMING_RING][2] = {};
+  int64_t count = 0;  // launches recorded since the last reset
+};
+static TimingRing& timing_ring() {
+  static thread_local TimingRing r;
+  return r;
+}
 cudaEvent_t timing_events(int which) {
-  static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
-  if (!ev[0]) {
-    cudaEventCreate(&ev[0]);
-    cudaEventCreate(&ev[1]);
+  TimingRing& r = timing_ring();
+  if (which == 0) ++r.count;  // a new launch opens the next slot
+  const int slot = (int)((r.count - 1 + TIMING_RING) % TIMING_RING);
+  if (!r.ev[slot][0]) {
+    cudaEventCreate(&r.ev[slot][0]);
+    cudaEventCreate(&r.ev[slot][1]);
   }
-  return ev[which];
+  return r.ev[slot][which];
 }
 
 template <int POLY, bool F16P, bool EXACT, bool X3 = false>
@@ -1240,9 +1254,25 @@ int launch_tc_attention(const AttnGeom& G, const TcArgs& a, cudaStream_t st,
 }  // namespace bsa
 
 extern "C" float bsa_last_kernel_ms(void) {
+  bsa::TimingRing& r = bsa::timing_ring();
+  if (r.count < 1) return -1.0f;
+  const int slot = (int)((r.count - 1) % bsa::TIMING_RING);
   float ms = -1.0f;
-  if (cudaEventSynchronize(bsa::timing_events(1)) != cudaSuccess) return -1.0f;
-  if (cudaEventElapsedTime(&ms, bsa::timing_events(0), bsa::timing_events(1)) != cudaSuccess)
-    return -1.0f;
+  if (cudaEventSynchronize(r.ev[slot][1]) != cudaSuccess) return -1.0f;
+  if (cudaEventElapsedTime(&ms, r.ev[slot][0], r.ev[slot][1]) != cudaSuccess) return -1.0f;
   return ms;
+}
+
+extern "C" int bsa_kernel_times(float* out, int32_t max_n, int32_t reset) {
+  bsa::TimingRing& r = bsa::timing_ring();
+  const int64_t avail = std::min<int64_t>(r.count, bsa::TIMING_RING);
+  const int n = (int)std::min<int64_t>(avail, max_n > 0 ? max_n : 0);
+  for (int i = 0; i < n; ++i) {  // the n most recent launches, oldest first
+    const int slot = (int)((r.count - n + i) % bsa::TIMING_RING);
+    if (cudaEventSynchronize(r.ev[slot][1]) != cudaSuccess ||
+        cudaEventElapsedTime(out + i, r.ev[slot][0], r.ev[slot][1]) != cudaSuccess)
+      return -1;
+  }
+  if (reset) r.count = 0;
+  return n;
 }

@@ -19,6 +19,7 @@ count.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import NamedTuple
 
@@ -131,6 +132,17 @@ def _check_out(out: torch.Tensor, q: torch.Tensor, out_dtype) -> None:
         raise ValueError(f"out is on {out.device}, inputs on {q.device}")
     if not out.is_contiguous():
         raise ValueError("out must be contiguous")
+
+
+def kernel_times(max_n: int = 64, reset: bool = True) -> list[float]:
+    """Device times (ms) of the most recent ``timing=True`` tensor-core
+    kernel launches on this thread, oldest first (up to 64, no host sync
+    needed between the launches); ``reset`` starts a new series."""
+    buf = (ctypes.c_float * max(1, max_n))()
+    n = N.lib().bsa_kernel_times(ctypes.cast(buf, ctypes.c_void_p), int(max_n), int(reset))
+    if n < 0:
+        raise RuntimeError("kernel_times: CUDA error reading the timing events")
+    return [float(buf[i]) for i in range(n)]
 
 
 def last_kernel_ms() -> float:
