@@ -208,6 +208,23 @@ def test_fused_stack_close_to_sparse_stack(bsa):
     assert rel < 2e-2, rel
 
 
+@pytest.mark.parametrize("S,specials_first", [(4, True), (5, False)])
+def test_fused_stack_other_layouts(bsa, S, specials_first):
+    """pi3-style 4 register tokens, and specials after the patches: the
+    fused stack (partitioned residual stream) still matches the sparse
+    stack within the bf16 tolerance."""
+    import torch
+    from paper_2509_07120_b200.stack import GlobalAttentionStack, policy_for
+    lay = bsa.TokenLayout(3, 1369, S, specials_first=specials_first)
+    st = GlobalAttentionStack(layers=2, heads=16, seed=3)
+    pol = policy_for(lay, 0.0, 0.75)
+    x = torch.randn((lay.total_tokens, 1024), generator=torch.Generator().manual_seed(8)).to(
+        "cuda", torch.bfloat16)
+    a = st.forward(x, lay, pol, mode="fused").float()
+    r = st.forward(x, lay, pol, mode="sparse").float()
+    assert ((a - r).norm() / r.norm()).item() < 2e-2
+
+
 def test_qkv_projection_rejects_bad_inputs(bsa):
     import torch
     lay, x, w, b = _inputs(1, 70, 0, 4, seed=0)
